@@ -1,0 +1,329 @@
+// ref_capi.cpp — extern "C" adapter over the unmodified reference tiletune
+// core. TEST INFRASTRUCTURE ONLY (see ref_capi.h). Every call goes through
+// the reference's own public headers (proj/core/include/tiletune/*.hpp).
+#include "ref_capi.h"
+
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tiletune/common.hpp"
+#include "tiletune/device.hpp"
+#include "tiletune/draft.hpp"
+#include "tiletune/features.hpp"
+#include "tiletune/momentum.hpp"
+#include "tiletune/oracle.hpp"
+#include "tiletune/ranker.hpp"
+#include "tiletune/schedule.hpp"
+#include "tiletune/workload.hpp"
+
+using namespace tiletune;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+std::string axis_name(const tt_op_spec& op, int a) {
+  return a < op.n_spatial ? "s" + std::to_string(a) : "r" + std::to_string(a - op.n_spatial);
+}
+
+TensorOpSpec to_op(const tt_op_spec& o) {
+  TensorOpSpec op;
+  op.name = "op";
+  for (int a = 0; a < o.n_spatial; ++a) op.spatial_axes.push_back({axis_name(o, a), o.extent[a]});
+  for (int r = 0; r < o.n_reduction; ++r)
+    op.reduction_axes.push_back({axis_name(o, o.n_spatial + r), o.extent[o.n_spatial + r]});
+  for (int b = 0; b < o.n_buffers; ++b) {
+    BufferSpec bs;
+    bs.name = "b" + std::to_string(b);
+    for (int q = 0; q < o.buffers[b].n_axes; ++q) bs.axes.push_back(axis_name(o, o.buffers[b].axes[q]));
+    bs.io = o.buffers[b].io == TT_IO_OUTPUT ? BufferIo::kOutput : BufferIo::kInput;
+    op.buffers.push_back(bs);
+  }
+  op.fused_elementwise = o.fused_elementwise;
+  op.kind = o.kind == TT_OP_ELEMENTWISE ? OpKind::kElementwise : OpKind::kTiled;
+  return op;
+}
+
+Sketch to_sketch(const tt_sketch& s) {
+  Sketch sk = generate_sketch(to_op(s.op), true);
+  sk.unroll_choices.assign(s.unroll, s.unroll + s.n_unroll);
+  return sk;
+}
+
+DeviceSpec to_dev(const tt_device_spec& d) {
+  DeviceSpec dev;
+  dev.m_l0 = d.m_l0, dev.m_l1 = d.m_l1, dev.pu_l1 = d.pu_l1, dev.n_l1 = d.n_l1;
+  dev.pu_l2 = d.pu_l2, dev.n_l2 = d.n_l2, dev.t_p = d.t_p, dev.t_m = d.t_m;
+  dev.element_bytes = d.element_bytes;
+  return dev;
+}
+
+Schedule get_sched(const tt_sketch& s, const int32_t* soa, int64_t ld, int64_t i) {
+  Schedule sc;
+  for (int a = 0; a < s.op.n_spatial; ++a) {
+    std::vector<int64_t> f(4);
+    for (int q = 0; q < 4; ++q) f[q] = soa[(int64_t)(4 * a + q) * ld + i];
+    sc.spatial_factors.push_back(f);
+  }
+  for (int r = 0; r < s.op.n_reduction; ++r) {
+    std::vector<int64_t> f(3);
+    for (int q = 0; q < 3; ++q) f[q] = soa[(int64_t)(4 * s.op.n_spatial + 3 * r + q) * ld + i];
+    sc.reduction_factors.push_back(f);
+  }
+  sc.unroll = soa[(int64_t)(tt_schedule_cols(&s) - 1) * ld + i];
+  return sc;
+}
+
+void put_sched(const tt_sketch& s, const Schedule& sc, int32_t* soa, int64_t ld, int64_t i) {
+  for (int a = 0; a < s.op.n_spatial; ++a)
+    for (int q = 0; q < 4; ++q) soa[(int64_t)(4 * a + q) * ld + i] = (int32_t)sc.spatial_factors[a][q];
+  for (int r = 0; r < s.op.n_reduction; ++r)
+    for (int q = 0; q < 3; ++q)
+      soa[(int64_t)(4 * s.op.n_spatial + 3 * r + q) * ld + i] = (int32_t)sc.reduction_factors[r][q];
+  soa[(int64_t)(tt_schedule_cols(&s) - 1) * ld + i] = (int32_t)sc.unroll;
+}
+
+void flatten(const RankerParams& p, double* out) {
+  for_each_tensor(p, [&](const std::string&, const Tensor& t) {
+    std::memcpy(out, t.v.data(), t.v.size() * sizeof(double));
+    out += t.v.size();
+  });
+}
+
+RankerParams unflatten(const double* in, int h) {
+  RngStream dummy(1);
+  RankerParams p = zeros_like(init_params(h, dummy));
+  for_each_tensor(p, [&](const std::string&, Tensor& t) {
+    std::memcpy(t.v.data(), in, t.v.size() * sizeof(double));
+    in += t.v.size();
+  });
+  return p;
+}
+
+HybridFeature make_feat(int S, int B, const double* stmt, const double* block) {
+  HybridFeature f;
+  f.statements.resize(S);
+  f.dataflow.resize(B);
+  for (int s = 0; s < S; ++s)
+    for (int q = 0; q < kStatementFeatureWidth; ++q) f.statements[s][q] = stmt[s * kStatementFeatureWidth + q];
+  for (int b = 0; b < B; ++b)
+    for (int q = 0; q < kDataflowFeatureWidth; ++q) f.dataflow[b][q] = block[b * kDataflowFeatureWidth + q];
+  return f;
+}
+
+double secs_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_random_init(const tt_sketch* sk, uint64_t seed, int64_t n, int32_t* soa, int64_t ld) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    RngStream rng(seed);
+    auto pop = random_init(s, n, rng);
+    for (int64_t i = 0; i < n; ++i) put_sched(*sk, pop[i], soa, ld, i);
+  });
+}
+
+int ref_draft_cost(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa,
+                   int64_t ld, int64_t n, int toggles, int threads, double* cost) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    DeviceSpec d = to_dev(*dev);
+    PenaltyToggles tg{(toggles & TT_TOGGLE_COMPUTE) != 0, (toggles & TT_TOGGLE_MEMORY) != 0};
+    std::vector<Schedule> pop(n);
+    for (int64_t i = 0; i < n; ++i) pop[i] = get_sched(*sk, soa, ld, i);
+    parallel_for(n, threads, [&](std::size_t i) { cost[i] = draft_cost(s, pop[i], d, tg).total; });
+  });
+}
+
+int ref_trace(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+              int64_t i, int64_t* symbols, double* penalties, double* stmt_cost, double* total) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    DeviceSpec d = to_dev(*dev);
+    Schedule sc = get_sched(*sk, soa, ld, i);
+    auto syms = extract_symbols(s, sc);
+    DraftCost c = draft_cost(s, sc, d);
+    for (std::size_t q = 0; q < syms.size(); ++q) {
+      const SymbolSet& y = syms[q].symbols;
+      int64_t v[8] = {y.s1, y.s2, y.s3, y.s4, y.s5, y.s6, y.s7, y.s8};
+      std::memcpy(symbols + 8 * q, v, sizeof(v));
+      PenaltySet p = compute_penalties(y, d);
+      double pv[7] = {p.p_l0_m, p.p_l0_c, p.p_l1_m, p.p_l1_c, p.alpha_l1, p.p_l2_c, p.p_l2_m};
+      std::memcpy(penalties + 7 * q, pv, sizeof(pv));
+      const auto& st = c.per_statement[q];
+      double cv[4] = {st.l_c, st.l_m, st.u_p, st.u_m};
+      std::memcpy(stmt_cost + 4 * q, cv, sizeof(cv));
+    }
+    *total = c.total;
+  });
+}
+
+int ref_explore(const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t k,
+                int64_t n, uint64_t seed, int threads, int32_t* soa_out, double* cost_out,
+                int64_t* count, uint64_t* evaluations) {
+  return guard([&] {
+    RngStream rng(seed);
+    ExploreResult r = explore(to_op(sk->op), to_dev(*dev), n_steps, (int)k, (int)n, rng, {}, threads);
+    *count = (int64_t)r.drafted.size();
+    *evaluations = r.evaluations;
+    for (std::size_t i = 0; i < r.drafted.size(); ++i) {
+      put_sched(*sk, r.drafted[i], soa_out, k, (int64_t)i);
+      cost_out[i] = r.draft_costs[i];
+    }
+  });
+}
+
+int ref_features(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+                 const int64_t* idx, int64_t k, double* stmt_out, double* block_out) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    DeviceSpec d = to_dev(*dev);
+    int S = tt_n_statements(&sk->op), B = tt_n_blocks(&sk->op);
+    for (int64_t q = 0; q < k; ++q) {
+      HybridFeature f = extract_features(s, get_sched(*sk, soa, ld, idx[q]), d);
+      for (int st = 0; st < S; ++st)
+        std::memcpy(stmt_out + (q * S + st) * TT_STMT_WIDTH, f.statements[st].data(), sizeof(double) * TT_STMT_WIDTH);
+      for (int b = 0; b < B; ++b)
+        std::memcpy(block_out + (q * B + b) * TT_BLOCK_WIDTH, f.dataflow[b].data(), sizeof(double) * TT_BLOCK_WIDTH);
+    }
+  });
+}
+
+int ref_init_params(int h, uint64_t seed, double* params) {
+  return guard([&] {
+    RngStream rng(seed);
+    flatten(init_params(h, rng), params);
+  });
+}
+
+int ref_score_batch(const double* params, int h, int n_stmt, int n_block, const double* stmt,
+                    const double* block, int64_t k, int attention_identity, int threads,
+                    double* out, uint64_t* forward_calls_delta) {
+  return guard([&] {
+    RankerParams p = unflatten(params, h);
+    std::vector<HybridFeature> feats(k);
+    for (int64_t q = 0; q < k; ++q)
+      feats[q] = make_feat(n_stmt, n_block, stmt + q * n_stmt * TT_STMT_WIDTH, block + q * n_block * TT_BLOCK_WIDTH);
+    ScoreOptions o;
+    o.attention_identity = attention_identity != 0;
+    uint64_t before = forward_calls();
+    auto s = score_batch(p, feats, o, threads);
+    if (forward_calls_delta) *forward_calls_delta = forward_calls() - before;
+    std::memcpy(out, s.data(), sizeof(double) * k);
+  });
+}
+
+int ref_select_top(const double* scores, const double* drafts, const uint8_t* excluded,
+                   int64_t n, int64_t b, int64_t* idx_out) {
+  return guard([&] {
+    std::vector<double> s(scores, scores + n), d(drafts, drafts + n);
+    std::vector<char> e(n, 0);
+    if (excluded)
+      for (int64_t i = 0; i < n; ++i) e[i] = excluded[i] ? 1 : 0;
+    auto r = select_top(s, d, e, (std::size_t)b);
+    for (int64_t i = 0; i < b; ++i) idx_out[i] = (int64_t)r[i];
+  });
+}
+
+int ref_momentum_update(double* phi, const double* target, int h, double m) {
+  return guard([&] {
+    SiameseState st;
+    st.params = unflatten(phi, h);
+    st.momentum = m;
+    SiameseState next = momentum_update(st, unflatten(target, h));
+    flatten(next.params, phi);
+  });
+}
+
+int ref_train(double* params, int h, int n_stmt, int n_block, const double* stmt,
+              const double* block, const double* latencies, int64_t k, int epochs, double lr,
+              int batch, uint64_t seed, double* initial_loss, double* final_loss) {
+  return guard([&] {
+    RankerParams p = unflatten(params, h);
+    TaskSamples ts;
+    ts.task = "op";
+    for (int64_t q = 0; q < k; ++q) {
+      ts.features.push_back(make_feat(n_stmt, n_block, stmt + q * n_stmt * TT_STMT_WIDTH, block + q * n_block * TT_BLOCK_WIDTH));
+      ts.latencies.push_back(latencies[q]);
+    }
+    TrainConfig cfg;
+    cfg.epochs = epochs, cfg.lr = lr, cfg.batch = batch, cfg.seed = seed;
+    TrainReport r = train(p, {ts}, cfg);
+    if (initial_loss) *initial_loss = r.initial_loss;
+    if (final_loss) *final_loss = r.final_loss;
+    flatten(p, params);
+  });
+}
+
+int ref_noiseless_latency(const tt_sketch* sk, const tt_device_spec* hidden, double stride_coeff,
+                          double occupancy_coeff, double launch_overhead_s, const int32_t* soa,
+                          int64_t ld, int64_t n, double* out) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    OracleDevice o;
+    o.hidden = to_dev(*hidden);
+    o.stride_coeff = stride_coeff;
+    o.occupancy_coeff = occupancy_coeff;
+    o.launch_overhead_s = launch_overhead_s;
+    for (int64_t i = 0; i < n; ++i) out[i] = noiseless_latency(s, get_sched(*sk, soa, ld, i), o);
+  });
+}
+
+int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t k, int64_t b,
+              uint64_t seed, const double* params, int h, int threads, int64_t* sel_idx,
+              double* sel_scores, int32_t* drafted_soa, double* drafted_cost,
+              int64_t* drafted_count, double* seconds) {
+  return guard([&] {
+    TensorOpSpec op = to_op(sk->op);
+    DeviceSpec d = to_dev(*dev);
+    RankerParams p = unflatten(params, h);
+    auto t0 = std::chrono::steady_clock::now();
+    RngStream rng(seed);
+    ExploreResult ex = explore(op, d, 1, (int)k, (int)n, rng, {}, threads);  // draft.cpp:156-221
+    seconds[0] = secs_since(t0);
+    auto t1 = std::chrono::steady_clock::now();
+    std::vector<HybridFeature> feats(ex.drafted.size());
+    parallel_for(feats.size(), threads, [&](std::size_t i) {  // tuner.cpp:366-369
+      feats[i] = extract_features(ex.sketch, ex.drafted[i], d);
+    });
+    seconds[1] = secs_since(t1);
+    auto t2 = std::chrono::steady_clock::now();
+    std::vector<double> scores = score_batch(p, feats, {}, threads);  // ranker.cpp:375-381
+    seconds[2] = secs_since(t2);
+    auto t3 = std::chrono::steady_clock::now();
+    std::vector<char> excluded(scores.size(), 0);
+    auto sel = select_top(scores, ex.draft_costs, excluded, (std::size_t)b);  // ranker.cpp:514-532
+    seconds[3] = secs_since(t3);
+    for (int64_t i = 0; i < b; ++i) {
+      sel_idx[i] = (int64_t)sel[i];
+      if (sel_scores) sel_scores[i] = scores[sel[i]];
+    }
+    *drafted_count = (int64_t)ex.drafted.size();
+    if (drafted_soa)
+      for (std::size_t i = 0; i < ex.drafted.size(); ++i) put_sched(*sk, ex.drafted[i], drafted_soa, k, (int64_t)i);
+    if (drafted_cost)
+      for (std::size_t i = 0; i < ex.drafted.size(); ++i) drafted_cost[i] = ex.draft_costs[i];
+  });
+}
+
+}  // extern "C"

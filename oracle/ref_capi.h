@@ -1,0 +1,60 @@
+/*
+ * ref_capi.h — extern "C" wrapper over the UNMODIFIED reference tiletune core
+ * (compiled from /root/reference/proj/core/src by oracle/Makefile into
+ * oracle/_ref/). TEST INFRASTRUCTURE ONLY: used to pin the oracle
+ * (tests/golden), and as bench.py's `--impl reference` arm, which times the
+ * reference's own public API on the host cores.
+ */
+#ifndef TT_REF_CAPI_H_
+#define TT_REF_CAPI_H_
+#include <stdint.h>
+
+#include "../include/tt/tt_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* every function returns 0 on success, -1 on a tiletune::Error (message via
+ * ref_last_error) */
+const char* ref_last_error(void);
+int ref_random_init(const tt_sketch* sk, uint64_t seed, int64_t n, int32_t* soa, int64_t ld);
+int ref_draft_cost(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa,
+                   int64_t ld, int64_t n, int toggles, int threads, double* cost);
+int ref_trace(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+              int64_t i, int64_t* symbols, double* penalties, double* stmt_cost, double* total);
+/* explore(op, dev, n_steps, K, N, RngStream(seed), toggles, threads): writes
+ * the drafted schedules (SoA, ld = K) and costs; returns the count in *count */
+int ref_explore(const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t k,
+                int64_t n, uint64_t seed, int threads, int32_t* soa_out, double* cost_out,
+                int64_t* count, uint64_t* evaluations);
+int ref_features(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+                 const int64_t* idx, int64_t k, double* stmt_out, double* block_out);
+int ref_init_params(int h, uint64_t seed, double* params);
+int ref_score_batch(const double* params, int h, int n_stmt, int n_block, const double* stmt,
+                    const double* block, int64_t k, int attention_identity, int threads,
+                    double* out, uint64_t* forward_calls);
+int ref_select_top(const double* scores, const double* drafts, const uint8_t* excluded,
+                   int64_t n, int64_t b, int64_t* idx_out);
+int ref_momentum_update(double* phi, const double* target, int h, double m);
+/* train(params, {one task}, cfg) with labels given (ranker.cpp:459-512) */
+int ref_train(double* params, int h, int n_stmt, int n_block, const double* stmt,
+              const double* block, const double* latencies, int64_t k, int epochs, double lr,
+              int batch, uint64_t seed, double* initial_loss, double* final_loss);
+int ref_noiseless_latency(const tt_sketch* sk, const tt_device_spec* hidden, double stride_coeff,
+                          double occupancy_coeff, double launch_overhead_s, const int32_t* soa,
+                          int64_t ld, int64_t n, double* out);
+
+/* The reference-API draft+verify round of SURVEY.md §3.2, timed inside:
+ * explore(n_steps=1) -> extract_features x K -> score_batch -> select_top.
+ * Writes the selected b schedules' ranks into sel_idx (positions within the
+ * drafted list) and wall seconds per stage into seconds[4]. */
+int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t k, int64_t b,
+              uint64_t seed, const double* params, int h, int threads, int64_t* sel_idx,
+              double* sel_scores, int32_t* drafted_soa, double* drafted_cost,
+              int64_t* drafted_count, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
