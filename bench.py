@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Draft+verify round throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the metric's 1-GPU configuration): the
+seven ResNet-50 conv2d subgraphs, 65,536 random candidates per subgraph
+round per GPU -> SA draft -> dedup top-512 -> PaCM verify (h = 64,
+random-init weights) -> select b = 10. One step = one round on each of the
+seven subgraphs. For N > 1 every rank drafts its own 65,536 candidates of
+the same counter-based population (weak scaling); the per-rank top-512
+lists (cost, global index, identity) are merged after one NCCL all-gather
+and verified on every rank.
+
+value: candidates scored / s with the population already resident in HBM.
+e2e:   the same through the public API from host memory: every round copies
+       its population (int32 SoA) and the PaCM weights host->device from
+       pinned memory and reads the selection back.
+Only rank 0 prints the JSON line. `--impl reference` times the unmodified
+reference (oracle/_ref, compiled from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidates scored/sec per draft+verify round (1/2/4/8 B200) vs host-CPU ref"
+UNIT = "candidates/s"
+R50 = ["r50_stem", "r50_c1x1_64", "r50_c3x3_64", "r50_c1x1_256", "r50_c3x3_128", "r50_c3x3_256", "r50_c3x3_512"]
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.path = gpu, None, None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 7 and f[0].replace(".", "").isdigit():
+                    rows.append(f)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------------------- ours --
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+
+    torch.cuda.set_device(local_rank)
+    dev = reference_device()
+    ctx = tt.Context(local_rank)
+    n, k, b, seed = args.n, args.k, args.b, args.seed
+    prec = tt.TT_PREC_BF16 if args.precision == "bf16" else tt.TT_PREC_FP64
+    names = R50 if args.workload == "r50" else [args.workload]
+    sketches = [make_sketch(WORKLOADS[w]()) for w in names]
+    first = rank * n
+    # inputs: each subgraph's population shard, resident in HBM, + pinned host copies for e2e
+    pops = [tt.random_init(ctx, sk, n, seed, first=first) for sk in sketches]
+    pops_host = [p.cpu().pin_memory() for p in pops]
+    params = tt.init_params(64, derive_seed(seed, TAG_INIT))
+    params_host = torch.from_numpy(params).pin_memory()
+    model = tt.PaCM(ctx, params_host, 64)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    gather_out = torch.empty((3, k), dtype=torch.int64, device="cuda")
+    gathered = torch.empty((world * 3 * k,), dtype=torch.int64, device="cuda")
+
+    def one_round(sk, soa):
+        if world == 1:
+            tt.round_async(ctx, sk, dev, n, k, b, soa=soa, precision=prec, band=args.band, first=first)
+        else:
+            tt.round_local_async(ctx, sk, dev, n, k, b, first, gather_out, soa=soa)
+            dist.all_gather_into_tensor(gathered, gather_out.reshape(-1))
+            tt.round_finish_merged_async(ctx, sk, dev, gathered, n * world, k, b, precision=prec, band=args.band)
+
+    def step_value():
+        for sk, soa in zip(sketches, pops):
+            one_round(sk, soa)
+
+    # warm-up + correctness gate: every subgraph's round must collect cleanly
+    for _ in range(args.warmup):
+        for sk, soa in zip(sketches, pops):
+            one_round(sk, soa)
+            out = tt.round_collect(ctx, b)
+            assert out.selected == b and out.status == 0, out
+    torch.cuda.synchronize()
+
+    def timed(step_fn, profile=False):
+        if profile:
+            tt.profile_enable(ctx, True)
+            tt.profile_read(ctx)
+        times = []
+        launches0 = tt.kernel_launches()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations, outside the events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step_fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = tt.kernel_launches() - launches0
+        prof = tt.profile_read(ctx) if profile else None
+        if profile:
+            tt.profile_enable(ctx, False)
+        return times, launches, prof
+
+    # ---- value: population resident in HBM
+    with ClockSampler(local_rank) as clk:
+        times, launches, _ = timed(step_value)
+    clocks = clk.summary()
+    out = tt.round_collect(ctx, b)  # last round of the last step
+    assert out.selected == b and out.status == 0
+
+    # ---- stage breakdown (separate pass, events per stage on the ctx stream)
+    ptimes, _, prof = timed(step_value, profile=True)
+    tt.round_collect(ctx, b)
+
+    # ---- e2e through the public API from host memory
+    def step_e2e():
+        for sk, soa, host in zip(sketches, pops, pops_host):
+            soa.copy_(host, non_blocking=True)      # H2D population (pinned)
+            model.load(params_host)                 # H2D PaCM weights (pinned, async)
+            if world == 1:
+                tt.draft_verify_round(ctx, sk, dev, n, k, b, soa=soa, precision=prec, band=args.band, first=first)
+            else:
+                one_round(sk, soa)
+                tt.round_collect(ctx, b)
+    etimes, elaunch, _ = timed(step_e2e)
+    h2d = sum(p.numel() * 4 for p in pops_host) + params_host.numel() * 8 * len(sketches)
+    d2h = len(sketches) * 8 * (4 + 4 * b)
+
+    # ---- e2e, seeded API (explore(seed) semantics: population drawn inside the call)
+    def step_seeded():
+        for sk in sketches:
+            model.load(params_host)
+            if world == 1:
+                tt.draft_verify_round(ctx, sk, dev, n, k, b, seed=seed, precision=prec, band=args.band, first=first)
+            else:
+                one_round(sk, None)
+                tt.round_collect(ctx, b)
+    stimes, _, _ = timed(step_seeded)
+
+    def agg(ts):
+        t = torch.tensor([sum(ts)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / 1e3  # seconds over all steps (max over ranks)
+
+    tot, etot, stot = agg(times), agg(etimes), agg(stimes)
+    cands = n * world * len(sketches) * args.steps
+    result = None
+    if rank == 0:
+        peaks, peaks_kind = load_peaks()
+        rounds = len(sketches) * args.steps
+        stage_ms = {s: v[0] / max(v[1], 1) for s, v in (prof or {}).items()}
+        roof = roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec)
+        cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+        result = {
+            "metric": METRIC, "value": cands / tot, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if prec == tt.TT_PREC_FP64 else "bf16+f64",
+            "data": "synthetic: random_init(seed=%d) populations, init_params(64) weights" % seed,
+            "config": {"workload": f"{args.workload}: {len(sketches)} subgraph rounds/step, N={n}/GPU/round, "
+                                   f"K={k}, b={b}, h=64, precision={args.precision}",
+                       "subgraphs": names, "n_per_gpu": n, "k": k, "b": b,
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "parallelism": f"dp{world} (population sharded, NCCL all-gather top-K merge)"},
+            "e2e": {"value": cands / etot, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "tt_round via paper_2402_02361_b200.tiletune.draft_verify_round, population + "
+                           "weights from pinned host memory"},
+            "e2e_seeded": {"value": cands / stot, "unit": UNIT,
+                           "h2d_bytes_per_step": params_host.numel() * 8 * len(sketches), "d2h_bytes_per_step": d2h,
+                           "api": "explore(seed) semantics: population drawn on device inside the call"},
+            "gpu_launches": launches,
+            "stage_ms_per_round": stage_ms,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+    return result
+
+
+def roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec):
+    """Roofline of the dominant stage, from the live per-stage event timings."""
+    if not stage_ms:
+        return None
+    dom = max(stage_ms, key=stage_ms.get)
+    if dom == "select":
+        # SA draft + top-K: algorithmic bytes = factor columns read + cost
+        # write + cost re-reads (compaction); SURVEY §8d per-candidate
+        per = [4 * (4 * sk.op.n_spatial + 3 * sk.op.n_reduction) + 8 + 8 for sk in sketches]
+        byts = args.n * sum(per) / len(per)
+        ach = byts / (stage_ms[dom] * 1e-3) / 1e9
+        peak = peaks["hbm_gbs"]
+        return {"bound": "hbm", "kernel": "draft select (K1 cost+hist, K2 scan/compact/finalize)",
+                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "peak_source": peaks_kind, "stage_ms": stage_ms[dom]}
+    flops = args.k * 320640.0
+    ach = flops / (stage_ms[dom] * 1e-3) / 1e12
+    peak = peaks["bf16_tflops"]
+    return {"bound": "tensor", "kernel": f"PaCM verify ({'tcgen05 bf16' if prec else 'fp64 CUDA cores'})",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+            "peak_source": peaks_kind + " bf16 dense (burst)", "stage_ms": stage_ms[dom],
+            "flop_per_candidate": 320640}
+
+
+# ------------------------------------------------------------------------------------ reference --
+
+def _ref_setup(args):
+    from tests import _refs as R  # checker loader: oracle/_ref (the reference compiled here)
+    return R
+
+
+def cpu_baseline(args, budget_s=20.0):
+    """The reference's own round (oracle/_ref) on the host cores, on a
+    bounded sample of the workload: whole subgraph rounds until budget_s."""
+    R = _ref_setup(args)
+    if not R.ref_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref missing"}
+    threads = os.cpu_count() or 1
+    done, secs, rounds = 0, 0.0, 0
+    t_end = time.time() + budget_s
+    names = R50 if args.workload == "r50" else [args.workload]
+    while time.time() < t_end and rounds < 64:
+        w = names[rounds % len(names)]
+        s, _ = ref_round(R, w, args.n, args.k, args.b, args.seed + rounds, threads)
+        secs += s
+        done += args.n
+        rounds += 1
+    return {"value": done / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{rounds} reference rounds (explore(n_steps=1)+extract_features+score_batch+select_top, "
+                      f"threads={threads}) over {names[:rounds]}... N={args.n}, K={args.k}"}
+
+
+def ref_round(R, workload, n, k, b, seed, threads):
+    import ctypes as C
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    sk = make_sketch(WORKLOADS[workload]())
+    dev = reference_device()
+    params = R.R_init_params(64, derive_seed(seed, TAG_INIT))
+    sel = np.zeros(b, np.int64)
+    sc = np.zeros(b)
+    cnt = C.c_int64(0)
+    secs = np.zeros(4)
+    R.check(R.ref().ref_round(C.byref(sk), C.byref(dev), n, k, b, seed, R.ptr(params, R.f64p), 64, threads,
+                              R.ptr(sel, R.i64p), R.ptr(sc, R.f64p), None, None, C.byref(cnt), R.ptr(secs, R.f64p)))
+    return float(secs.sum()), secs
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    R = _ref_setup(args)
+    if not R.ref_available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libtiletune_ref.so not built (make -C oracle ref)"}
+    threads = os.cpu_count() or 1
+    names = R50 if args.workload == "r50" else [args.workload]
+    # bounded sample per step: ref_rounds_per_step subgraph rounds
+    per_step = min(len(names), args.ref_rounds_per_step)
+    for i in range(args.warmup):
+        ref_round(R, names[i % len(names)], args.n, args.k, args.b, args.seed, threads)
+    tot, stage = 0.0, np.zeros(4)
+    for s in range(args.steps):
+        for r in range(per_step):
+            t, st = ref_round(R, names[(s * per_step + r) % len(names)], args.n, args.k, args.b, args.seed, threads)
+            tot += t
+            stage += st
+    cands = args.n * per_step * args.steps
+    v = cands / tot
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: N={args.n}/round, K={args.k}, b={args.b}, h=64",
+                       "rounds_per_step": per_step, "subgraphs": names},
+            "stage_s_per_round": {"explore": stage[0] / (per_step * args.steps),
+                                  "features": stage[1] / (per_step * args.steps),
+                                  "score_batch": stage[2] / (per_step * args.steps),
+                                  "select_top": stage[3] / (per_step * args.steps)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{per_step} subgraph round(s) per step of the reference API"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="r50")
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--k", type=int, default=512)
+    ap.add_argument("--b", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "bf16"])
+    ap.add_argument("--band", type=float, default=0.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-rounds-per-step", type=int, default=1)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        res = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if rank == 0 and res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

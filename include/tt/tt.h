@@ -1,0 +1,221 @@
+/*
+ * tt.h — the drop-in C ABI of the B200 draft+verify exploration round.
+ *
+ * Every entry point is extern "C", takes plain pointers and sizes, and
+ * returns an int status (TT_OK = 0). The error codes mirror tiletune::Error
+ * codes (proj/core/include/tiletune/common.hpp:44-50) plus TT_E_CUDA; the
+ * message of the last failure on a context is tt_last_error(ctx). Each
+ * function names the reference interface it replaces.
+ *
+ * Memory: arguments named *_dev are device pointers, *_host host pointers;
+ * everything is caller-owned. A context owns one CUDA stream (or adopts the
+ * caller's via tt_ctx_set_stream) plus its scratch; calls on one context are
+ * serialised on its stream, distinct contexts are independent. Functions
+ * documented "async" only enqueue work on the stream.
+ *
+ * There is no CPU fallback: every compute entry point launches sm_100a
+ * kernels and fails with TT_E_CUDA when no device is usable.
+ */
+#ifndef TT_TT_H_
+#define TT_TT_H_
+
+#include <stdint.h>
+
+#include "tt_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum tt_status {
+  TT_OK = 0,
+  TT_E_PARSE = 1,    /* tiletune::err::kParse */
+  TT_E_VALIDATE = 2, /* tiletune::err::kValidate */
+  TT_E_CONFIG = 3,   /* tiletune::err::kConfig */
+  TT_E_STATE = 4,    /* tiletune::err::kState */
+  TT_E_IO = 5,       /* tiletune::err::kIo */
+  TT_E_CUDA = 6,     /* device / launch failure */
+  TT_E_NCCL = 7      /* collective failure (reserved; collectives run in the host orchestrator) */
+};
+
+/* PaCM arithmetic for tt_pacm_score / tt_round */
+enum tt_precision {
+  TT_PREC_FP64 = 0, /* CUDA-core fp64, reference accumulation order (parity mode) */
+  TT_PREC_BF16 = 1  /* tcgen05 tensor cores, bf16 operands, fp32 TMEM accumulators */
+};
+
+typedef struct tt_ctx tt_ctx;
+
+/* "E_VALIDATE" etc. — the reference's stable code strings */
+const char* tt_status_code(int status);
+const char* tt_version(void);
+/* Number of CUDA kernels this library has launched (process-wide). */
+uint64_t tt_kernel_launches(void);
+
+/* ------------------------------------------------------------ context -- */
+int tt_ctx_create(int device, tt_ctx** out);
+void tt_ctx_destroy(tt_ctx* ctx);
+const char* tt_last_error(const tt_ctx* ctx);
+int tt_ctx_set_stream(tt_ctx* ctx, void* cuda_stream); /* NULL restores the ctx stream */
+void* tt_ctx_stream(const tt_ctx* ctx);
+int tt_ctx_sync(tt_ctx* ctx);
+
+/* ------------------------------------------------ problem model (host) -- */
+/* generate_sketch(op, elementwise_fallback) (schedule.cpp:150-164) incl.
+ * validate_op (workload.cpp:49-93); unroll choices {1,4,16}. */
+int tt_sketch_from_op(const tt_op_spec* op, int elementwise_fallback, tt_sketch* out);
+/* validate_device (device.cpp:105-122) */
+int tt_validate_device(const tt_device_spec* dev);
+/* space_size (schedule.cpp:188-195), saturating */
+uint64_t tt_space_size(const tt_sketch* sketch);
+/* RNG draws random_init consumes per schedule (one per (axis, prime) + 1) */
+int tt_draws_per_schedule(const tt_sketch* sketch);
+
+/* ------------------------------------------------ K0 population (async) -- */
+/* random_init(sketch, n, RngStream(seed)) (schedule.cpp:166-186), schedules
+ * [first, first + n) of the stream, written as SoA columns (tt_types.h).
+ * identity_dev (nullable) receives each schedule's exact 64-bit identity. */
+int tt_population_generate(tt_ctx* ctx, const tt_sketch* sketch, uint64_t seed, int64_t first, int64_t n,
+                           int32_t* soa_dev, int64_t ld, uint64_t* identity_dev);
+/* Exact identity <-> schedule (the replacement for schedule_key /
+ * schedule_from_key identity, schedule.cpp:280-338). Requires
+ * tt_space_size < 2^64. */
+int tt_schedule_identity(tt_ctx* ctx, const tt_sketch* sketch, const int32_t* soa_dev, int64_t ld, int64_t n,
+                         uint64_t* identity_dev);
+int tt_schedule_from_identity(tt_ctx* ctx, const tt_sketch* sketch, const uint64_t* identity_dev, int64_t n,
+                              int32_t* soa_dev, int64_t ld);
+
+/* ---------------------------------------------------- K1 SA draft cost -- */
+/* draft_cost(sketch, sched, device, toggles).total (draft.cpp:129-154) for n
+ * schedules; bit-exact fp64. Synchronous: TT_E_VALIDATE if any schedule
+ * fails validate_schedule (schedule.cpp:242-278), as the reference throws. */
+int tt_draft_cost(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const int32_t* soa_dev,
+                  int64_t ld, int64_t n, int toggles, double* cost_dev);
+
+/* --------------------------------------------- K2 PriorFilter (top-K) -- */
+/* explore(op, dev, n_steps = 1, draft_size = k, ...) semantics
+ * (draft.cpp:156-221): the k lowest UNIQUE schedules by (cost, first index),
+ * ascending. Population given explicitly. Outputs: population index
+ * (+ index_base), cost, identity; *count_host = min(k, unique). Synchronous. */
+int tt_draft_topk(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const int32_t* soa_dev,
+                  int64_t ld, int64_t n, int64_t k, int toggles, int64_t index_base, int64_t* idx_dev,
+                  double* cost_dev, uint64_t* identity_dev, int64_t* count_host);
+/* The same over the counter-based population random_init(., RngStream(seed))
+ * restricted to schedules [first, first + n): K0+K1+K2 fused, the
+ * population is never materialised. This is explore(n_steps = 1). */
+int tt_explore1(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, uint64_t seed, int64_t first,
+                int64_t n, int64_t k, int toggles, int64_t* idx_dev, double* cost_dev, uint64_t* identity_dev,
+                int64_t* count_host);
+/* Merge R rank-local top-k lists (C1's consumer): m entries of (cost,
+ * global index, identity), global index < 0 = empty slot. Same semantics as
+ * one explore over the union. Synchronous. */
+int tt_topk_merge(tt_ctx* ctx, const double* cost_dev, const int64_t* gidx_dev, const uint64_t* identity_dev,
+                  int64_t m, int64_t k, int64_t* idx_dev, double* out_cost_dev, uint64_t* out_identity_dev,
+                  int64_t* count_host);
+
+/* ------------------------------------------------- features & PaCM -- */
+/* extract_features (features.cpp:98-257), fp64: stmt [k][S][24], block
+ * [k][B][23] with S = tt_n_statements, B = tt_n_blocks. Async. */
+int tt_features(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const uint64_t* identity_dev,
+                int64_t k, double* stmt_dev, double* block_dev);
+int tt_features_soa(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const int32_t* soa_dev,
+                    int64_t ld, const int64_t* idx_dev, int64_t k, double* stmt_dev, double* block_dev);
+/* Load RankerParams (ranker.hpp:48-58) flattened in for_each_tensor order
+ * (tt_types.h) from host or device memory; hidden width h. */
+int tt_pacm_load(tt_ctx* ctx, const double* params, int h);
+/* score() for k drafted candidates given by identity (ranker.cpp:370-373);
+ * advances tt_forward_calls by k. Async. */
+int tt_pacm_score(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const uint64_t* identity_dev,
+                  int64_t k, int precision, double* score_dev);
+/* score_batch(params, feats, opts) on given features (ranker.cpp:375-381). */
+int tt_pacm_score_features(tt_ctx* ctx, const double* stmt_dev, const double* block_dev, int n_stmt, int n_block,
+                           int64_t k, int attention_identity, double* score_dev);
+/* forward_calls / reset_forward_calls (ranker.hpp:88-90), process-wide */
+uint64_t tt_forward_calls(void);
+void tt_reset_forward_calls(void);
+
+/* ----------------------------------------------------- K2b select_top -- */
+/* select_top (ranker.cpp:514-532): b best by (score desc, draft asc, index
+ * asc), excluded (nullable, 1 = excluded) never chosen. Synchronous;
+ * TT_E_STATE "requested b but only m unmeasured candidates available". */
+int tt_select_top(tt_ctx* ctx, const double* scores_dev, const double* drafts_dev, const uint8_t* excluded_dev,
+                  int64_t n, int64_t b, int64_t* idx_host);
+
+/* ------------------------------------------------------------- K4 MoA -- */
+/* train's GD update p -= lr * g (ranker.cpp:502-506). Async. */
+int tt_gd_step(tt_ctx* ctx, double* params_dev, const double* grads_dev, int64_t n, double lr);
+/* momentum_update phi' = t + m (phi - t) (momentum.cpp:28-46); TT_E_STATE
+ * unless 0 <= m < 1. Async. */
+int tt_momentum_update(tt_ctx* ctx, double* phi_dev, const double* target_dev, int64_t n, double m);
+
+/* ------------------------------------------------------------- round -- */
+typedef struct tt_round_config {
+  int64_t n;          /* candidates drafted this round (this rank's shard) */
+  int64_t k;          /* draft_size handed to PaCM (tuner.hpp:38, 512) */
+  int64_t b;          /* measurement batch (tuner.hpp:37, 10) */
+  int32_t toggles;    /* TT_TOGGLES_ALL */
+  int32_t precision;  /* tt_precision */
+  double band;        /* TT_PREC_BF16: certified |score error| bound */
+  int64_t first;      /* seeded source: first schedule index of the shard */
+} tt_round_config;
+
+typedef struct tt_round_result {
+  int64_t selected; /* min(b, drafted) */
+  int64_t drafted;  /* unique drafted candidates (<= k) */
+  int64_t rescored; /* fp64-rescored candidates (certification band) */
+  int32_t status;   /* internal selector flags, 0 when clean */
+  int32_t _pad;
+} tt_round_result;
+
+/* One draft+verify round (tuner.cpp:361-396 minus the measurement):
+ * SA draft over n candidates -> dedup top-k -> features + PaCM over the
+ * drafted set -> select_top(b). The population is soa_dev (explicit, may be
+ * NULL) or the counter-based random_init stream of `seed`. Requires
+ * tt_pacm_load. Outputs b entries (host): population index, score, draft
+ * cost, identity. Synchronous (one small device->host copy at the end). */
+int tt_round(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
+             const int32_t* soa_dev, int64_t ld, uint64_t seed, int64_t* sel_index_host, double* sel_score_host,
+             double* sel_cost_host, uint64_t* sel_identity_host, tt_round_result* result_host);
+/* Async variant: enqueue only; results land in the context and are read
+ * with tt_round_collect (which synchronises). */
+int tt_round_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
+                   const int32_t* soa_dev, int64_t ld, uint64_t seed);
+int tt_round_collect(tt_ctx* ctx, int64_t* sel_index_host, double* sel_score_host, double* sel_cost_host,
+                     uint64_t* sel_identity_host, tt_round_result* result_host);
+
+/* Sharded round, draft half (async): this rank's K-entry list of (cost,
+ * global index, identity) for the all-gather; unused slots get index -1.
+ * cfg->first = global index of this shard's first candidate. */
+int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
+                         const tt_round_config* cfg, const int32_t* soa_dev, int64_t ld, uint64_t seed,
+                         double* cost_dev, int64_t* gidx_dev, uint64_t* identity_dev);
+/* Sharded round, verify half, async: merge + features + PaCM + select;
+ * read with tt_round_collect. */
+int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
+                                 const tt_round_config* cfg, const double* cost_dev, const int64_t* gidx_dev,
+                                 const uint64_t* identity_dev, int64_t m);
+/* Stage timing with CUDA events on the context stream (0 draft select,
+ * 1 PaCM, 2 certification rescoring, 3 select_top + gather, 4 merge).
+ * tt_profile_read synchronises, returns per-stage summed ms and counts
+ * since the last read. */
+int tt_profile_enable(tt_ctx* ctx, int on);
+int tt_profile_read(tt_ctx* ctx, double* ms_sum, int64_t* count, int n_stages);
+
+/* Sharded round, verify half: after the all-gather of every rank's local
+ * top-k (cost, global index, identity) lists, merge them and finish the
+ * round (features -> PaCM -> select_top) on identical data on every rank. */
+int tt_round_finish_merged(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
+                           const tt_round_config* cfg, const double* cost_dev, const int64_t* gidx_dev,
+                           const uint64_t* identity_dev, int64_t m, int64_t* sel_index_host,
+                           double* sel_score_host, double* sel_cost_host, uint64_t* sel_identity_host,
+                           tt_round_result* result_host);
+
+/* Device views of the last round's drafted set (valid until the next round). */
+int tt_round_drafted(const tt_ctx* ctx, const int64_t** idx_dev, const double** cost_dev,
+                     const uint64_t** identity_dev, const double** score_dev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TT_TT_H_ */

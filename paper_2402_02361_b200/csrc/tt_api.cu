@@ -1,0 +1,1005 @@
+// tt_api.cu — the C ABI of include/tt/tt.h: context, validation, plan
+// compilation (tt_sketch -> DevSketch) and the round orchestration.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tt/tt.h"
+#include "tt_kernels.h"
+
+using namespace tt;
+
+struct tt_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  SelScratch sel;
+  // drafted set of the current round
+  int64_t k_cap = 0;
+  int64_t* d_idx = nullptr;
+  double* d_cost = nullptr;
+  uint64_t* d_id = nullptr;
+  double* d_score = nullptr;
+  double* d_score_fast = nullptr;
+  int64_t* d_count = nullptr;
+  uint8_t* d_excluded = nullptr;
+  int32_t* d_sublist = nullptr;
+  int* d_sublist_count = nullptr;
+  // selection
+  int64_t b_cap = 0;
+  int64_t* d_pos = nullptr;
+  int64_t* d_pos_count = nullptr;
+  int64_t* d_pos_fast = nullptr;
+  int64_t* d_pos_fast_count = nullptr;
+  int* d_status = nullptr;
+  int64_t* d_record = nullptr;
+  int64_t* h_record = nullptr;  // pinned
+  // PaCM params
+  double* d_params = nullptr;
+  int h = 0;
+  int64_t n_params = 0;
+  void* d_packed = nullptr;
+  bool packed_ok = false;
+  // merge inputs
+  int64_t m_cap = 0;
+  // last async round
+  int64_t last_b = 0;
+  int64_t last_k = 0;
+  bool pending = false;
+  tt_round_config last_cfg{};
+  tt_sketch last_sketch{};
+  tt_device_spec last_dev{};
+  const int32_t* last_soa = nullptr;
+  int64_t last_ld = 0;
+  uint64_t last_seed = 0;
+  int64_t last_need = 0;
+  // stage profiling with CUDA events on the ctx stream
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_live;
+  cudaEvent_t ev_open[8] = {};
+};
+
+namespace {
+constexpr int kStages = 8;  // 0 select, 1 pacm, 2 certify, 3 finish, 4 merge
+
+cudaEvent_t ev_get(tt_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(tt_ctx* c, int stage) {
+  if (!c->prof) return;
+  c->ev_open[stage] = ev_get(c);
+  cudaEventRecord(c->ev_open[stage], c->stream);
+}
+
+void prof_end(tt_ctx* c, int stage) {
+  if (!c->prof || !c->ev_open[stage]) return;
+  cudaEvent_t e = ev_get(c);
+  cudaEventRecord(e, c->stream);
+  c->ev_live.push_back({stage, {c->ev_open[stage], e}});
+  c->ev_open[stage] = nullptr;
+}
+}  // namespace
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+
+void tt::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" uint64_t tt_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+
+std::atomic<uint64_t> g_forward_calls{0};
+
+int fail(tt_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define TT_CUDA(ctx, call)                                                                   \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) return fail(ctx, TT_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TT_LAUNCHED(ctx)                                                                     \
+  do {                                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                     \
+    if (e_ != cudaSuccess) return fail(ctx, TT_E_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+int log2i(int64_t v) {
+  int l = 0;
+  while ((int64_t{1} << l) < v) ++l;
+  return l;
+}
+
+void factorize(int64_t n, std::vector<std::pair<int64_t, int>>& out) {
+  out.clear();
+  for (int64_t p = 2; p * p <= n; ++p)
+    if (n % p == 0) {
+      int e = 0;
+      while (n % p == 0) n /= p, ++e;
+      out.emplace_back(p, e);
+    }
+  if (n > 1) out.emplace_back(n, 1);
+}
+
+uint64_t binom_sat(int64_t n, int64_t k) {
+  if (k < 0 || k > n) return 0;
+  if (n - k < k) k = n - k;
+  unsigned __int128 r = 1;
+  for (int64_t i = 1; i <= k; ++i) {
+    r = r * (unsigned __int128)(n - k + i) / (unsigned __int128)i;
+    if (r > (unsigned __int128)UINT64_MAX) return UINT64_MAX;
+  }
+  return (uint64_t)r;
+}
+
+uint64_t sat_mul(uint64_t a, uint64_t b) {
+  if (a == 0 || b == 0) return 0;
+  if (a > UINT64_MAX / b) return UINT64_MAX;
+  return a * b;
+}
+
+// validate_op (workload.cpp:49-93) on the POD form + the limits of this build.
+int validate_op(tt_ctx* ctx, const tt_op_spec& op) {
+  const int na = op.n_spatial + op.n_reduction;
+  if (op.n_spatial < 0 || op.n_reduction < 0 || na > TT_MAX_AXES)
+    return fail(ctx, TT_E_VALIDATE, "op: bad axis counts");
+  if (op.kind == TT_OP_TILED && op.n_spatial == 0)
+    return fail(ctx, TT_E_VALIDATE, "op: a tiled op needs at least one spatial axis");
+  if (op.n_spatial > kMaxSp || op.n_reduction > kMaxRed)
+    return fail(ctx, TT_E_VALIDATE, "op: this build supports at most 4 spatial and 3 reduction axes");
+  for (int a = 0; a < na; ++a) {
+    if (op.extent[a] < 1)
+      return fail(ctx, TT_E_VALIDATE, "op: axis " + std::to_string(a) + " extent must be >= 1, got " +
+                                          std::to_string(op.extent[a]));
+    if (op.extent[a] >= (int64_t{1} << 31)) return fail(ctx, TT_E_VALIDATE, "op: extent exceeds int32 factors");
+  }
+  if (op.n_buffers < 1 || op.n_buffers > TT_MAX_BUFFERS) return fail(ctx, TT_E_VALIDATE, "op: no buffers");
+  int outputs = 0;
+  uint32_t referenced = 0;
+  for (int b = 0; b < op.n_buffers; ++b) {
+    const tt_buffer_spec& bs = op.buffers[b];
+    if (bs.n_axes < 1 || bs.n_axes > TT_MAX_AXES)
+      return fail(ctx, TT_E_VALIDATE, "op: buffer " + std::to_string(b) + " has no axes");
+    uint32_t seen = 0;
+    for (int q = 0; q < bs.n_axes; ++q) {
+      const int ax = bs.axes[q];
+      if (ax < 0 || ax >= na)
+        return fail(ctx, TT_E_VALIDATE, "op: buffer " + std::to_string(b) + " references unknown axis");
+      if (seen & (1u << ax)) return fail(ctx, TT_E_VALIDATE, "op: buffer " + std::to_string(b) + " repeats axis");
+      seen |= 1u << ax;
+    }
+    referenced |= seen;
+    if (bs.io == TT_IO_OUTPUT) ++outputs;
+  }
+  if (outputs != 1)
+    return fail(ctx, TT_E_VALIDATE, "op: exactly one output buffer required, got " + std::to_string(outputs));
+  for (int a = 0; a < na; ++a)
+    if (!(referenced & (1u << a)))
+      return fail(ctx, TT_E_VALIDATE, "op: axis " + std::to_string(a) + " referenced by no buffer");
+  if (op.fused_elementwise < 0) return fail(ctx, TT_E_VALIDATE, "op: fused_elementwise must be >= 0");
+  return TT_OK;
+}
+
+int compile_sketch(tt_ctx* ctx, const tt_sketch* sk, DevSketch& S) {
+  if (!sk) return fail(ctx, TT_E_STATE, "null sketch");
+  const tt_op_spec& op = sk->op;
+  int rc = validate_op(ctx, op);
+  if (rc) return rc;
+  if (sk->n_unroll < 1 || sk->n_unroll > TT_MAX_UNROLL) return fail(ctx, TT_E_VALIDATE, "sketch: bad unroll choices");
+  std::memset(&S, 0, sizeof(S));
+  S.n_sp = op.n_spatial, S.n_red = op.n_reduction, S.n_axes = op.n_spatial + op.n_reduction;
+  S.cols = 4 * S.n_sp + 3 * S.n_red + 1;
+  S.kind = op.kind, S.n_unroll = sk->n_unroll, S.fused = op.fused_elementwise;
+  for (int a = 0; a < S.n_axes; ++a) {
+    S.extent[a] = op.extent[a];
+    S.arity[a] = a < S.n_sp ? (op.kind == TT_OP_ELEMENTWISE ? 2 : 4) : 3;
+  }
+  for (int u = 0; u < TT_MAX_UNROLL; ++u) S.unroll[u] = u < sk->n_unroll ? sk->unroll[u] : sk->unroll[0];
+  S.innermost_spatial = S.n_sp - 1;
+  int out_buf = -1;
+  for (int b = 0; b < op.n_buffers; ++b)
+    if (op.buffers[b].io == TT_IO_OUTPUT && out_buf < 0) out_buf = b;
+  auto mask_of = [&](const tt_buffer_spec& bs) {
+    uint32_t m = 0;
+    for (int q = 0; q < bs.n_axes; ++q) m |= 1u << bs.axes[q];
+    return m;
+  };
+  const tt_buffer_spec& ob = op.buffers[out_buf];
+  S.out_mask = mask_of(ob);
+  S.out_last = ob.axes[ob.n_axes - 1];
+  S.out_rank = ob.n_axes;
+  S.n_in = 0;
+  for (int b = 0; b < op.n_buffers; ++b) {
+    const tt_buffer_spec& bs = op.buffers[b];
+    if (bs.io != TT_IO_INPUT) continue;
+    const int q = S.n_in++;
+    S.in_mask[q] = mask_of(bs);
+    S.in_last[q] = bs.axes[bs.n_axes - 1];
+    S.in_rank[q] = bs.n_axes;
+    int64_t size = 1;
+    int red = 0;
+    for (int t = 0; t < bs.n_axes; ++t) {
+      size *= op.extent[bs.axes[t]];
+      red |= bs.axes[t] >= S.n_sp;
+    }
+    S.in_size[q] = size;
+    S.in_has_red[q] = red;
+  }
+  S.output_size = 1;
+  for (int a = 0; a < S.n_sp; ++a) S.output_size *= op.extent[a];
+  S.red_total = 1;
+  for (int r = 0; r < S.n_red; ++r) S.red_total *= op.extent[S.n_sp + r];
+  S.flops = S.output_size * (op.kind == TT_OP_TILED ? S.red_total : 1);
+  // random_init draw plan + identity radix
+  std::vector<std::pair<int64_t, int>> pf;
+  S.n_prime = 0;
+  uint64_t space = 1;
+  for (int a = 0; a < S.n_axes; ++a) {
+    factorize(op.extent[a], pf);
+    for (auto& [p, e] : pf) {
+      if (S.n_prime >= TT_MAX_PRIMES) return fail(ctx, TT_E_VALIDATE, "op: too many distinct prime factors");
+      const int q = S.n_prime++;
+      S.pr_axis[q] = a, S.pr_e[q] = e, S.pr_p[q] = p;
+      S.pr_count[q] = binom_sat(e + S.arity[a] - 1, S.arity[a] - 1);
+      space = sat_mul(space, S.pr_count[q]);
+    }
+  }
+  S.space = sat_mul(space, (uint64_t)sk->n_unroll);
+  S.id_exact = S.space != UINT64_MAX;
+  return TT_OK;
+}
+
+int compile_device(tt_ctx* ctx, const tt_device_spec* d, DevDevice& D) {
+  if (!d) return fail(ctx, TT_E_STATE, "null device");
+  int rc = tt_validate_device(d);
+  if (rc) return fail(ctx, rc, "device: invalid device spec (validate_device)");
+  D.m_l0 = d->m_l0, D.m_l1 = d->m_l1, D.pu_l1 = d->pu_l1, D.n_l1 = d->n_l1;
+  D.pu_l2 = d->pu_l2, D.n_l2 = d->n_l2, D.t_p = d->t_p, D.t_m = d->t_m;
+  D.log2_nl1 = log2i(d->n_l1), D.log2_nl2 = log2i(d->n_l2);
+  D.pu_l1_n_l1 = d->pu_l1 * d->n_l1;
+  return TT_OK;
+}
+
+template <typename T>
+int grow(tt_ctx* ctx, T*& p, int64_t& cap, int64_t want) {
+  if (want <= cap && p) return TT_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  TT_CUDA(ctx, cudaMalloc((void**)&p, sizeof(T) * (size_t)(want > 0 ? want : 1)));
+  cap = want;
+  return TT_OK;
+}
+
+int ensure_k(tt_ctx* ctx, int64_t k) {
+  if (k <= ctx->k_cap) return TT_OK;
+  cudaFree(ctx->d_idx), cudaFree(ctx->d_cost), cudaFree(ctx->d_id), cudaFree(ctx->d_score);
+  cudaFree(ctx->d_score_fast), cudaFree(ctx->d_excluded), cudaFree(ctx->d_sublist);
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_idx, sizeof(int64_t) * k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_cost, sizeof(double) * k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_id, sizeof(uint64_t) * k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_score, sizeof(double) * k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_score_fast, sizeof(double) * k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_excluded, k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_sublist, sizeof(int32_t) * k));
+  ctx->k_cap = k;
+  return TT_OK;
+}
+
+int ensure_b(tt_ctx* ctx, int64_t b) {
+  if (b <= ctx->b_cap) return TT_OK;
+  cudaFree(ctx->d_pos), cudaFree(ctx->d_pos_fast), cudaFree(ctx->d_record);
+  if (ctx->h_record) cudaFreeHost(ctx->h_record);
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos, sizeof(int64_t) * b));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos_fast, sizeof(int64_t) * b));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_record, sizeof(int64_t) * (4 + 4 * b)));
+  TT_CUDA(ctx, cudaMallocHost((void**)&ctx->h_record, sizeof(int64_t) * (4 + 4 * b)));
+  ctx->b_cap = b;
+  return TT_OK;
+}
+
+int ensure_cost(tt_ctx* ctx, int64_t n) { return grow(ctx, ctx->sel.cost, ctx->sel.cost_cap, n); }
+
+int sync_check(tt_ctx* ctx) {
+  TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  TT_CUDA(ctx, cudaGetLastError());
+  return TT_OK;
+}
+
+// Runs the selector with retries (NEED_MORE: duplicates ate into the
+// target; the threshold is raised until k unique survive or all pass).
+int select_sync(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const int32_t* soa, int64_t ld, uint64_t s0,
+                int64_t first, bool seeded, int64_t n, int64_t k, int toggles, int64_t index_base, int64_t* idx,
+                double* cost, uint64_t* id, int64_t* count_host) {
+  int64_t need = k + k / 8 + 16;
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+    if (n > kSmallSelectMax) {
+      int rc = ensure_cost(ctx, n);
+      if (rc) return rc;
+    }
+    if (launch_select(S, D, soa, ld, s0, first, seeded, n, k, need, toggles, index_base, ctx->sel, idx, cost, id,
+                      ctx->d_count, ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    TT_LAUNCHED(ctx);
+    SelState st;
+    int invalid = 0;
+    TT_CUDA(ctx, cudaMemcpyAsync(&st, ctx->sel.state, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(ctx, cudaMemcpyAsync(&invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int rc = sync_check(ctx);
+    if (rc) return rc;
+    if (invalid) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule (factor products / unroll)");
+    if (n > kSmallSelectMax && (st.status & TT_SEL_OVERFLOW))
+      return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
+    if (n > kSmallSelectMax && (st.status & TT_SEL_NEED_MORE)) {
+      need *= 2;
+      continue;
+    }
+    TT_CUDA(ctx, cudaMemcpy(count_host, ctx->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return TT_OK;
+  }
+  return fail(ctx, TT_E_STATE, "draft selector did not converge");
+}
+
+uint64_t seed_state(uint64_t seed) { return seed ? seed : kGolden; }
+
+}  // namespace
+
+extern "C" {
+
+const char* tt_version(void) { return "paper_2402_02361_b200 0.1 (sm_100a)"; }
+
+const char* tt_status_code(int s) {
+  switch (s) {
+    case TT_OK: return "OK";
+    case TT_E_PARSE: return "E_PARSE";
+    case TT_E_VALIDATE: return "E_VALIDATE";
+    case TT_E_CONFIG: return "E_CONFIG";
+    case TT_E_STATE: return "E_STATE";
+    case TT_E_IO: return "E_IO";
+    case TT_E_CUDA: return "E_CUDA";
+    case TT_E_NCCL: return "E_NCCL";
+  }
+  return "E_UNKNOWN";
+}
+
+int tt_ctx_create(int device, tt_ctx** out) {
+  if (!out) return TT_E_STATE;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return TT_E_CUDA;
+  if (device < 0 || device >= n) return TT_E_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return TT_E_CUDA;
+  tt_ctx* c = new tt_ctx();
+  c->device = device;
+  auto bad = [&](cudaError_t e) {
+    if (e != cudaSuccess) {
+      tt_ctx_destroy(c);
+      return true;
+    }
+    return false;
+  };
+  if (bad(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking))) return TT_E_CUDA;
+  c->stream = c->own;
+  if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
+  if (bad(cudaMemset(c->sel.hist, 0, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.tkeys, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.tvals, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMemset(c->sel.tkeys, 0xff, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMemset(c->sel.tvals, 0xff, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.state, sizeof(SelState)))) return TT_E_CUDA;
+  if (bad(cudaMemset(c->sel.state, 0, sizeof(SelState)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.invalid, sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_count, sizeof(int64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_pos_count, sizeof(int64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_pos_fast_count, sizeof(int64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_status, 2 * sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_sublist_count, sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMemset(c->d_sublist_count, 0, sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaDeviceSynchronize())) return TT_E_CUDA;
+  *out = c;
+  return TT_OK;
+}
+
+void tt_ctx_destroy(tt_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.tkeys, c->sel.tvals, c->sel.state, c->sel.invalid,
+                  c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
+                  c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
+                  c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_record) cudaFreeHost(c->h_record);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+const char* tt_last_error(const tt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int tt_ctx_set_stream(tt_ctx* ctx, void* s) {
+  if (!ctx) return TT_E_STATE;
+  ctx->stream = s ? (cudaStream_t)s : ctx->own;
+  return TT_OK;
+}
+
+void* tt_ctx_stream(const tt_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int tt_ctx_sync(tt_ctx* ctx) {
+  if (!ctx) return TT_E_STATE;
+  return sync_check(ctx);
+}
+
+int tt_sketch_from_op(const tt_op_spec* op, int elementwise_fallback, tt_sketch* out) {
+  if (!op || !out) return TT_E_STATE;
+  int rc = validate_op(nullptr, *op);
+  if (rc) return rc;
+  if (op->kind == TT_OP_ELEMENTWISE && !elementwise_fallback) return TT_E_VALIDATE;
+  std::memset(out, 0, sizeof(*out));
+  out->op = *op;
+  out->n_unroll = 3;
+  out->unroll[0] = 1, out->unroll[1] = 4, out->unroll[2] = 16;
+  return TT_OK;
+}
+
+int tt_validate_device(const tt_device_spec* d) {
+  if (!d) return TT_E_STATE;
+  if (d->m_l0 <= 0 || d->m_l1 <= 0 || d->pu_l1 <= 0 || d->n_l1 <= 0 || d->pu_l2 <= 0 || d->n_l2 <= 0 ||
+      !(d->t_p > 0.0) || !(d->t_m > 0.0) || d->element_bytes <= 0)
+    return TT_E_VALIDATE;
+  if (!is_pow2(d->n_l1) || !is_pow2(d->n_l2)) return TT_E_VALIDATE;
+  if (d->t_p == __builtin_inf() || d->t_m == __builtin_inf()) return TT_E_VALIDATE;
+  return TT_OK;
+}
+
+uint64_t tt_space_size(const tt_sketch* sk) {
+  DevSketch S;
+  if (compile_sketch(nullptr, sk, S)) return 0;
+  return S.space;
+}
+
+int tt_draws_per_schedule(const tt_sketch* sk) {
+  DevSketch S;
+  if (compile_sketch(nullptr, sk, S)) return -1;
+  return S.n_prime + 1;
+}
+
+int tt_population_generate(tt_ctx* ctx, const tt_sketch* sk, uint64_t seed, int64_t first, int64_t n,
+                           int32_t* soa, int64_t ld, uint64_t* id) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if (n < 0 || first < 0 || (soa && ld < n)) return fail(ctx, TT_E_STATE, "population: bad n/ld");
+  if (launch_generate(S, seed_state(seed), first, n, soa, ld, id, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_schedule_identity(tt_ctx* ctx, const tt_sketch* sk, const int32_t* soa, int64_t ld, int64_t n, uint64_t* id) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "identity: schedule space exceeds 2^64");
+  if (launch_identity(S, soa, ld, n, id, ctx->stream)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_schedule_from_identity(tt_ctx* ctx, const tt_sketch* sk, const uint64_t* id, int64_t n, int32_t* soa,
+                              int64_t ld) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "identity: schedule space exceeds 2^64");
+  if (launch_from_identity(S, id, n, soa, ld, ctx->stream)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_draft_cost(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+                  int64_t n, int toggles, double* cost) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if (n < 0 || ld < n) return fail(ctx, TT_E_STATE, "draft_cost: bad n/ld");
+  if (n == 0) return TT_OK;
+  TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+  if (launch_draft_cost(S, D, soa, ld, 0, 0, false, n, toggles, cost, nullptr, ctx->sel.invalid, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  int invalid = 0;
+  TT_CUDA(ctx, cudaMemcpyAsync(&invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if ((rc = sync_check(ctx))) return rc;
+  if (invalid) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule (factor products / unroll)");
+  return TT_OK;
+}
+
+int tt_draft_topk(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+                  int64_t n, int64_t k, int toggles, int64_t index_base, int64_t* idx, double* cost, uint64_t* id,
+                  int64_t* count) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if (k < 1) return fail(ctx, TT_E_STATE, "explore: draft_size must be >= 1");
+  if (n < 2) return fail(ctx, TT_E_STATE, "explore: pop_size must be >= 2");
+  if (ld < n) return fail(ctx, TT_E_STATE, "draft_topk: ld < n");
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "draft_topk: schedule space exceeds 2^64 identities");
+  return select_sync(ctx, S, D, soa, ld, 0, 0, false, n, k, toggles, index_base, idx, cost, id, count);
+}
+
+int tt_explore1(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, uint64_t seed, int64_t first,
+                int64_t n, int64_t k, int toggles, int64_t* idx, double* cost, uint64_t* id, int64_t* count) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if (k < 1) return fail(ctx, TT_E_STATE, "explore: draft_size must be >= 1");
+  if (n < 2) return fail(ctx, TT_E_STATE, "explore: pop_size must be >= 2");
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "explore1: schedule space exceeds 2^64 identities");
+  return select_sync(ctx, S, D, nullptr, 0, seed_state(seed), first, true, n, k, toggles, first, idx, cost, id, count);
+}
+
+int tt_topk_merge(tt_ctx* ctx, const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k,
+                  int64_t* idx, double* out_cost, uint64_t* out_id, int64_t* count) {
+  if (!ctx) return TT_E_STATE;
+  if (m < 0 || m > 4096) return fail(ctx, TT_E_STATE, "merge: at most 4096 gathered entries per call");
+  if (launch_merge(cost, gidx, id, (int)m, k, idx, out_cost, out_id, ctx->d_count, ctx->stream))
+    return fail(ctx, TT_E_STATE, "merge: launch");
+  TT_LAUNCHED(ctx);
+  TT_CUDA(ctx, cudaMemcpyAsync(count, ctx->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  return sync_check(ctx);
+}
+
+int tt_features(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const uint64_t* id, int64_t k,
+                double* stmt, double* block) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  CandRef r{nullptr, 0, nullptr, 0, id};
+  if (launch_features64(S, D, r, k, stmt, block, ctx->stream)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_features_soa(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,
+                    const int64_t* idx, int64_t k, double* stmt, double* block) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  CandRef r{soa, ld, idx, 0, nullptr};
+  if (launch_features64(S, D, r, k, stmt, block, ctx->stream)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_pacm_load(tt_ctx* ctx, const double* params, int h) {
+  if (!ctx) return TT_E_STATE;
+  if (h < 1 || h > 512) return fail(ctx, TT_E_STATE, "hidden width must be in [1, 512]");
+  const int64_t np = tt_param_count(h);
+  if (ctx->h != h) {
+    if (ctx->d_params) cudaFree(ctx->d_params);
+    if (ctx->d_packed) cudaFree(ctx->d_packed);
+    ctx->d_params = nullptr, ctx->d_packed = nullptr;
+    TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_params, sizeof(double) * np));
+    ctx->h = h;
+    ctx->n_params = np;
+  }
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_params, params, sizeof(double) * np, cudaMemcpyDefault, ctx->stream));
+  ctx->packed_ok = false;
+  return TT_OK;
+}
+
+uint64_t tt_forward_calls(void) { return g_forward_calls.load(std::memory_order_relaxed); }
+void tt_reset_forward_calls(void) { g_forward_calls.store(0, std::memory_order_relaxed); }
+
+}  // extern "C"
+
+namespace {
+
+int ensure_packed(tt_ctx* ctx) {
+  if (ctx->packed_ok) return TT_OK;
+  if (!ctx->d_packed) TT_CUDA(ctx, cudaMalloc(&ctx->d_packed, pacm_tc_packed_bytes(ctx->h)));
+  if (launch_pacm_tc_pack(ctx->d_params, ctx->h, ctx->d_packed, ctx->stream))
+    return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: packing failed");
+  TT_LAUNCHED(ctx);
+  ctx->packed_ok = true;
+  return TT_OK;
+}
+
+// Scores the drafted set (positions [0, *count_dev)) into ctx->d_score.
+int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef ref, int64_t k_max, int precision,
+                  int64_t b, double band, const int64_t* count_dev) {
+  if (precision == TT_PREC_FP64) {
+    prof_begin(ctx, 1);
+    if (launch_pacm64(S, D, ref, count_dev, k_max, nullptr, nullptr, ctx->d_params, ctx->h, 0, ctx->d_score,
+                      ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    prof_end(ctx, 1);
+    TT_LAUNCHED(ctx);
+    TT_CUDA(ctx, cudaMemsetAsync(ctx->d_sublist_count, 0, sizeof(int), ctx->stream));
+    return TT_OK;
+  }
+  if (precision != TT_PREC_BF16) return fail(ctx, TT_E_CONFIG, "unknown precision");
+  if (!pacm_tc_supported(S, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
+  int rc = ensure_packed(ctx);
+  if (rc) return rc;
+  prof_begin(ctx, 1);
+  if (launch_pacm_tc(S, D, ref, count_dev, k_max, ctx->d_packed, ctx->h, ctx->d_score_fast, ctx->stream))
+    return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
+  prof_end(ctx, 1);
+  TT_LAUNCHED(ctx);
+  if (b > 0) {
+    prof_begin(ctx, 2);
+    // certified selection: exact fp64 rescoring of the boundary band
+    launch_select_top(ctx->d_score_fast, ctx->d_cost, nullptr, k_max, count_dev, b, ctx->d_pos_fast,
+                      ctx->d_pos_fast_count, ctx->d_status + 1, ctx->stream);
+    launch_band(ctx->d_score_fast, count_dev, k_max, ctx->d_pos_fast, ctx->d_pos_fast_count, band, ctx->d_sublist,
+                ctx->d_sublist_count, ctx->d_excluded, ctx->stream);
+    TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_score, ctx->d_score_fast, sizeof(double) * k_max, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+    if (launch_pacm64(S, D, ref, count_dev, k_max, ctx->d_sublist, ctx->d_sublist_count, ctx->d_params, ctx->h, 0,
+                      ctx->d_score, ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    prof_end(ctx, 2);
+    TT_LAUNCHED(ctx);
+  } else {
+    TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_score, ctx->d_score_fast, sizeof(double) * k_max, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+  }
+  return TT_OK;
+}
+
+// Everything after the drafted set exists on the device.
+int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg,
+                      CandRef ref) {
+  int rc = score_drafted(ctx, S, D, ref, cfg->k, cfg->precision, cfg->b, cfg->band > 0 ? cfg->band : 0.05,
+                         ctx->d_count);
+  if (rc) return rc;
+  const bool certified = cfg->precision != TT_PREC_FP64;
+  prof_begin(ctx, 3);
+  launch_select_top(ctx->d_score, ctx->d_cost, certified ? ctx->d_excluded : nullptr, cfg->k, ctx->d_count, cfg->b,
+                    ctx->d_pos, ctx->d_pos_count, ctx->d_status, ctx->stream);
+  launch_gather(ctx->d_pos, ctx->d_pos_count, ctx->d_count, ctx->sel.state, nullptr, ctx->d_sublist_count,
+                ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, cfg->b, ctx->d_record, ctx->stream);
+  prof_end(ctx, 3);
+  TT_LAUNCHED(ctx);
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_record, ctx->d_record, sizeof(int64_t) * (4 + 4 * cfg->b),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+  return TT_OK;
+}
+
+int check_round_cfg(tt_ctx* ctx, const tt_round_config* cfg) {
+  if (!cfg) return fail(ctx, TT_E_STATE, "null round config");
+  if (cfg->k < 1) return fail(ctx, TT_E_CONFIG, "draft_size must be >= 1");
+  if (cfg->b < 1) return fail(ctx, TT_E_CONFIG, "batch must be >= 1");
+  if (cfg->k < cfg->b) return fail(ctx, TT_E_CONFIG, "draft_size must be >= batch");
+  if (cfg->n < 2) return fail(ctx, TT_E_CONFIG, "pop_size must be >= 2");
+  if (!ctx->d_params) return fail(ctx, TT_E_STATE, "round: tt_pacm_load first");
+  return TT_OK;
+}
+
+int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need) {
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if ((rc = check_round_cfg(ctx, cfg))) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "round: schedule space exceeds 2^64 identities");
+  if ((rc = ensure_k(ctx, cfg->k))) return rc;
+  if ((rc = ensure_b(ctx, cfg->b))) return rc;
+  const bool seeded = soa == nullptr;
+  if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
+  if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+  prof_begin(ctx, 0);
+  if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k, need, cfg->toggles,
+                    cfg->first, ctx->sel, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  prof_end(ctx, 0);
+  TT_LAUNCHED(ctx);
+  CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
+  if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  ctx->pending = true;
+  ctx->last_b = cfg->b;
+  ctx->last_k = cfg->k;
+  ctx->last_cfg = *cfg;
+  ctx->last_sketch = *sk;
+  ctx->last_dev = *dev;
+  ctx->last_soa = soa;
+  ctx->last_ld = ld;
+  ctx->last_seed = seed;
+  ctx->last_need = need;
+  return TT_OK;
+}
+
+int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* sel_cost, uint64_t* sel_id,
+                  tt_round_result* res, bool allow_retry) {
+  if (!ctx->pending) return fail(ctx, TT_E_STATE, "round: nothing enqueued");
+  int rc = sync_check(ctx);
+  ctx->pending = false;
+  if (rc) return rc;
+  const int64_t b = ctx->last_b;
+  if (((int)ctx->h_record[2] & TT_SEL_NEED_MORE) && allow_retry) {
+    // duplicates consumed the selector's margin: raise the target, redo
+    int64_t need = ctx->last_need * 2;
+    bool ok = false;
+    for (int attempt = 0; attempt < 62 && !ok; ++attempt, need *= 2) {
+      tt_round_config cfg = ctx->last_cfg;
+      if ((rc = round_enqueue(ctx, &ctx->last_sketch, &ctx->last_dev, &cfg, ctx->last_soa, ctx->last_ld,
+                              ctx->last_seed, need)))
+        return rc;
+      if ((rc = sync_check(ctx))) return rc;
+      ctx->pending = false;
+      ok = !((int)ctx->h_record[2] & TT_SEL_NEED_MORE);
+    }
+    if (!ok) return fail(ctx, TT_E_STATE, "draft selector did not converge");
+  }
+  const int64_t* rec = ctx->h_record;
+  const int status = (int)rec[2];
+  const int sel_status = status & 0xff;
+  if (sel_status & TT_SEL_OVERFLOW)
+    return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
+  if (ctx->last_soa) {
+    int invalid = 0;
+    TT_CUDA(ctx, cudaMemcpy(&invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost));
+    if (invalid) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
+  }
+  const int64_t selected = rec[0];
+  const int64_t* ix = rec + 4;
+  const double* sc = (const double*)(ix + b);
+  const double* co = sc + b;
+  const uint64_t* ids = (const uint64_t*)(co + b);
+  for (int64_t e = 0; e < b; ++e) {
+    if (sel_index) sel_index[e] = ix[e];
+    if (sel_score) sel_score[e] = sc[e];
+    if (sel_cost) sel_cost[e] = co[e];
+    if (sel_id) sel_id[e] = ids[e];
+  }
+  if (res) {
+    res->selected = selected;
+    res->drafted = rec[1];
+    res->rescored = rec[3];
+    res->status = status;
+  }
+  g_forward_calls.fetch_add((uint64_t)rec[1], std::memory_order_relaxed);
+  return TT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tt_pacm_score(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const uint64_t* id, int64_t k,
+                  int precision, double* score) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if (!ctx->d_params) return fail(ctx, TT_E_STATE, "score: tt_pacm_load first");
+  if (k <= 0) return TT_OK;
+  CandRef ref{nullptr, 0, nullptr, 0, id};
+  if (precision == TT_PREC_FP64) {
+    if (launch_pacm64(S, D, ref, nullptr, k, nullptr, nullptr, ctx->d_params, ctx->h, 0, score, ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  } else if (precision == TT_PREC_BF16) {
+    if (!pacm_tc_supported(S, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
+    if ((rc = ensure_packed(ctx))) return rc;
+    if (launch_pacm_tc(S, D, ref, nullptr, k, ctx->d_packed, ctx->h, score, ctx->stream))
+      return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
+  } else {
+    return fail(ctx, TT_E_CONFIG, "unknown precision");
+  }
+  TT_LAUNCHED(ctx);
+  g_forward_calls.fetch_add((uint64_t)k, std::memory_order_relaxed);
+  return TT_OK;
+}
+
+int tt_pacm_score_features(tt_ctx* ctx, const double* stmt, const double* block, int n_stmt, int n_block, int64_t k,
+                           int attention_identity, double* score) {
+  if (!ctx) return TT_E_STATE;
+  if (!ctx->d_params) return fail(ctx, TT_E_STATE, "score: tt_pacm_load first");
+  if (n_stmt < 1 || n_block < 1)
+    return fail(ctx, TT_E_STATE, "feature must have at least one statement and one dataflow block");
+  if (launch_pacm64_feats(stmt, block, n_stmt, n_block, k, ctx->d_params, ctx->h, attention_identity, score,
+                          ctx->stream))
+    return fail(ctx, TT_E_STATE, "score launch");
+  TT_LAUNCHED(ctx);
+  g_forward_calls.fetch_add((uint64_t)(k > 0 ? k : 0), std::memory_order_relaxed);
+  return TT_OK;
+}
+
+int tt_select_top(tt_ctx* ctx, const double* scores, const double* drafts, const uint8_t* excluded, int64_t n,
+                  int64_t b, int64_t* idx_host) {
+  if (!ctx) return TT_E_STATE;
+  if (b < 1) return fail(ctx, TT_E_STATE, "select_top: b must be >= 1");
+  int rc = ensure_b(ctx, b);
+  if (rc) return rc;
+  if (launch_select_top(scores, drafts, excluded, n, nullptr, b, ctx->d_pos, ctx->d_pos_count, ctx->d_status,
+                        ctx->stream))
+    return fail(ctx, TT_E_STATE, "select_top: n too large for b (tiles * b must be <= 4096)");
+  TT_LAUNCHED(ctx);
+  int status = 0;
+  int64_t cnt = 0;
+  TT_CUDA(ctx, cudaMemcpyAsync(&status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(ctx, cudaMemcpyAsync(&cnt, ctx->d_pos_count, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  if ((rc = sync_check(ctx))) return rc;
+  if (status)
+    return fail(ctx, TT_E_STATE, "select_top: requested " + std::to_string(b) + " but only " + std::to_string(cnt) +
+                                     " unmeasured candidates available");
+  TT_CUDA(ctx, cudaMemcpy(idx_host, ctx->d_pos, sizeof(int64_t) * b, cudaMemcpyDeviceToHost));
+  return TT_OK;
+}
+
+int tt_gd_step(tt_ctx* ctx, double* params, const double* grads, int64_t n, double lr) {
+  if (!ctx) return TT_E_STATE;
+  launch_gd_step(params, grads, n, lr, ctx->stream);
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_momentum_update(tt_ctx* ctx, double* phi, const double* target, int64_t n, double m) {
+  if (!ctx) return TT_E_STATE;
+  if (!(m >= 0.0 && m < 1.0)) return fail(ctx, TT_E_STATE, "momentum must lie in [0, 1)");
+  launch_momentum(phi, target, n, m, ctx->stream);
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_round_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                   const int32_t* soa, int64_t ld, uint64_t seed) {
+  if (!ctx) return TT_E_STATE;
+  if (!cfg) return fail(ctx, TT_E_STATE, "null round config");
+  return round_enqueue(ctx, sk, dev, cfg, soa, ld, seed, cfg->k + cfg->k / 8 + 16);
+}
+
+int tt_round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* sel_cost, uint64_t* sel_id,
+                     tt_round_result* res) {
+  if (!ctx) return TT_E_STATE;
+  return round_collect(ctx, sel_index, sel_score, sel_cost, sel_id, res, true);
+}
+
+int tt_round(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+             const int32_t* soa, int64_t ld, uint64_t seed, int64_t* sel_index, double* sel_score, double* sel_cost,
+             uint64_t* sel_id, tt_round_result* res) {
+  int rc = tt_round_async(ctx, sk, dev, cfg, soa, ld, seed);
+  if (rc) return rc;
+  return round_collect(ctx, sel_index, sel_score, sel_cost, sel_id, res, true);
+}
+
+int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                         const int32_t* soa, int64_t ld, uint64_t seed, double* cost_out, int64_t* gidx_out,
+                         uint64_t* id_out) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if ((rc = check_round_cfg(ctx, cfg))) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "round: schedule space exceeds 2^64 identities");
+  const bool seeded = soa == nullptr;
+  if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
+  TT_CUDA(ctx, cudaMemsetAsync(gidx_out, 0xff, sizeof(int64_t) * cfg->k, ctx->stream));  // -1 = empty slot
+  TT_CUDA(ctx, cudaMemsetAsync(cost_out, 0, sizeof(double) * cfg->k, ctx->stream));
+  TT_CUDA(ctx, cudaMemsetAsync(id_out, 0, sizeof(uint64_t) * cfg->k, ctx->stream));
+  if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+  prof_begin(ctx, 0);
+  if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k,
+                    cfg->k + cfg->k / 8 + 16, cfg->toggles, cfg->first, ctx->sel, gidx_out, cost_out, id_out,
+                    ctx->d_count, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  prof_end(ctx, 0);
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev,
+                                 const tt_round_config* cfg, const double* cost, const int64_t* gidx,
+                                 const uint64_t* id, int64_t m) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if ((rc = check_round_cfg(ctx, cfg))) return rc;
+  if (m < 0 || m > 4096) return fail(ctx, TT_E_STATE, "merge: at most 4096 gathered entries per call");
+  if ((rc = ensure_k(ctx, cfg->k))) return rc;
+  if ((rc = ensure_b(ctx, cfg->b))) return rc;
+  prof_begin(ctx, 4);
+  if (launch_merge(cost, gidx, id, (int)m, cfg->k, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->stream))
+    return fail(ctx, TT_E_STATE, "merge launch");
+  prof_end(ctx, 4);
+  TT_LAUNCHED(ctx);
+  CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
+  if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  ctx->pending = true;
+  ctx->last_b = cfg->b;
+  ctx->last_k = cfg->k;
+  ctx->last_soa = nullptr;
+  ctx->last_need = -1;  // no retry: the local selections are the caller's
+  return TT_OK;
+}
+
+int tt_round_finish_merged(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                           const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t* sel_index,
+                           double* sel_score, double* sel_cost, uint64_t* sel_id, tt_round_result* res) {
+  int rc = tt_round_finish_merged_async(ctx, sk, dev, cfg, cost, gidx, id, m);
+  if (rc) return rc;
+  return round_collect(ctx, sel_index, sel_score, sel_cost, sel_id, res, false);
+}
+
+int tt_profile_enable(tt_ctx* ctx, int on) {
+  if (!ctx) return TT_E_STATE;
+  ctx->prof = on != 0;
+  return TT_OK;
+}
+
+int tt_profile_read(tt_ctx* ctx, double* ms_sum, int64_t* count, int n_stages) {
+  if (!ctx) return TT_E_STATE;
+  int rc = sync_check(ctx);
+  if (rc) return rc;
+  for (int s = 0; s < n_stages; ++s) ms_sum[s] = 0.0, count[s] = 0;
+  for (auto& [stage, pr] : ctx->ev_live) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    if (stage < n_stages) ms_sum[stage] += ms, count[stage] += 1;
+    ctx->ev_pool.push_back(pr.first);
+    ctx->ev_pool.push_back(pr.second);
+  }
+  ctx->ev_live.clear();
+  return TT_OK;
+}
+
+int tt_round_drafted(const tt_ctx* ctx, const int64_t** idx, const double** cost, const uint64_t** id,
+                     const double** score) {
+  if (!ctx || !ctx->d_idx) return TT_E_STATE;
+  if (idx) *idx = ctx->d_idx;
+  if (cost) *cost = ctx->d_cost;
+  if (id) *id = ctx->d_id;
+  if (score) *score = ctx->d_score;
+  return TT_OK;
+}
+
+}  // extern "C"

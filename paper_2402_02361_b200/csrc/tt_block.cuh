@@ -1,0 +1,85 @@
+// tt_block.cuh — CTA-wide primitives staged in shared memory: bitonic sort
+// of (key1, key2, payload) triples and an exclusive scan. Used by the
+// draft top-K finalisation, the cross-rank merge and select_top.
+#pragma once
+
+#include <cstdint>
+
+namespace tt {
+
+// Ascending lexicographic (a, b[, c]) bitonic sort of n = 2^m entries, all
+// in shared memory, executed by the whole CTA. With KEY3 = false, c is a
+// payload carried along.
+template <bool KEY3 = false>
+__device__ __forceinline__ void block_bitonic_sort(uint64_t* a, uint64_t* b, uint64_t* c, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a0 = a[lo], a1 = a[hi], b0 = b[lo], b1 = b[hi];
+        const uint64_t c0 = c[lo], c1 = c[hi];
+        bool gt = a0 > a1 || (a0 == a1 && b0 > b1);
+        bool lt = a0 < a1 || (a0 == a1 && b0 < b1);
+        if (KEY3 && a0 == a1 && b0 == b1) gt = c0 > c1, lt = c0 < c1;
+        if (up ? gt : lt) {
+          a[lo] = a1, a[hi] = a0;
+          b[lo] = b1, b[hi] = b0;
+          c[lo] = c1, c[hi] = c0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Exclusive prefix sum over flags[0..n) (n <= 32 * blockDim, values small),
+// result in out[0..n) and the total returned to every thread. `warp_tot`
+// needs 32 ints of shared memory.
+__device__ __forceinline__ int block_exclusive_scan(const int* flags, int* out, int n, int* warp_tot) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int beg = threadIdx.x * per;
+  int local = 0;
+  for (int q = 0; q < per; ++q)
+    if (beg + q < n) local += flags[beg + q];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    int v = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += u;
+    }
+    if (lane < nw) warp_tot[lane] = v;  // inclusive warp prefix
+  }
+  __syncthreads();
+  int run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
+  for (int q = 0; q < per; ++q)
+    if (beg + q < n) {
+      out[beg + q] = run;
+      run += flags[beg + q];
+    }
+  const int nw = (blockDim.x + 31) >> 5;
+  const int total = warp_tot[nw - 1];
+  __syncthreads();
+  return total;
+}
+
+__host__ __device__ __forceinline__ int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace tt

@@ -1,0 +1,100 @@
+// tt_kernels.h — internal launcher interface between the C-ABI layer
+// (tt_api.cu) and the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tt_device.cuh"
+
+namespace tt {
+
+// Kernel launches issued by this library (tt_kernel_launches()).
+void note_launch();
+
+constexpr int64_t kSmallSelectMax = 4096;
+
+enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2 };
+
+// Device-resident state of one top-K selection (k_draft.cu).
+struct SelState {
+  uint64_t prefix;  // threshold: keys with (key >> shift) <= prefix survive
+  int32_t shift;
+  int32_t done;
+  int64_t below;
+  int64_t need;
+  int32_t all;
+  int32_t status;
+  uint32_t survivors;
+  uint32_t unique;
+  int64_t count;
+};
+
+struct SelScratch {
+  double* cost = nullptr;  // N costs
+  int64_t cost_cap = 0;
+  uint32_t* hist = nullptr;  // 4096 bins, zero between uses
+  uint64_t* tkeys = nullptr;  // hash table, all-ones between uses
+  uint64_t* tvals = nullptr;
+  SelState* state = nullptr;
+  int* invalid = nullptr;
+};
+
+// k_draft.cu
+int launch_generate(const DevSketch& S, uint64_t s0, int64_t first, int64_t n, int32_t* soa, int64_t ld,
+                    uint64_t* id_out, cudaStream_t st);
+int launch_identity(const DevSketch& S, const int32_t* soa, int64_t ld, int64_t n, uint64_t* id_out,
+                    cudaStream_t st);
+int launch_from_identity(const DevSketch& S, const uint64_t* id, int64_t n, int32_t* soa, int64_t ld,
+                         cudaStream_t st);
+int launch_draft_cost(const DevSketch& S, const DevDevice& D, const int32_t* soa, int64_t ld, uint64_t s0,
+                      int64_t first, bool seeded, int64_t n, int toggles, double* cost, uint32_t* hist,
+                      int* invalid, cudaStream_t st);
+int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, int64_t ld, uint64_t s0,
+                  int64_t first, bool seeded, int64_t n, int64_t k, int64_t need, int toggles,
+                  int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
+                  int64_t* out_count, cudaStream_t st);
+int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
+                 double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);
+
+// k_pacm64.cu — fp64 PaCM (parity mode / certification rescoring)
+// Candidates are addressed by identity (population-independent) or by
+// (soa, ld, local index). `list`/`count` optionally restrict scoring to a
+// device-side sublist of positions (count read on device).
+struct CandRef {
+  const int32_t* soa;  // nullptr → reconstruct from identities
+  int64_t ld;
+  const int64_t* idx;  // population index per position (minus index_base)
+  int64_t index_base;
+  const uint64_t* id;  // identities per position (when soa == nullptr)
+};
+int launch_features64(const DevSketch& S, const DevDevice& D, CandRef ref, int64_t k, double* stmt_out,
+                      double* block_out, cudaStream_t st);
+int launch_pacm64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                  const int32_t* sublist, const int* sublist_count, const double* params, int h,
+                  int attention_identity, double* score_out, cudaStream_t st);
+int launch_pacm64_feats(const double* stmt, const double* block, int n_stmt, int n_block, int64_t k,
+                        const double* params, int h, int attention_identity, double* score_out, cudaStream_t st);
+
+// k_pacm_tc.cu — tcgen05/TMEM fast path (bf16 operands, fp32 accumulators)
+bool pacm_tc_supported(const DevSketch& S, int h);
+size_t pacm_tc_packed_bytes(int h);
+int launch_pacm_tc_pack(const double* params, int h, void* packed, cudaStream_t st);
+int launch_pacm_tc(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                   const void* packed, int h, double* score_out, cudaStream_t st);
+
+// k_select.cu
+int launch_select_top(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n,
+                      const int64_t* n_dev, int64_t b, int64_t* out_pos, int64_t* out_count, int* status,
+                      cudaStream_t st);
+int launch_band(const double* fast, const int64_t* n_dev, int64_t n_max, const int64_t* pos_fast,
+                const int64_t* pos_count, double band, int32_t* sublist, int* sublist_count, uint8_t* excluded,
+                cudaStream_t st);
+int launch_gd_step(double* params, const double* grads, int64_t n, double lr, cudaStream_t st);
+int launch_momentum(double* phi, const double* target, int64_t n, double m, cudaStream_t st);
+int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
+                  const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
+                  const uint64_t* id, const double* scores, int64_t b, int64_t* out, cudaStream_t st);
+
+}  // namespace tt
