@@ -7,16 +7,18 @@
 // the draft_size lowest (cost, discovery) entries.
 //
 // K2 design (HBM-bound, no full sort of N):
-//   * N <= 4096: one CTA computes every cost into shared memory, sorts
-//     (cost, index) bitonically, dedups and emits — a single launch.
+//   * N <= 4096: one CTA computes every cost in registers, sorts (cost,
+//     index) with a register/shuffle bitonic network, dedups, emits.
 //   * N  > 4096: K1 writes costs and a 4096-bin shared-memory histogram of
 //     the cost bit pattern (positive doubles order like their bits); a 1-CTA
-//     scan finds the bin holding the K-th key; up to two refine passes
-//     narrow it 12 bits at a time until at most kSurvivorCap keys survive;
-//     a compaction pass inserts survivors into a hash table keyed by their
-//     exact 64-bit identity (atomicMin keeps the first index: the reference's
-//     "first discovery wins" dedup); a 1-CTA finalisation sorts the unique
-//     survivors by (cost, index) and emits the K lowest.
+//     scan finds the bin holding the need-th key; up to two refine passes
+//     narrow it 12 bits at a time until at most kSurvivorTarget keys
+//     survive; a compaction pass appends the survivors; a 1-CTA finaliser
+//     sorts them, resolves identities only inside equal-cost runs, drops
+//     later duplicates ("first discovery wins") and emits the K lowest.
+//   * Pathological ties (> kSurvivorCap keys sharing a 36-bit cost prefix)
+//     switch to an identity-keyed hash-table compaction that deduplicates
+//     on insert (atomicMin keeps the first index).
 // Identical schedules have identical costs, so the threshold never splits
 // a duplicate group; selection is exact for any input.
 #include <cstdint>
@@ -28,8 +30,12 @@
 namespace tt {
 
 constexpr int kHistBins = 4096;
-constexpr int kSurvivorCap = 4096;   // unique survivors the finaliser sorts
-constexpr int kTableCap = 16384;     // hash slots (load <= 0.25 at the cap)
+constexpr int kSurvivorTarget = 1024;  // refine while more keys survive
+constexpr int kFinalCap = 1024;        // survivors the (append-path) finaliser sorts
+constexpr int kSurvivorCap = 4096;     // entries the hash-path finaliser / merge sort
+constexpr int kTableCap = 16384;       // hash slots of the fallback path
+constexpr int kSortE = 4;              // keys per thread in the 4096-entry sorts
+constexpr int kFinalE = 1;             // keys per thread in the 1024-entry sorts (1024 threads)
 constexpr uint64_t kEmpty = ~0ull;
 
 struct Src {
@@ -49,6 +55,14 @@ __device__ __forceinline__ uint64_t load_cand(const DevSketch& S, const Src& src
     load_factors<NSP, NRED>(src.soa, src.ld, i, F, with_unroll);
     return 0;
   }
+}
+
+template <int NSP, int NRED, bool SEED>
+__device__ __forceinline__ uint64_t identity_at(const DevSketch& S, const Src& src, int64_t i) {
+  Factors<NSP, NRED> F;
+  const uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, true);
+  if constexpr (SEED) return id;
+  return identity_of<NSP, NRED>(S, F);
 }
 
 // validate_schedule (schedule.cpp:242-278) on the register copy
@@ -145,16 +159,16 @@ __global__ void __launch_bounds__(256) k_draft_cost(DevSketch S, DevDevice D, Sr
 // --------------------------------------------------------- K2 selector ----
 // Scan: find the histogram bin that contains the need-th smallest key.
 __global__ void __launch_bounds__(1024) k_sel_scan(uint32_t* __restrict__ hist, SelState* __restrict__ st,
-                                                   int64_t need, int64_t n, int level) {
+                                                   int64_t need, int level) {
   __shared__ int counts[kHistBins];
   __shared__ int excl[kHistBins];
   __shared__ int wt[32];
   __shared__ int found;
-  if (level > 0 && st->done) return;  // refine not needed: nothing to do (hist untouched)
+  if (level > 0 && st->done) return;  // nothing to refine (hist untouched)
   if (level == 0 && threadIdx.x == 0) {
     st->prefix = 0, st->shift = 64, st->below = 0, st->done = 0, st->all = 0, st->status = 0;
     st->need = need;
-    st->survivors = 0, st->unique = 0, st->count = 0;
+    st->survivors = 0, st->unique = 0, st->count = 0, st->nsurv = 0;
   }
   for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
     counts[b] = (int)hist[b];
@@ -164,35 +178,30 @@ __global__ void __launch_bounds__(1024) k_sel_scan(uint32_t* __restrict__ hist, 
   __syncthreads();
   const int total = block_exclusive_scan(counts, excl, kHistBins, wt);
   const int64_t below = level == 0 ? 0 : st->below;
-  const int64_t want = (level == 0 ? need : st->need) - below;
+  const int64_t want = need - below;
   for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
     if (counts[b] > 0 && excl[b] < want && excl[b] + counts[b] >= want) found = b;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const int width = level == 0 ? 12 : 12;
-  const int new_shift = level == 0 ? 51 : (st->shift - width < 0 ? 0 : st->shift - width);
-  if (found < 0) {  // fewer keys than needed in range: everything survives
+  const int new_shift = level == 0 ? 51 : (st->shift - 12 < 0 ? 0 : st->shift - 12);
+  if (found < 0) {  // fewer keys than needed: everything in range survives
     if (level == 0) {
       st->all = 1;
-      st->done = 1;
-      st->survivors = (uint32_t)(total < 0 ? 0 : total);
-    } else {
-      // cannot happen (the refined bin held >= want keys); keep whole bin
-      st->done = 1;
+      st->survivors = (uint32_t)total;
     }
+    st->done = 1;
     return;
   }
   const int64_t surv = below + excl[found] + counts[found];
   const uint64_t prefix = level == 0 ? (uint64_t)found : ((st->prefix << (st->shift - new_shift)) | (uint64_t)found);
   st->prefix = prefix;
   st->shift = new_shift;
-  if (surv <= kSurvivorCap || new_shift == 0 || level >= 2) {
+  if (surv <= kSurvivorTarget || new_shift == 0 || level >= 2) {
     st->done = 1;
     st->survivors = (uint32_t)(surv > 0xffffffffLL ? 0xffffffffu : surv);
   } else {
     st->below = below + excl[found];
   }
-  (void)n;
 }
 
 // Refine: histogram the next 12 bits of the keys inside the current bin.
@@ -214,64 +223,52 @@ __global__ void __launch_bounds__(256) k_sel_refine(const double* __restrict__ c
     if (sh[b]) atomicAdd(&hist[b], sh[b]);
 }
 
-__device__ __forceinline__ uint64_t slot_hash(uint64_t id) { return scramble64(id + kGolden); }
-
-// Compaction: survivors → identity-keyed hash table (first index wins).
-template <int NSP, int NRED, bool SEED>
-__global__ void __launch_bounds__(256) k_sel_compact(DevSketch S, Src src, const double* __restrict__ cost,
-                                                     int64_t n, SelState* __restrict__ st,
-                                                     uint64_t* __restrict__ tkeys, uint64_t* __restrict__ tvals) {
-  const uint64_t prefix = st->prefix;
-  const int shift = st->shift;
-  const bool all = st->all != 0;
-  int local_unique = 0;
-  bool overflow = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = cost_key(__ldg(cost + i));
-    const bool keep = all || shift >= 64 || (k >> shift) <= prefix;
-    if (!keep) continue;
-    Factors<NSP, NRED> F;
-    uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, true);
-    if constexpr (!SEED) id = identity_of<NSP, NRED>(S, F);
-    uint64_t h = slot_hash(id) & (kTableCap - 1);
-    int probes = 0;
-    while (true) {
-      const uint64_t prev = atomicCAS((unsigned long long*)&tkeys[h], (unsigned long long)kEmpty,
-                                      (unsigned long long)id);
-      if (prev == kEmpty || prev == id) {
-        atomicMin((unsigned long long*)&tvals[h], (unsigned long long)i);
-        local_unique += prev == kEmpty;
-        break;
-      }
-      h = (h + 1) & (kTableCap - 1);
-      if (++probes >= kTableCap) {
-        overflow = true;
-        break;
-      }
-    }
-  }
-  if (local_unique) atomicAdd(&st->unique, (uint32_t)local_unique);
-  if (overflow) atomicOr(&st->status, TT_SEL_OVERFLOW);
+__device__ __forceinline__ bool survives(uint64_t k, const SelState& st) {
+  return st.all || st.shift >= 64 || (k >> st.shift) <= st.prefix;
 }
 
-// Sort (cost, index, identity) entries, drop later duplicates of an
-// identity (duplicates share the cost, so they are adjacent runs of the
-// (cost, index) order), emit the first K. Entries >= nvalid are padding.
-__device__ void sort_dedup_emit(uint64_t* a, uint64_t* b, uint64_t* c, int* flag, int* pos, int* wt,
-                                int nvalid, int npow2, int64_t k, int64_t index_base,
-                                int64_t* __restrict__ out_idx, double* __restrict__ out_cost,
-                                uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count) {
-  for (int e = threadIdx.x + nvalid; e < npow2; e += blockDim.x) a[e] = kEmpty, b[e] = kEmpty, c[e] = kEmpty;
-  block_bitonic_sort(a, b, c, npow2);
-  for (int e = threadIdx.x; e < npow2; e += blockDim.x) {
+// Compaction: append survivors (warp-aggregated atomics). Order is
+// irrelevant: the finaliser sorts by (cost, index).
+__global__ void __launch_bounds__(256) k_sel_compact(const double* __restrict__ cost, int64_t n,
+                                                     SelState* __restrict__ st, uint64_t* __restrict__ skey,
+                                                     int64_t* __restrict__ sidx) {
+  const SelState s = *st;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint64_t k = 0;
+    bool keep = false;
+    if (i < n) {
+      k = cost_key(__ldg(cost + i));
+      keep = survives(k, s);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    uint32_t pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&st->nsurv, (uint32_t)__popc(m));
+    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+    if (keep) {
+      const uint32_t p = pos0 + __popc(m & ((1u << lane) - 1u));
+      if (p < kSurvivorCap) skey[p] = k, sidx[p] = i;
+    }
+  }
+}
+
+// Dedup + emit over sorted shared arrays a (cost key), b (local index),
+// c (identity; valid wherever an equal-cost neighbour exists).
+__device__ void dedup_emit(const uint64_t* a, const uint64_t* b, const uint64_t* c, int* flag, int* pos, int* wt,
+                           int nvalid, int np, int64_t k, int64_t index_base, int64_t* __restrict__ out_idx,
+                           double* __restrict__ out_cost, uint64_t* __restrict__ out_id,
+                           int64_t* __restrict__ out_count) {
+  for (int e = threadIdx.x; e < np; e += blockDim.x) {
     int keep = e < nvalid;
     for (int q = e - 1; keep && q >= 0 && a[q] == a[e]; --q)
       if (c[q] == c[e]) keep = 0;
     flag[e] = keep;
   }
   __syncthreads();
-  const int total = block_exclusive_scan(flag, pos, npow2, wt);
-  for (int e = threadIdx.x; e < npow2; e += blockDim.x) {
+  const int total = block_exclusive_scan(flag, pos, np, wt);
+  for (int e = threadIdx.x; e < np; e += blockDim.x) {
     if (flag[e] && pos[e] < k) {
       const int o = pos[e];
       out_idx[o] = (int64_t)b[e] + index_base;
@@ -282,18 +279,170 @@ __device__ void sort_dedup_emit(uint64_t* a, uint64_t* b, uint64_t* c, int* flag
   if (threadIdx.x == 0) *out_count = total < k ? total : k;
 }
 
-// Finalise: unique survivors from the hash table → sorted top-K.
-__global__ void __launch_bounds__(1024) k_sel_finalize(const double* __restrict__ cost, SelState* __restrict__ st,
-                                                       uint64_t* __restrict__ tkeys, uint64_t* __restrict__ tvals,
-                                                       int64_t k, int64_t n, int64_t index_base,
+struct SortSmem {
+  Key2* xchg;
+  uint64_t *a, *b, *c;
+  int *flag, *pos;
+};
+
+__host__ __device__ inline size_t sort_smem_bytes(int n) {
+  return (size_t)n * (sizeof(Key2) + 3 * sizeof(uint64_t) + 2 * sizeof(int));
+}
+
+__device__ inline SortSmem carve_sort(unsigned char* base, int n) {
+  SortSmem s;
+  s.xchg = (Key2*)base;
+  s.a = (uint64_t*)(s.xchg + n);
+  s.b = s.a + n;
+  s.c = s.b + n;
+  s.flag = (int*)(s.c + n);
+  s.pos = s.flag + n;
+  return s;
+}
+
+// Sorted keys → shared arrays, identities for the entries of equal-cost
+// runs (duplicates can only hide there), dedup, emit. Requires
+// kSortE * blockDim.x == kSurvivorCap.
+template <int NSP, int NRED, bool SEED>
+__device__ void sort_ties_emit(const DevSketch& S, const Src& src, Key2 (&kk)[kFinalE], SortSmem& sm, int nvalid,
+                               int64_t k, int64_t* out_idx, double* out_cost, uint64_t* out_id,
+                               int64_t* out_count, int* wt) {
+  block_sort_reg<kFinalE, Key2>(kk, sm.xchg);
+  const int NT = blockDim.x;
+#pragma unroll
+  for (int e = 0; e < kFinalE; ++e) {
+    const int p = e * NT + threadIdx.x;
+    sm.a[p] = kk[e].a;
+    sm.b[p] = kk[e].b;
+  }
+  __syncthreads();
+  const int np = kFinalE * NT;
+  // identities only inside equal-cost runs: the only place duplicates hide
+  for (int p = threadIdx.x; p < np; p += NT) {
+    uint64_t id = kEmpty - 1 - (uint64_t)p;  // unique placeholder, never compared equal
+    if (p < nvalid) {
+      const bool tie = (p > 0 && sm.a[p - 1] == sm.a[p]) || (p + 1 < nvalid && sm.a[p + 1] == sm.a[p]);
+      if (tie) id = identity_at<NSP, NRED, SEED>(S, src, (int64_t)sm.b[p]);
+    }
+    sm.c[p] = id;
+  }
+  __syncthreads();
+  dedup_emit(sm.a, sm.b, sm.c, sm.flag, sm.pos, wt, nvalid, np, k, src.index_base, out_idx, out_cost, nullptr,
+             out_count);
+  if (out_id) {  // identities of the emitted entries, one per thread
+    __syncthreads();
+    const int64_t cnt = *out_count;
+    for (int o = threadIdx.x; o < cnt; o += NT)
+      out_id[o] = identity_at<NSP, NRED, SEED>(S, src, out_idx[o] - src.index_base);
+  }
+}
+
+// Finalise (append path): survivors → sorted, deduplicated top-K.
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(1024) k_sel_finalize(DevSketch S, Src src, SelState* __restrict__ st,
+                                                       const uint64_t* __restrict__ skey,
+                                                       const int64_t* __restrict__ sidx, int64_t k, int64_t n,
                                                        int64_t* __restrict__ out_idx, double* __restrict__ out_cost,
                                                        uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* a = (uint64_t*)smem;
-  uint64_t* b = a + kSurvivorCap;
-  uint64_t* c = b + kSurvivorCap;
-  int* flag = (int*)(c + kSurvivorCap);
-  int* pos = flag + kSurvivorCap;
+  SortSmem sm = carve_sort(smem, kFinalCap);
+  __shared__ int wt[32];
+  const uint32_t ns = st->nsurv;
+  if (ns > (uint32_t)kFinalCap) {  // heavy ties: hash path (host retries)
+    if (threadIdx.x == 0) {
+      st->status |= TT_SEL_OVERFLOW;
+      *out_count = 0;
+    }
+    return;
+  }
+  const int m = (int)ns;
+  Key2 kk[kFinalE];
+#pragma unroll
+  for (int e = 0; e < kFinalE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    kk[e].a = p < m ? skey[p] : kEmpty;
+    kk[e].b = p < m ? (uint64_t)sidx[p] : kEmpty;
+  }
+  sort_ties_emit<NSP, NRED, SEED>(S, src, kk, sm, m, k, out_idx, out_cost, out_id, out_count, wt);
+  if (threadIdx.x == 0) {
+    const int64_t cnt = *out_count;
+    const bool everything = st->all || (int64_t)m >= n;
+    if (cnt < k && !everything) st->status |= TT_SEL_NEED_MORE;  // duplicates ate the margin
+    st->count = cnt;
+  }
+}
+
+// N <= 4096: the whole selection in one CTA.
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Src src, int64_t n, int toggles,
+                                                    int64_t k, SelState* __restrict__ st,
+                                                    int64_t* __restrict__ out_idx, double* __restrict__ out_cost,
+                                                    uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count,
+                                                    int* __restrict__ invalid) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SortSmem sm = carve_sort(smem, kFinalCap);
+  __shared__ int wt[32];
+  bool bad = false;
+  Key2 kk[kFinalE];
+#pragma unroll
+  for (int e = 0; e < kFinalE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    kk[e].a = kEmpty, kk[e].b = kEmpty;
+    if (p < n) {
+      Factors<NSP, NRED> F;
+      load_cand<NSP, NRED, SEED>(S, src, p, F, false);
+      if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
+      kk[e].a = cost_key(draft_cost_of<NSP, NRED>(S, D, F, toggles));
+      kk[e].b = (uint64_t)p;
+    }
+  }
+  if (bad) atomicOr(invalid, 1);
+  sort_ties_emit<NSP, NRED, SEED>(S, src, kk, sm, (int)n, k, out_idx, out_cost, out_id, out_count, wt);
+  if (threadIdx.x == 0 && st) {
+    st->status = 0;
+    st->count = *out_count;
+  }
+}
+
+// ---------------------------------------------- hash fallback (ties) ----
+__device__ __forceinline__ uint64_t slot_hash(uint64_t id) { return scramble64(id + kGolden); }
+
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(256) k_sel_compact_hash(DevSketch S, Src src, const double* __restrict__ cost,
+                                                          int64_t n, SelState* __restrict__ st,
+                                                          uint64_t* __restrict__ tkeys, uint64_t* __restrict__ tvals) {
+  const SelState s = *st;
+  bool overflow = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!survives(cost_key(__ldg(cost + i)), s)) continue;
+    const uint64_t id = identity_at<NSP, NRED, SEED>(S, src, i);
+    uint64_t h = slot_hash(id) & (kTableCap - 1);
+    for (int probes = 0;; ++probes) {
+      const uint64_t prev = atomicCAS((unsigned long long*)&tkeys[h], (unsigned long long)kEmpty,
+                                      (unsigned long long)id);
+      if (prev == kEmpty || prev == id) {
+        atomicMin((unsigned long long*)&tvals[h], (unsigned long long)i);
+        break;
+      }
+      h = (h + 1) & (kTableCap - 1);
+      if (probes >= kTableCap) {
+        overflow = true;
+        break;
+      }
+    }
+  }
+  if (overflow) atomicOr(&st->status, TT_SEL_OVERFLOW);
+}
+
+__global__ void __launch_bounds__(1024) k_sel_finalize_hash(const double* __restrict__ cost, SelState* __restrict__ st,
+                                                            uint64_t* __restrict__ tkeys, uint64_t* __restrict__ tvals,
+                                                            int64_t k, int64_t n, int64_t index_base,
+                                                            int64_t* __restrict__ out_idx,
+                                                            double* __restrict__ out_cost,
+                                                            uint64_t* __restrict__ out_id,
+                                                            int64_t* __restrict__ out_count) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SortSmem sm = carve_sort(smem, kSurvivorCap);
   __shared__ int wt[32];
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
@@ -306,82 +455,47 @@ __global__ void __launch_bounds__(1024) k_sel_finalize(const double* __restrict_
     tkeys[s] = kEmpty;  // restore the empty-table invariant
     tvals[s] = kEmpty;
     const int e = atomicAdd(&cnt, 1);
-    if (e < kSurvivorCap) {
-      a[e] = cost_key(cost[idx]);
-      b[e] = idx;
-      c[e] = id;
-    } else {
-      overflow = true;
-    }
+    if (e < kSurvivorCap) sm.a[e] = cost_key(cost[idx]), sm.b[e] = idx, sm.c[e] = id;
+    else overflow = true;
   }
-  if (overflow) atomicOr(&st->status, TT_SEL_OVERFLOW);
   __syncthreads();
   const int u = cnt < kSurvivorCap ? cnt : kSurvivorCap;
-  const int np = next_pow2(u < 2 ? 2 : u);
-  sort_dedup_emit(a, b, c, flag, pos, wt, u, np, k, index_base, out_idx, out_cost, out_id, out_count);
+  // sort key: (cost, index << 12 | collection slot); the slot finds the
+  // identity again after the sort
+  Key2 kk[kSortE];
+#pragma unroll
+  for (int e = 0; e < kSortE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    kk[e].a = p < u ? sm.a[p] : kEmpty;
+    kk[e].b = p < u ? (((uint64_t)sm.b[p]) << 12) | (uint64_t)p : kEmpty;
+  }
+  __syncthreads();
+  block_sort_reg<kSortE, Key2>(kk, sm.xchg);
+  const int NT = blockDim.x;
+  for (int p = threadIdx.x; p < kSurvivorCap; p += NT) sm.a[p] = sm.c[p];  // identities by slot
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kSortE; ++e) {
+    const int p = e * NT + threadIdx.x;
+    const bool v = p < u;
+    sm.c[p] = v ? sm.a[(int)(kk[e].b & 4095u)] : kEmpty - 1 - (uint64_t)p;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kSortE; ++e) {
+    const int p = e * NT + threadIdx.x;
+    sm.a[p] = kk[e].a;
+    sm.b[p] = kk[e].a == kEmpty ? kEmpty : (kk[e].b >> 12);
+  }
+  __syncthreads();
+  dedup_emit(sm.a, sm.b, sm.c, sm.flag, sm.pos, wt, u, kSurvivorCap, k, index_base, out_idx, out_cost, out_id,
+             out_count);
   if (threadIdx.x == 0) {
-    // fewer unique survivors than K while keys were cut off: raise the target
+    if (overflow) st->status |= TT_SEL_OVERFLOW;
+    else st->status &= ~TT_SEL_OVERFLOW;
     const bool everything = st->all || (int64_t)st->survivors >= n;
-    if (u < k && !everything) atomicOr(&st->status, TT_SEL_NEED_MORE);
-    st->count = u < k ? u : k;
-  }
-}
-
-// N <= 4096: the whole selection in one CTA.
-template <int NSP, int NRED, bool SEED>
-__global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Src src, int64_t n, int toggles,
-                                                    int64_t k, SelState* __restrict__ st,
-                                                    int64_t* __restrict__ out_idx, double* __restrict__ out_cost,
-                                                    uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count,
-                                                    int* __restrict__ invalid) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int np = next_pow2(n < 2 ? 2 : (int)n);
-  uint64_t* a = (uint64_t*)smem;
-  uint64_t* b = a + np;
-  uint64_t* c = b + np;
-  int* flag = (int*)(c + np);
-  int* pos = flag + np;
-  __shared__ int wt[32];
-  bool bad = false;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    Factors<NSP, NRED> F;
-    const uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, false);
-    if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
-    a[i] = cost_key(draft_cost_of<NSP, NRED>(S, D, F, toggles));
-    b[i] = (uint64_t)i;
-    c[i] = id;
-  }
-  if (bad) atomicOr(invalid, 1);
-  for (int e = threadIdx.x + (int)n; e < np; e += blockDim.x) a[e] = kEmpty, b[e] = kEmpty, c[e] = kEmpty;
-  block_bitonic_sort(a, b, c, np);
-  if constexpr (!SEED) {
-    // identities only where a cost tie makes them matter
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      const bool tie = (e > 0 && a[e - 1] == a[e]) || (e + 1 < n && a[e + 1] == a[e]);
-      if (tie) {
-        Factors<NSP, NRED> F;
-        load_factors<NSP, NRED>(src.soa, src.ld, (int64_t)b[e], F, true);
-        c[e] = identity_of<NSP, NRED>(S, F);
-      } else {
-        c[e] = kEmpty - 1 - (uint64_t)e;  // unique placeholder, never compared equal
-      }
-    }
-    __syncthreads();
-  }
-  sort_dedup_emit(a, b, c, flag, pos, wt, (int)n, np, k, src.index_base, out_idx, out_cost, out_id, out_count);
-  if constexpr (!SEED) {
-    if (out_id) {
-      __syncthreads();
-      const int64_t cnt = *out_count;
-      for (int o = threadIdx.x; o < cnt; o += blockDim.x) {
-        Factors<NSP, NRED> F;
-        load_factors<NSP, NRED>(src.soa, src.ld, out_idx[o] - src.index_base, F, true);
-        out_id[o] = identity_of<NSP, NRED>(S, F);
-      }
-    }
-  }
-  if (threadIdx.x == 0 && st) {
-    st->status = 0;
+    if (u < k && !everything) st->status |= TT_SEL_NEED_MORE;
+    else st->status &= ~TT_SEL_NEED_MORE;
     st->count = *out_count;
   }
 }
@@ -392,35 +506,49 @@ __global__ void __launch_bounds__(1024) k_merge(const double* __restrict__ cost,
                                                 int64_t* __restrict__ out_idx, double* __restrict__ out_cost,
                                                 uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int np = next_pow2(m < 2 ? 2 : m);
-  uint64_t* a = (uint64_t*)smem;
-  uint64_t* b = a + np;
-  uint64_t* c = b + np;
-  int* flag = (int*)(c + np);
-  int* pos = flag + np;
+  SortSmem sm = carve_sort(smem, kSurvivorCap);
   __shared__ int wt[32];
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    a[e] = gidx[e] < 0 ? kEmpty : cost_key(cost[e]);  // negative index = empty slot
-    b[e] = gidx[e] < 0 ? kEmpty : (uint64_t)gidx[e];
-    c[e] = gidx[e] < 0 ? kEmpty : id[e];
-  }
   __shared__ int valid;
   if (threadIdx.x == 0) valid = 0;
   __syncthreads();
+  Key2 kk[kSortE];
   int mine = 0;
-  for (int e = threadIdx.x; e < m; e += blockDim.x) mine += gidx[e] >= 0;
+#pragma unroll
+  for (int e = 0; e < kSortE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    const bool v = p < m && gidx[p] >= 0;  // negative index = empty slot
+    // position p in the low 12 bits finds the identity after the sort;
+    // global indices < 2^51 keep the (index, p) order = index order
+    kk[e].a = v ? cost_key(cost[p]) : kEmpty;
+    kk[e].b = v ? (((uint64_t)gidx[p]) << 12) | (uint64_t)p : kEmpty;
+    mine += v;
+  }
   if (mine) atomicAdd(&valid, mine);
+  block_sort_reg<kSortE, Key2>(kk, sm.xchg);
+  const int NT = blockDim.x;
+#pragma unroll
+  for (int e = 0; e < kSortE; ++e) {
+    const int p = e * NT + threadIdx.x;
+    const bool v = kk[e].a != kEmpty;
+    sm.a[p] = kk[e].a;
+    sm.b[p] = v ? (kk[e].b >> 12) : kEmpty;
+    sm.c[p] = v ? id[kk[e].b & 4095u] : kEmpty - 1 - (uint64_t)p;
+  }
   __syncthreads();
-  // empty slots carry all-ones keys, sort last and fall outside `valid`
-  sort_dedup_emit(a, b, c, flag, pos, wt, valid, np, k, 0, out_idx, out_cost, out_id, out_count);
+  dedup_emit(sm.a, sm.b, sm.c, sm.flag, sm.pos, wt, valid, kSurvivorCap, k, 0, out_idx, out_cost, out_id, out_count);
 }
 
 // ------------------------------------------------------------ launchers ----
-size_t small_select_smem(int64_t n);
 static int grid_for(int64_t n, int threads, int max_blocks) {
   int64_t g = (n + threads - 1) / threads;
   if (g > max_blocks) g = max_blocks;
   return (int)(g < 1 ? 1 : g);
+}
+
+template <typename F>
+static void set_smem(F* f, size_t bytes) {
+  static_assert(sizeof(F*) > 0, "");
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 int launch_generate(const DevSketch& S, uint64_t s0, int64_t first, int64_t n, int32_t* soa, int64_t ld,
@@ -456,63 +584,96 @@ int launch_draft_cost(const DevSketch& S, const DevDevice& D, const int32_t* soa
 template <int NSP, int NRED, bool SEED>
 static void run_small(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
                       SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id, int64_t* out_count,
-                      size_t sm, cudaStream_t st) {
-  auto f = k_sel_small<NSP, NRED, SEED>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  tt::note_launch(), f<<<1, 1024, sm, st>>>(S, D, src, n, toggles, k, w.state, out_idx, out_cost, out_id, out_count, w.invalid);
+                      cudaStream_t st) {
+  const size_t sm = sort_smem_bytes(kFinalCap);
+  static bool init = false;
+  if (!init) set_smem(k_sel_small<NSP, NRED, SEED>, sm), init = true;
+  tt::note_launch();
+  k_sel_small<NSP, NRED, SEED><<<1, kFinalCap / kFinalE, sm, st>>>(S, D, src, n, toggles, k, w.state, out_idx,
+                                                                   out_cost, out_id, out_count, w.invalid);
 }
 
-size_t small_select_smem(int64_t n) {
-  const int np = next_pow2(n < 2 ? 2 : (int)n);
-  return (size_t)np * (3 * sizeof(uint64_t) + 2 * sizeof(int));
+template <int NSP, int NRED, bool SEED>
+static void run_tail(const DevSketch& S, const Src& src, int64_t n, int64_t k, bool hash, SelScratch& w,
+                     int64_t* out_idx, double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st) {
+  const size_t sm = sort_smem_bytes(kSurvivorCap);
+  const int g = grid_for(n, 256, 148 * 8);
+  if (!hash) {
+    tt::note_launch();
+    k_sel_compact<<<g, 256, 0, st>>>(w.cost, n, w.state, w.skey, w.sidx);
+    const size_t smf = sort_smem_bytes(kFinalCap);
+    static bool init = false;
+    if (!init) set_smem(k_sel_finalize<NSP, NRED, SEED>, smf), init = true;
+    tt::note_launch();
+    k_sel_finalize<NSP, NRED, SEED><<<1, kFinalCap / kFinalE, smf, st>>>(S, src, w.state, w.skey, w.sidx, k, n,
+                                                                         out_idx, out_cost, out_id, out_count);
+  } else {
+    tt::note_launch();
+    k_sel_compact_hash<NSP, NRED, SEED><<<g, 256, 0, st>>>(S, src, w.cost, n, w.state, w.tkeys, w.tvals);
+    static bool init = false;
+    if (!init) set_smem(k_sel_finalize_hash, sm), init = true;
+    tt::note_launch();
+    k_sel_finalize_hash<<<1, kSurvivorCap / kSortE, sm, st>>>(w.cost, w.state, w.tkeys, w.tvals, k, n,
+                                                              src.index_base, out_idx, out_cost, out_id, out_count);
+  }
 }
 
 int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, int64_t ld, uint64_t s0,
                   int64_t first, bool seeded, int64_t n, int64_t k, int64_t need, int toggles,
                   int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
-                  int64_t* out_count, cudaStream_t st) {
+                  int64_t* out_count, cudaStream_t st, bool hash) {
   Src src{soa, ld, s0, first, index_base};
   if (n <= kSmallSelectMax) {
-    const size_t sm = small_select_smem(n);
     if (seeded)
-      return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, true>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, sm, st)));
-    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, false>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, sm, st)));
+      return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, true>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
+    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, false>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
   }
   {
     int rc = launch_draft_cost(S, D, soa, ld, s0, first, seeded, n, toggles, w.cost, w.hist, w.invalid, st);
     if (rc) return rc;
   }
-  tt::note_launch(), k_sel_scan<<<1, 1024, 0, st>>>(w.hist, w.state, need, n, 0);
+  tt::note_launch();
+  k_sel_scan<<<1, 1024, 0, st>>>(w.hist, w.state, need, 0);
   for (int lv = 1; lv <= 2; ++lv) {
     const int g = grid_for(n, 256, 148 * 8);
-    tt::note_launch(), k_sel_refine<<<g, 256, 0, st>>>(w.cost, n, w.state, w.hist);
-    tt::note_launch(), k_sel_scan<<<1, 1024, 0, st>>>(w.hist, w.state, need, n, lv);
+    tt::note_launch();
+    k_sel_refine<<<g, 256, 0, st>>>(w.cost, n, w.state, w.hist);
+    tt::note_launch();
+    k_sel_scan<<<1, 1024, 0, st>>>(w.hist, w.state, need, lv);
   }
-  {
-    const int g = grid_for(n, 256, 148 * 8);
-    int rc;
-    if (seeded)
-      rc = TT_DISPATCH_SHAPE(S.n_sp, S.n_red,
-                             (tt::note_launch(), k_sel_compact<NSP, NRED, true><<<g, 256, 0, st>>>(S, src, w.cost, n, w.state, w.tkeys, w.tvals)));
-    else
-      rc = TT_DISPATCH_SHAPE(S.n_sp, S.n_red,
-                             (tt::note_launch(), k_sel_compact<NSP, NRED, false><<<g, 256, 0, st>>>(S, src, w.cost, n, w.state, w.tkeys, w.tvals)));
-    if (rc) return rc;
-  }
-  const size_t sm = (size_t)kSurvivorCap * (3 * sizeof(uint64_t) + 2 * sizeof(int));
-  cudaFuncSetAttribute(k_sel_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  tt::note_launch(), k_sel_finalize<<<1, 1024, sm, st>>>(w.cost, w.state, w.tkeys, w.tvals, k, n, index_base, out_idx, out_cost,
-                                      out_id, out_count);
-  return 0;
+  if (seeded)
+    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_tail<NSP, NRED, true>(S, src, n, k, hash, w, out_idx, out_cost, out_id, out_count, st)));
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_tail<NSP, NRED, false>(S, src, n, k, hash, w, out_idx, out_cost, out_id, out_count, st)));
+}
+
+// Identities of the b selected candidates, written into the round record
+// (positions pos[e] of the drafted index list idx).
+template <int NSP, int NRED, bool SEED>
+__global__ void k_selected_identity(DevSketch S, Src src, const int64_t* __restrict__ pos,
+                                    const int64_t* __restrict__ pos_count, const int64_t* __restrict__ idx, int64_t b,
+                                    uint64_t* __restrict__ out) {
+  const int64_t cnt = *pos_count;
+  for (int64_t e = threadIdx.x; e < b; e += blockDim.x)
+    out[e] = e < cnt ? identity_at<NSP, NRED, SEED>(S, src, idx[pos[e]] - src.index_base) : 0;
+}
+
+int launch_selected_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
+                             bool seeded, const int64_t* pos, const int64_t* pos_count, const int64_t* idx, int64_t b,
+                             uint64_t* out, cudaStream_t st) {
+  Src src{soa, ld, s0, first, first};
+  if (seeded)
+    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_selected_identity<NSP, NRED, true><<<1, 32, 0, st>>>(S, src, pos, pos_count, idx, b, out)));
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_selected_identity<NSP, NRED, false><<<1, 32, 0, st>>>(S, src, pos, pos_count, idx, b, out)));
 }
 
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st) {
   if (m > kSurvivorCap) return -1;
-  const int np = next_pow2(m < 2 ? 2 : m);
-  const size_t sm = (size_t)np * (3 * sizeof(uint64_t) + 2 * sizeof(int));
-  cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  tt::note_launch(), k_merge<<<1, 1024, sm, st>>>(cost, gidx, id, m, k, out_idx, out_cost, out_id, out_count);
+  const size_t sm = sort_smem_bytes(kSurvivorCap);
+  static bool init = false;
+  if (!init) set_smem(k_merge, sm), init = true;
+  tt::note_launch();
+  k_merge<<<1, kSurvivorCap / kSortE, sm, st>>>(cost, gidx, id, m, k, out_idx, out_cost, out_id, out_count);
   return 0;
 }
 

@@ -22,115 +22,193 @@ __device__ __forceinline__ uint64_t ordered(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-struct TopbScratch {
-  uint64_t* a;
-  uint64_t* b;
-  uint64_t* c;
-};
+constexpr int kTopbE = 4;  // keys per thread
 
-// Phase 1: each CTA sorts one tile and keeps its b best.
+// Phase 1: each CTA sorts one tile of up to 4 * blockDim keys
+// (~score, draft, index) in registers and keeps its b best. With
+// final_out the CTA writes the answer directly.
 __global__ void __launch_bounds__(1024) k_topb_tile(const double* __restrict__ scores, const double* __restrict__ drafts,
                                                     const uint8_t* __restrict__ excluded, int64_t n,
                                                     const int64_t* __restrict__ n_dev, int64_t b, int final_out,
-                                                    uint64_t* __restrict__ wa, uint64_t* __restrict__ wb,
-                                                    uint64_t* __restrict__ wc, int64_t* __restrict__ out_pos,
+                                                    Key3* __restrict__ win, int64_t* __restrict__ out_pos,
                                                     int64_t* __restrict__ out_count, int* __restrict__ status) {
-  extern __shared__ __align__(16) uint64_t sk[];
-  uint64_t* a = sk;
-  uint64_t* bb = a + kSelTile;
-  uint64_t* c = bb + kSelTile;
+  extern __shared__ __align__(16) unsigned char sraw[];
+  Key3* xchg = (Key3*)sraw;
   __shared__ int avail;
   if (n_dev) n = *n_dev < n ? *n_dev : n;
-  const int64_t base = (int64_t)blockIdx.x * kSelTile;
-  const int m = (int)((n - base) < kSelTile ? (n - base) : kSelTile);
-  const int np = next_pow2(m < 2 ? 2 : m);
+  const int tile = kTopbE * blockDim.x;
+  const int64_t base = (int64_t)blockIdx.x * tile;
   if (threadIdx.x == 0) avail = 0;
   __syncthreads();
   int mine = 0;
-  for (int e = threadIdx.x; e < np; e += blockDim.x) {
-    const int64_t i = base + e;
-    const bool ok = e < m && !(excluded && excluded[i]);
-    a[e] = ok ? ~ordered(scores[i]) : kAll;
-    bb[e] = ok ? ordered(drafts[i]) : kAll;
-    c[e] = ok ? (uint64_t)i : kAll;
+  Key3 kk[kTopbE];
+#pragma unroll
+  for (int e = 0; e < kTopbE; ++e) {
+    const int64_t i = base + e * blockDim.x + threadIdx.x;
+    const bool ok = i < n && !(excluded && excluded[i]);
+    kk[e].a = ok ? ~ordered(scores[i]) : kAll;
+    kk[e].b = ok ? ordered(drafts[i]) : kAll;
+    kk[e].c = ok ? (uint32_t)i : 0xffffffffu;
     mine += ok;
   }
   if (mine) atomicAdd(&avail, mine);
-  block_bitonic_sort<true>(a, bb, c, np);
+  block_sort_reg<kTopbE, Key3>(kk, xchg);
   const int keep = (int)(b < avail ? b : avail);
-  if (final_out) {
-    for (int e = threadIdx.x; e < keep; e += blockDim.x) out_pos[e] = (int64_t)c[e];
-    if (threadIdx.x == 0) {
-      *out_count = keep;
-      *status = avail < b ? 1 : 0;
+#pragma unroll
+  for (int e = 0; e < kTopbE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    if (p < b) {
+      if (final_out) {
+        if (p < keep) out_pos[p] = (int64_t)kk[e].c;
+      } else {
+        Key3 w = kk[e];
+        if (p >= keep) w.a = kAll, w.b = kAll, w.c = 0xffffffffu;
+        win[(int64_t)blockIdx.x * b + p] = w;
+      }
     }
-  } else {
-    for (int e = threadIdx.x; e < b; e += blockDim.x) {
-      const int64_t o = (int64_t)blockIdx.x * b + e;
-      wa[o] = e < keep ? a[e] : kAll;
-      wb[o] = e < keep ? bb[e] : kAll;
-      wc[o] = e < keep ? c[e] : kAll;
-    }
+  }
+  if (final_out && threadIdx.x == 0) {
+    *out_count = keep;
+    *status = avail < b ? 1 : 0;
   }
 }
 
-// Phase 2: merge the tiles' winners.
-__global__ void __launch_bounds__(1024) k_topb_merge(const uint64_t* __restrict__ wa, const uint64_t* __restrict__ wb,
-                                                     const uint64_t* __restrict__ wc, int m, int64_t b,
+// Phase 2: merge the tiles' winners (all of them fit one CTA).
+__global__ void __launch_bounds__(1024) k_topb_merge(const Key3* __restrict__ win, int m, int64_t b,
                                                      int64_t* __restrict__ out_pos, int64_t* __restrict__ out_count,
                                                      int* __restrict__ status) {
-  extern __shared__ __align__(16) uint64_t sk[];
-  const int np = next_pow2(m < 2 ? 2 : m);
-  uint64_t* a = sk;
-  uint64_t* bb = a + np;
-  uint64_t* c = bb + np;
+  extern __shared__ __align__(16) unsigned char sraw[];
+  Key3* xchg = (Key3*)sraw;
   __shared__ int avail;
   if (threadIdx.x == 0) avail = 0;
   __syncthreads();
   int mine = 0;
-  for (int e = threadIdx.x; e < np; e += blockDim.x) {
-    a[e] = e < m ? wa[e] : kAll;
-    bb[e] = e < m ? wb[e] : kAll;
-    c[e] = e < m ? wc[e] : kAll;
-    mine += e < m && c[e] != kAll;
+  Key3 kk[kTopbE];
+#pragma unroll
+  for (int e = 0; e < kTopbE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    if (p < m) kk[e] = win[p];
+    else kk[e].a = kAll, kk[e].b = kAll, kk[e].c = 0xffffffffu;
+    mine += p < m && kk[e].a != kAll;
   }
   if (mine) atomicAdd(&avail, mine);
-  block_bitonic_sort<true>(a, bb, c, np);
+  block_sort_reg<kTopbE, Key3>(kk, xchg);
   const int keep = (int)(b < avail ? b : avail);
-  for (int e = threadIdx.x; e < keep; e += blockDim.x) out_pos[e] = (int64_t)c[e];
+#pragma unroll
+  for (int e = 0; e < kTopbE; ++e) {
+    const int p = e * blockDim.x + threadIdx.x;
+    if (p < keep) out_pos[p] = (int64_t)kk[e].c;
+  }
   if (threadIdx.x == 0) {
     *out_count = keep;
     *status = avail < b ? 1 : 0;
   }
 }
 
-// Scratch for phase 1 winners lives in a static device buffer sized for
-// the largest supported call (tiles * b <= kSelTile).
-__device__ uint64_t g_topb_a[kSelTile], g_topb_b[kSelTile], g_topb_c[kSelTile];
+// Small b over one tile (the round's case: b = 10 of K = 512): b rounds of
+// a CTA-wide arg-min over the (~score, draft, index) keys — O(b * n) work
+// instead of a full sorting network.
+constexpr int kArgThreads = 256;
+
+__device__ __forceinline__ Key3 kmin(const Key3& x, const Key3& y) { return y.lt(x) ? y : x; }
+
+__global__ void __launch_bounds__(kArgThreads) k_topb_argmin(const double* __restrict__ scores,
+                                                             const double* __restrict__ drafts,
+                                                             const uint8_t* __restrict__ excluded, int64_t n,
+                                                             const int64_t* __restrict__ n_dev, int64_t b,
+                                                             int64_t* __restrict__ out_pos,
+                                                             int64_t* __restrict__ out_count, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  Key3* ks = (Key3*)sraw;
+  __shared__ Key3 wbest[kArgThreads / 32];
+  __shared__ int avail;
+  if (n_dev) n = *n_dev < n ? *n_dev : n;
+  if (threadIdx.x == 0) avail = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const bool ok = !(excluded && excluded[i]);
+    Key3 k;
+    k.a = ok ? ~ordered(scores[i]) : kAll;
+    k.b = ok ? ordered(drafts[i]) : kAll;
+    k.c = ok ? (uint32_t)i : 0xffffffffu;
+    ks[i] = k;
+    mine += ok;
+  }
+  if (mine) atomicAdd(&avail, mine);
+  __syncthreads();
+  const int keep = (int)(b < avail ? b : avail);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int it = 0; it < keep; ++it) {
+    Key3 best;
+    best.a = kAll, best.b = kAll, best.c = 0xffffffffu;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) best = kmin(best, ks[i]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) best = kmin(best, best.shfl_xor(off));
+    if (lane == 0) wbest[warp] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Key3 m = wbest[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = kmin(m, wbest[w]);
+      out_pos[it] = (int64_t)m.c;
+      ks[m.c].a = kAll, ks[m.c].b = kAll, ks[m.c].c = 0xffffffffu;  // taken
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_count = keep;
+    *status = avail < b ? 1 : 0;
+  }
+}
+
+// Scratch for phase-1 winners (tiles * b <= kSelTile).
+__device__ Key3 g_topb_win[kSelTile];
+
+static int threads_for(int64_t m) {
+  int nt = 32;
+  while (nt < 1024 && (int64_t)kTopbE * nt < m) nt <<= 1;
+  return nt;
+}
 
 int launch_select_top(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n,
                       const int64_t* n_dev, int64_t b, int64_t* out_pos, int64_t* out_count, int* status,
                       cudaStream_t st) {
-  if (b < 1 || n < 0) return -1;
+  if (b < 1 || n < 0 || n >= (int64_t{1} << 32)) return -1;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_topb_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelTile * sizeof(Key3)));
+    cudaFuncSetAttribute(k_topb_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelTile * sizeof(Key3)));
+    init = true;
+  }
   const int64_t tiles = (n + kSelTile - 1) / kSelTile;
-  const size_t sm1 = (size_t)kSelTile * 3 * sizeof(uint64_t);
-  cudaFuncSetAttribute(k_topb_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+  if (tiles <= 1 && b <= 32) {
+    static bool init2 = false;
+    if (!init2) {
+      cudaFuncSetAttribute(k_topb_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSelTile * sizeof(Key3)));
+      init2 = true;
+    }
+    tt::note_launch();
+    k_topb_argmin<<<1, kArgThreads, (n > 0 ? n : 1) * sizeof(Key3), st>>>(scores, drafts, excluded, n, n_dev, b,
+                                                                          out_pos, out_count, status);
+    return 0;
+  }
   if (tiles <= 1) {
-    tt::note_launch(), k_topb_tile<<<1, 1024, sm1, st>>>(scores, drafts, excluded, n, n_dev, b, 1, nullptr, nullptr, nullptr, out_pos,
-                                      out_count, status);
+    const int nt = threads_for(n);
+    tt::note_launch();
+    k_topb_tile<<<1, nt, kTopbE * nt * sizeof(Key3), st>>>(scores, drafts, excluded, n, n_dev, b, 1, nullptr, out_pos,
+                                                           out_count, status);
     return 0;
   }
   if (b > kSelTile || tiles * b > kSelTile) return -2;
-  uint64_t *wa, *wb, *wc;
-  cudaGetSymbolAddress((void**)&wa, g_topb_a);
-  cudaGetSymbolAddress((void**)&wb, g_topb_b);
-  cudaGetSymbolAddress((void**)&wc, g_topb_c);
-  tt::note_launch(), k_topb_tile<<<(unsigned)tiles, 1024, sm1, st>>>(scores, drafts, excluded, n, n_dev, b, 0, wa, wb, wc, out_pos,
-                                                  out_count, status);
+  Key3* win;
+  cudaGetSymbolAddress((void**)&win, g_topb_win);
+  tt::note_launch();
+  k_topb_tile<<<(unsigned)tiles, 1024, kSelTile * sizeof(Key3), st>>>(scores, drafts, excluded, n, n_dev, b, 0, win,
+                                                                      out_pos, out_count, status);
   const int m = (int)(tiles * b);
-  const size_t sm2 = (size_t)next_pow2(m) * 3 * sizeof(uint64_t);
-  cudaFuncSetAttribute(k_topb_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-  tt::note_launch(), k_topb_merge<<<1, 1024, sm2, st>>>(wa, wb, wc, m, b, out_pos, out_count, status);
+  const int nt = threads_for(m);
+  tt::note_launch();
+  k_topb_merge<<<1, nt, kTopbE * nt * sizeof(Key3), st>>>(win, m, b, out_pos, out_count, status);
   return 0;
 }
 

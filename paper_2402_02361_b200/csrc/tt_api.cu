@@ -58,6 +58,7 @@ struct tt_ctx {
   int64_t last_ld = 0;
   uint64_t last_seed = 0;
   int64_t last_need = 0;
+  bool last_hash = false;
   // stage profiling with CUDA events on the ctx stream
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -260,6 +261,12 @@ int compile_sketch(tt_ctx* ctx, const tt_sketch* sk, DevSketch& S) {
       if (S.n_prime >= TT_MAX_PRIMES) return fail(ctx, TT_E_VALIDATE, "op: too many distinct prime factors");
       const int q = S.n_prime++;
       S.pr_axis[q] = a, S.pr_e[q] = e, S.pr_p[q] = p;
+      if (p & 1) {  // modular inverse of odd p mod 2^32 (Newton), divisibility limit
+        uint32_t inv = (uint32_t)p;
+        for (int it = 0; it < 5; ++it) inv *= 2u - (uint32_t)p * inv;
+        S.pr_inv[q] = inv;
+        S.pr_lim[q] = 0xffffffffu / (uint32_t)p;
+      }
       S.pr_count[q] = binom_sat(e + S.arity[a] - 1, S.arity[a] - 1);
       space = sat_mul(space, S.pr_count[q]);
     }
@@ -331,6 +338,7 @@ int select_sync(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const int32
                 int64_t first, bool seeded, int64_t n, int64_t k, int toggles, int64_t index_base, int64_t* idx,
                 double* cost, uint64_t* id, int64_t* count_host) {
   int64_t need = k + k / 8 + 16;
+  bool hash = false;
   for (int attempt = 0; attempt < 64; ++attempt) {
     TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
     if (n > kSmallSelectMax) {
@@ -338,7 +346,7 @@ int select_sync(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const int32
       if (rc) return rc;
     }
     if (launch_select(S, D, soa, ld, s0, first, seeded, n, k, need, toggles, index_base, ctx->sel, idx, cost, id,
-                      ctx->d_count, ctx->stream))
+                      ctx->d_count, ctx->stream, hash))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
     SelState st;
@@ -348,8 +356,12 @@ int select_sync(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const int32
     int rc = sync_check(ctx);
     if (rc) return rc;
     if (invalid) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule (factor products / unroll)");
-    if (n > kSmallSelectMax && (st.status & TT_SEL_OVERFLOW))
-      return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
+    if (n > kSmallSelectMax && (st.status & TT_SEL_OVERFLOW)) {
+      if (hash)
+        return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
+      hash = true;  // > 4096 keys share the threshold prefix: dedup on insert
+      continue;
+    }
     if (n > kSmallSelectMax && (st.status & TT_SEL_NEED_MORE)) {
       need *= 2;
       continue;
@@ -402,6 +414,8 @@ int tt_ctx_create(int device, tt_ctx** out) {
   c->stream = c->own;
   if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.hist, 0, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.skey, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.sidx, 4096 * sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.tkeys, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.tvals, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.tkeys, 0xff, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
@@ -424,7 +438,10 @@ void tt_ctx_destroy(tt_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.tkeys, c->sel.tvals, c->sel.state, c->sel.invalid,
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& pr : c->ev_live) cudaEventDestroy(pr.second.first), cudaEventDestroy(pr.second.second);
+  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.skey, c->sel.sidx, c->sel.tkeys, c->sel.tvals, c->sel.state,
+                  c->sel.invalid,
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed};
@@ -688,6 +705,9 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
 }
 
 // Everything after the drafted set exists on the device.
+// ref: how the drafted candidates are addressed (SoA / counter stream /
+// identities). Identities of the b selections come from d_id for merged
+// rounds, otherwise they are computed for those b only.
 int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg,
                       CandRef ref) {
   int rc = score_drafted(ctx, S, D, ref, cfg->k, cfg->precision, cfg->b, cfg->band > 0 ? cfg->band : 0.05,
@@ -697,8 +717,13 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
   prof_begin(ctx, 3);
   launch_select_top(ctx->d_score, ctx->d_cost, certified ? ctx->d_excluded : nullptr, cfg->k, ctx->d_count, cfg->b,
                     ctx->d_pos, ctx->d_pos_count, ctx->d_status, ctx->stream);
+  const bool by_id = ref.id != nullptr;
   launch_gather(ctx->d_pos, ctx->d_pos_count, ctx->d_count, ctx->sel.state, nullptr, ctx->d_sublist_count,
-                ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, cfg->b, ctx->d_record, ctx->stream);
+                ctx->d_idx, ctx->d_cost, by_id ? ctx->d_id : nullptr, ctx->d_score, cfg->b, ctx->d_record, ctx->stream);
+  if (!by_id)
+    launch_selected_identity(S, ref.soa, ref.ld, ref.s0, ref.seeded ? cfg->first : ref.index_base, ref.seeded != 0,
+                             ctx->d_pos, ctx->d_pos_count, ctx->d_idx, cfg->b,
+                             (uint64_t*)(ctx->d_record + 4 + 3 * cfg->b), ctx->stream);
   prof_end(ctx, 3);
   TT_LAUNCHED(ctx);
   TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_record, ctx->d_record, sizeof(int64_t) * (4 + 4 * cfg->b),
@@ -717,7 +742,7 @@ int check_round_cfg(tt_ctx* ctx, const tt_round_config* cfg) {
 }
 
 int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
-                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need) {
+                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need, bool hash = false) {
   DevSketch S;
   DevDevice D;
   int rc = compile_sketch(ctx, sk, S);
@@ -732,12 +757,16 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
   prof_begin(ctx, 0);
   if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k, need, cfg->toggles,
-                    cfg->first, ctx->sel, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->stream))
+                    cfg->first, ctx->sel, ctx->d_idx, ctx->d_cost, nullptr, ctx->d_count, ctx->stream, hash))
     return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
   prof_end(ctx, 0);
   TT_LAUNCHED(ctx);
-  CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
+  // the verifier re-derives each drafted candidate from its population
+  // index: a SoA gather, or a counter-based regeneration
+  CandRef ref = seeded ? CandRef{nullptr, 0, ctx->d_idx, 0, nullptr, seed_state(seed), 1, 0}
+                       : CandRef{soa, ld, ctx->d_idx, cfg->first, nullptr, 0, 0, 0};
   if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  ctx->last_hash = hash;
   ctx->pending = true;
   ctx->last_b = cfg->b;
   ctx->last_k = cfg->k;
@@ -758,20 +787,31 @@ int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* se
   ctx->pending = false;
   if (rc) return rc;
   const int64_t b = ctx->last_b;
-  if (((int)ctx->h_record[2] & TT_SEL_NEED_MORE) && allow_retry) {
-    // duplicates consumed the selector's margin: raise the target, redo
-    int64_t need = ctx->last_need * 2;
+  const int retry_mask = TT_SEL_NEED_MORE | TT_SEL_OVERFLOW;
+  if (((int)ctx->h_record[2] & retry_mask) && allow_retry) {
+    // NEED_MORE: duplicates consumed the selector's margin → raise the
+    // target; OVERFLOW: > 4096 keys tie at the threshold → hash path
+    int64_t need = ctx->last_need;
+    bool hash = ctx->last_hash;
     bool ok = false;
-    for (int attempt = 0; attempt < 62 && !ok; ++attempt, need *= 2) {
+    for (int attempt = 0; attempt < 62 && !ok; ++attempt) {
+      const int st = (int)ctx->h_record[2];
+      if (st & TT_SEL_OVERFLOW) {
+        if (hash) break;
+        hash = true;
+      } else {
+        need *= 2;
+      }
       tt_round_config cfg = ctx->last_cfg;
       if ((rc = round_enqueue(ctx, &ctx->last_sketch, &ctx->last_dev, &cfg, ctx->last_soa, ctx->last_ld,
-                              ctx->last_seed, need)))
+                              ctx->last_seed, need, hash)))
         return rc;
       if ((rc = sync_check(ctx))) return rc;
       ctx->pending = false;
-      ok = !((int)ctx->h_record[2] & TT_SEL_NEED_MORE);
+      ok = !((int)ctx->h_record[2] & retry_mask);
     }
-    if (!ok) return fail(ctx, TT_E_STATE, "draft selector did not converge");
+    if (!ok && ((int)ctx->h_record[2] & TT_SEL_NEED_MORE))
+      return fail(ctx, TT_E_STATE, "draft selector did not converge");
   }
   const int64_t* rec = ctx->h_record;
   const int status = (int)rec[2];

@@ -76,6 +76,106 @@ __device__ __forceinline__ int block_exclusive_scan(const int* flags, int* out, 
   return total;
 }
 
+// ---- register/shuffle bitonic sort -------------------------------------
+// Every thread holds E keys at positions p = e * NT + t (NT = blockDim.x, a
+// multiple of 32). Exchanges with partner p ^ stride run in registers when
+// stride >= NT, through warp shuffles when stride < 32, and through shared
+// memory otherwise — so most of the log^2 n stages never touch shared
+// memory. Keys must be strictly ordered (the callers append a unique index).
+// The comparators are written branch-free: with the short-circuit form,
+// ptxas 12.9 -O3 produced a network that duplicated tied-prefix keys at
+// 1024 threads under register pressure (tools/dbg_sort.cu reproduces it;
+// -Xptxas -O0 and the branch-free form both sort correctly).
+struct Key2 {  // (a, b) lexicographic
+  uint64_t a, b;
+  __host__ __device__ __forceinline__ bool lt(const Key2& o) const {
+    const bool alt = a < o.a, aeq = a == o.a, blt = b < o.b;
+    return alt | (aeq & blt);
+  }
+  __device__ __forceinline__ Key2 shfl_xor(int m) const {
+    Key2 r;
+    r.a = __shfl_xor_sync(0xffffffffu, a, m);
+    r.b = __shfl_xor_sync(0xffffffffu, b, m);
+    return r;
+  }
+};
+
+struct Key3 {  // (a, b, c) lexicographic
+  uint64_t a, b;
+  uint32_t c;
+  __host__ __device__ __forceinline__ bool lt(const Key3& o) const {
+    // branch-free form (see block_sort_reg note on ptxas)
+    const bool alt = a < o.a, aeq = a == o.a, blt = b < o.b, beq = b == o.b, clt = c < o.c;
+    return alt | (aeq & (blt | (beq & clt)));
+  }
+  __device__ __forceinline__ Key3 shfl_xor(int m) const {
+    Key3 r;
+    r.a = __shfl_xor_sync(0xffffffffu, a, m);
+    r.b = __shfl_xor_sync(0xffffffffu, b, m);
+    r.c = __shfl_xor_sync(0xffffffffu, c, m);
+    return r;
+  }
+};
+
+// Sorts the n = E * blockDim.x keys ascending; `xchg` = shared scratch of n keys.
+template <int E, typename K>
+__device__ __forceinline__ void block_sort_reg(K (&k)[E], K* xchg) {
+  const int NT = blockDim.x;
+  const int t = threadIdx.x;
+  const int n = E * NT;
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= NT) {
+        // in-register stage; ES is a compile-time constant in every branch so
+        // k[] stays in registers (a runtime register index would spill it)
+        const int es = stride / NT;
+#pragma unroll
+        for (int ES = 1; ES < E; ES <<= 1) {
+          if (es == ES) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int f = e ^ ES;
+              if (f > e) {
+                const int p = e * NT + t;
+                const bool up = (p & size) == 0;
+                const bool sw = up ? k[f].lt(k[e]) : k[e].lt(k[f]);
+                if (sw) {
+                  const K tmp = k[e];
+                  k[e] = k[f];
+                  k[f] = tmp;
+                }
+              }
+            }
+          }
+        }
+      } else if (stride >= 32) {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) xchg[e * NT + t] = k[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e * NT + t;
+          const K o = xchg[p ^ stride];
+          const bool lower = (p & stride) == 0, up = (p & size) == 0;
+          const bool take = (lower == up) ? o.lt(k[e]) : k[e].lt(o);
+          if (take) k[e] = o;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e * NT + t;
+          const K o = k[e].shfl_xor(stride);
+          const bool lower = (p & stride) == 0, up = (p & size) == 0;
+          const bool take = (lower == up) ? o.lt(k[e]) : k[e].lt(o);
+          if (take) k[e] = o;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 __host__ __device__ __forceinline__ int next_pow2(int v) {
   int p = 1;
   while (p < v) p <<= 1;

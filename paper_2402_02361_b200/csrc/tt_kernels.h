@@ -13,7 +13,7 @@ namespace tt {
 // Kernel launches issued by this library (tt_kernel_launches()).
 void note_launch();
 
-constexpr int64_t kSmallSelectMax = 4096;
+constexpr int64_t kSmallSelectMax = 1024;
 
 enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2 };
 
@@ -29,13 +29,17 @@ struct SelState {
   uint32_t survivors;
   uint32_t unique;
   int64_t count;
+  uint32_t nsurv;  // appended survivors
+  uint32_t _pad;
 };
 
 struct SelScratch {
   double* cost = nullptr;  // N costs
   int64_t cost_cap = 0;
   uint32_t* hist = nullptr;  // 4096 bins, zero between uses
-  uint64_t* tkeys = nullptr;  // hash table, all-ones between uses
+  uint64_t* skey = nullptr;  // 4096 survivor keys
+  int64_t* sidx = nullptr;   // 4096 survivor indices
+  uint64_t* tkeys = nullptr;  // hash table (tie fallback), all-ones between uses
   uint64_t* tvals = nullptr;
   SelState* state = nullptr;
   int* invalid = nullptr;
@@ -54,20 +58,26 @@ int launch_draft_cost(const DevSketch& S, const DevDevice& D, const int32_t* soa
 int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, int64_t ld, uint64_t s0,
                   int64_t first, bool seeded, int64_t n, int64_t k, int64_t need, int toggles,
                   int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
-                  int64_t* out_count, cudaStream_t st);
+                  int64_t* out_count, cudaStream_t st, bool hash = false);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);
+int launch_selected_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
+                             bool seeded, const int64_t* pos, const int64_t* pos_count, const int64_t* idx, int64_t b,
+                             uint64_t* out, cudaStream_t st);
 
 // k_pacm64.cu — fp64 PaCM (parity mode / certification rescoring)
 // Candidates are addressed by identity (population-independent) or by
 // (soa, ld, local index). `list`/`count` optionally restrict scoring to a
 // device-side sublist of positions (count read on device).
 struct CandRef {
-  const int32_t* soa;  // nullptr → reconstruct from identities
+  const int32_t* soa;  // explicit population (SoA) ...
   int64_t ld;
-  const int64_t* idx;  // population index per position (minus index_base)
+  const int64_t* idx;  // population index per position (soa: minus index_base)
   int64_t index_base;
-  const uint64_t* id;  // identities per position (when soa == nullptr)
+  const uint64_t* id;  // ... or identities per position ...
+  uint64_t s0;         // ... or the counter-based stream: schedule idx[pos]
+  int32_t seeded;
+  int32_t _pad;
 };
 int launch_features64(const DevSketch& S, const DevDevice& D, CandRef ref, int64_t k, double* stmt_out,
                       double* block_out, cudaStream_t st);
