@@ -1,15 +1,372 @@
-// k_pacm_tc.cu — tcgen05/TMEM PaCM (placeholder until the tensor-core
-// kernel lands; the fp64 path serves every precision request meanwhile).
+// k_pacm_tc.cu — fused features + PaCM forward on the 5th-gen tensor cores.
+//
+// run_forward (ranker.cpp:159-209) for a tile of 16 candidates per CTA:
+// every candidate contributes 8 rows (its <= 8 statement vectors, zero
+// padded, and its <= 8 dataflow blocks), so each GEMM is one M = 128
+// tcgen05.mma chain with the accumulator in TMEM:
+//
+//   D1[128x64]  = Xs[128x32]  . W1      (statement layer 1)      TMEM cols   0..63
+//   D2[128x64]  = Xb[128x32]  . We      (block embedding)         TMEM cols  64..127
+//   D3[128x64]  = tanh(D1+b1) . W2      (statement layer 2)       TMEM cols 128..191
+//   D4[128x192] = tanh(D2+be) . [Wq|Wk|Wv]                        TMEM cols 192..383
+//
+// Operands are bf16 in shared memory (K-major, no swizzle), accumulation is
+// fp32. The feature rows are computed in the prologue straight into the A
+// operand tiles (features.cpp:98-257 in fp32; no HBM round trip); the packed
+// weights arrive by one 1-D bulk TMA copy (cp.async.bulk) on an mbarrier.
+// Epilogues (tanh, masked row sums, the per-candidate 8x8 softmax
+// attention, mean pooling, the 2h -> h -> 1 head) run in fp32 on the CUDA
+// cores, one thread per TMEM lane (= row).
+//
+// Scores carry bf16 operand rounding (|Δ| vs fp64 typically 1e-3..3e-2);
+// the round certifies its selection by rescoring the boundary band in fp64.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "tt_features.cuh"
 #include "tt_kernels.h"
+#include "tt_tc.cuh"
 
 namespace tt {
 
-bool pacm_tc_supported(const DevSketch&, int) { return false; }
-size_t pacm_tc_packed_bytes(int) { return 16; }
-int launch_pacm_tc_pack(const double*, int, void*, cudaStream_t) { return -1; }
-int launch_pacm_tc(const DevSketch&, const DevDevice&, CandRef, const int64_t*, int64_t, const void*, int, double*,
-                   cudaStream_t) {
-  return -1;
+constexpr int kTcH = 64;            // hidden width of the tensor-core path
+constexpr int kTcCand = 16;         // candidates per CTA tile
+constexpr int kTcRows = 128;        // 16 candidates x 8 rows
+constexpr int kTcThreads = 128;     // one thread per row / TMEM lane
+
+// packed weight image (bytes), built once per tt_pacm_load by k_tc_pack
+constexpr uint32_t kOffW1 = 0;                        // bf16 [64 n][32 k]
+constexpr uint32_t kOffWe = kOffW1 + 64 * 32 * 2;     // bf16 [64][32]
+constexpr uint32_t kOffW2 = kOffWe + 64 * 32 * 2;     // bf16 [64][64]
+constexpr uint32_t kOffWqkv = kOffW2 + 64 * 64 * 2;   // bf16 [192][64]
+constexpr uint32_t kOffBias = kOffWqkv + 192 * 64 * 2;  // f32 b1, be, b2, bq, bk, bv (6 x 64)
+constexpr uint32_t kOffHw1 = kOffBias + 6 * 64 * 4;   // f32 [128 m][64 j]
+constexpr uint32_t kOffHb1 = kOffHw1 + 128 * 64 * 4;  // f32 [64]
+constexpr uint32_t kOffHw2 = kOffHb1 + 64 * 4;        // f32 [64]
+constexpr uint32_t kOffHb2 = kOffHw2 + 64 * 4;        // f32 [4]
+constexpr uint32_t kPackBytes = kOffHb2 + 16;
+
+// shared-memory carve (bytes)
+constexpr uint32_t kSmW = 0;
+constexpr uint32_t kSmXs = (kPackBytes + 127) / 128 * 128;
+constexpr uint32_t kSmXb = kSmXs + kTcRows * 32 * 2;
+constexpr uint32_t kSmA2 = kSmXb + kTcRows * 32 * 2;
+constexpr uint32_t kSmA3 = kSmA2 + kTcRows * 64 * 2;
+constexpr uint32_t kSmK = kSmA3 + kTcRows * 64 * 2;
+constexpr uint32_t kSmV = kSmK + kTcRows * 64 * 4;
+constexpr uint32_t kSmCat = kSmV + kTcRows * 64 * 4;
+constexpr uint32_t kSmBar = kSmCat + kTcCand * 128 * 4;
+constexpr uint32_t kSmTotal = kSmBar + 64;
+
+bool pacm_tc_supported(const DevSketch& S, int h) {
+  const int n_stmt = 2 * S.n_in + 2;
+  const int n_block = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
+  return h == kTcH && n_stmt <= 8 && n_block <= 8;
+}
+
+size_t pacm_tc_packed_bytes(int) { return kPackBytes; }
+
+// ------------------------------------------------------------- packing ----
+__global__ void k_tc_pack(const double* __restrict__ p, uint8_t* __restrict__ out) {
+  const int h = kTcH;
+  const double *w1 = p, *b1 = w1 + 24 * h, *w2 = b1 + h, *b2 = w2 + h * h;
+  const double *we = b2 + h, *be = we + 23 * h, *wq = be + h, *bq = wq + h * h;
+  const double *wk = bq + h, *bk = wk + h * h, *wv = bk + h, *bv = wv + h * h;
+  const double *hw1 = bv + h, *hb1 = hw1 + 2 * h * h, *hw2 = hb1 + h, *hb2 = hw2 + h;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  __nv_bfloat16* W1 = (__nv_bfloat16*)(out + kOffW1);
+  __nv_bfloat16* We = (__nv_bfloat16*)(out + kOffWe);
+  __nv_bfloat16* W2 = (__nv_bfloat16*)(out + kOffW2);
+  __nv_bfloat16* Wqkv = (__nv_bfloat16*)(out + kOffWqkv);
+  for (int e = tid; e < 64 * 32; e += nth) {  // B operands: row = output n, K = input k
+    const int n = e / 32, k = e % 32;
+    W1[tc::kmaj_off(n, k, 64) / 2] = __float2bfloat16_rn(k < 24 ? (float)w1[k * h + n] : 0.f);
+    We[tc::kmaj_off(n, k, 64) / 2] = __float2bfloat16_rn(k < 23 ? (float)we[k * h + n] : 0.f);
+  }
+  for (int e = tid; e < 64 * 64; e += nth) {
+    const int n = e / 64, k = e % 64;
+    W2[tc::kmaj_off(n, k, 64) / 2] = __float2bfloat16_rn((float)w2[k * h + n]);
+  }
+  for (int e = tid; e < 192 * 64; e += nth) {
+    const int n = e / 64, k = e % 64;
+    const double* w = n < 64 ? wq : (n < 128 ? wk : wv);
+    Wqkv[tc::kmaj_off(n, k, 192) / 2] = __float2bfloat16_rn((float)w[k * h + (n & 63)]);
+  }
+  float* bias = (float*)(out + kOffBias);
+  for (int e = tid; e < 64; e += nth) {
+    bias[e] = (float)b1[e], bias[64 + e] = (float)be[e], bias[128 + e] = (float)b2[e];
+    bias[192 + e] = (float)bq[e], bias[256 + e] = (float)bk[e], bias[320 + e] = (float)bv[e];
+    ((float*)(out + kOffHb1))[e] = (float)hb1[e];
+    ((float*)(out + kOffHw2))[e] = (float)hw2[e];
+  }
+  for (int e = tid; e < 128 * 64; e += nth) ((float*)(out + kOffHw1))[e] = (float)hw1[e];
+  if (tid == 0) ((float*)(out + kOffHb2))[0] = (float)hb2[0];
+}
+
+int launch_pacm_tc_pack(const double* params, int h, void* packed, cudaStream_t st) {
+  if (h != kTcH) return -1;
+  tt::note_launch();
+  k_tc_pack<<<64, 256, 0, st>>>(params, (uint8_t*)packed);
+  return 0;
+}
+
+// ---------------------------------------------------------------- kernel ----
+template <int NSP, int NRED>
+__device__ __forceinline__ void tc_load_ref(const DevSketch& S, const CandRef& r, int64_t pos, Factors<NSP, NRED>& F) {
+  if (r.soa) load_factors<NSP, NRED>(r.soa, r.ld, r.idx[pos] - r.index_base, F, true);
+  else if (r.seeded) generate<NSP, NRED>(S, r.s0, (uint64_t)r.idx[pos], F);
+  else from_identity<NSP, NRED>(S, r.id[pos], F);
+}
+
+__device__ __forceinline__ void st_bf16x8(uint8_t* base, uint32_t off, const float* v) {
+  __nv_bfloat162 p[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) p[q] = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+  *(uint4*)(base + off) = *(uint4*)p;
+}
+
+template <int NSP, int NRED>
+__global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(DevSketch S, DevDevice D, CandRef r,
+                                                            const int64_t* __restrict__ count_dev, int64_t k_max,
+                                                            const uint8_t* __restrict__ pack,
+                                                            double* __restrict__ score_out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int t = threadIdx.x, warp = t >> 5;
+  const int64_t count = count_dev ? (*count_dev < k_max ? *count_dev : k_max) : k_max;
+  const int64_t tile0 = (int64_t)blockIdx.x * kTcCand;
+  if (tile0 >= count) return;  // CTA-uniform, before any TMEM/mbarrier use
+
+  uint8_t* wp = sm + kSmW;
+  uint8_t* xs = sm + kSmXs;
+  uint8_t* xb = sm + kSmXb;
+  uint8_t* a2 = sm + kSmA2;
+  uint8_t* a3 = sm + kSmA3;
+  float* kb = (float*)(sm + kSmK);
+  float* vb = (float*)(sm + kSmV);
+  float* cat = (float*)(sm + kSmCat);
+  uint64_t* bars = (uint64_t*)(sm + kSmBar);  // [0] weights landed, [1] MMA done
+  uint32_t* tslot = (uint32_t*)(sm + kSmBar + 16);
+
+  if (warp == 0) tc::tmem_alloc<512>(tslot);
+  if (t == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    tc::fence_mbar_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (t == 0) {  // weights: one bulk TMA copy, overlapped with the feature prologue
+    tc::mbar_expect_tx(&bars[0], kPackBytes);
+    tc::bulk_g2s(wp, pack, kPackBytes, &bars[0]);
+  }
+
+  // ---- prologue: hybrid features straight into the A tiles ----
+  const int c = t >> 3, i = t & 7;
+  const int64_t pos = tile0 + c;
+  const int n_stmt = 2 * S.n_in + 2;
+  const int n_block = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
+  {
+    float rs[32], rb[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) rs[q] = 0.f, rb[q] = 0.f;
+    if (pos < count) {
+      Factors<NSP, NRED> F;
+      tc_load_ref<NSP, NRED>(S, r, pos, F);
+      CandInfo<NSP, NRED> C;
+      cand_info<NSP, NRED>(S, D, F, C);
+      if (i < n_stmt) feature_row<float, NSP, NRED>(S, D, C, i, rs);
+      if (i < n_block) feature_row<float, NSP, NRED>(S, D, C, n_stmt + i, rb);
+    }
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      st_bf16x8(xs, tc::kmaj_off(t, 8 * kc, kTcRows), rs + 8 * kc);
+      st_bf16x8(xb, tc::kmaj_off(t, 8 * kc, kTcRows), rb + 8 * kc);
+    }
+  }
+  tc::fence_async_smem();
+  __syncthreads();
+
+  constexpr uint32_t LBO_A = kTcRows * 16;  // 2048: next 8-wide K chunk of a 128-row tile
+  const uint32_t sxs = tc::smem_u32(xs), sxb = tc::smem_u32(xb), sa2 = tc::smem_u32(a2), sa3 = tc::smem_u32(a3);
+  const uint32_t sw = tc::smem_u32(wp);
+  if (t == 0) {
+    tc::mbar_wait(&bars[0], 0);
+    tc::tc_fence_after();
+    const uint32_t id64 = tc::idesc_bf16_f32(128, 64);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {  // K = 32 = 2 x 16
+      tc::mma_bf16(tmem + 0, tc::desc_k_none(sxs + 2 * s * LBO_A, LBO_A, 128),
+                   tc::desc_k_none(sw + kOffW1 + 2 * s * 1024, 1024, 128), id64, s > 0);
+      tc::mma_bf16(tmem + 64, tc::desc_k_none(sxb + 2 * s * LBO_A, LBO_A, 128),
+                   tc::desc_k_none(sw + kOffWe + 2 * s * 1024, 1024, 128), id64, s > 0);
+    }
+    tc::mma_commit(&bars[1]);
+  }
+  tc::mbar_wait(&bars[1], 0);
+  tc::tc_fence_after();
+
+  const float* bias = (const float*)(wp + kOffBias);
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  // ---- epilogue 1: tanh(D1 + b1) -> A2, tanh(D2 + be) -> A3 (bf16) ----
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    float v[16];
+    tc::tmem_ld16(trow + 16 * ch, v);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = tanhf(v[q] + bias[16 * ch + q]);
+    st_bf16x8(a2, tc::kmaj_off(t, 16 * ch, kTcRows), v);
+    st_bf16x8(a2, tc::kmaj_off(t, 16 * ch + 8, kTcRows), v + 8);
+    tc::tmem_ld16(trow + 64 + 16 * ch, v);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = tanhf(v[q] + bias[64 + 16 * ch + q]);
+    st_bf16x8(a3, tc::kmaj_off(t, 16 * ch, kTcRows), v);
+    st_bf16x8(a3, tc::kmaj_off(t, 16 * ch + 8, kTcRows), v + 8);
+  }
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (t == 0) {
+    const uint32_t id64 = tc::idesc_bf16_f32(128, 64), id192 = tc::idesc_bf16_f32(128, 192);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // K = 64 = 4 x 16
+      tc::mma_bf16(tmem + 128, tc::desc_k_none(sa2 + 2 * s * LBO_A, LBO_A, 128),
+                   tc::desc_k_none(sw + kOffW2 + 2 * s * 1024, 1024, 128), id64, s > 0);
+      tc::mma_bf16(tmem + 192, tc::desc_k_none(sa3 + 2 * s * LBO_A, LBO_A, 128),
+                   tc::desc_k_none(sw + kOffWqkv + 2 * s * 3072, 3072, 128), id192, s > 0);
+    }
+    tc::mma_commit(&bars[1]);
+  }
+  tc::mbar_wait(&bars[1], 1);
+  tc::tc_fence_after();
+
+  // ---- epilogue 2a: statement branch, tanh(D3 + b2), masked sum over rows ----
+  {
+    float* z = vb;  // staging (V is written later)
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      float v[16];
+      tc::tmem_ld16(trow + 128 + 16 * ch, v);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) z[t * 64 + 16 * ch + q] = i < n_stmt ? tanhf(v[q] + bias[128 + 16 * ch + q]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // candidate c, columns 8i..8i+7 (concat[0:h] = sum of rows)
+      const int j = 8 * i + q;
+      float s = 0.f;
+      for (int rr = 0; rr < n_stmt; ++rr) s += z[(8 * c + rr) * 64 + j];
+      cat[c * 128 + j] = s;
+    }
+    __syncthreads();
+  }
+  // ---- epilogue 2b: Q (registers), K and V (shared) with biases ----
+  float qv[64];
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    float v[16];
+    tc::tmem_ld16(trow + 192 + 16 * ch, v);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) qv[16 * ch + q] = v[q] + bias[192 + 16 * ch + q];
+    tc::tmem_ld16(trow + 256 + 16 * ch, v);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) kb[t * 64 + 16 * ch + q] = v[q] + bias[256 + 16 * ch + q];
+    tc::tmem_ld16(trow + 320 + 16 * ch, v);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) vb[t * 64 + 16 * ch + q] = v[q] + bias[320 + 16 * ch + q];
+  }
+  __syncthreads();
+  // ---- attention within the candidate (rows 8c .. 8c+B-1) ----
+  {
+    const float scale = 0.125f;  // 1 / sqrt(64)
+    float lg[8];
+    float mx = -3.0e38f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      float d = 0.f;
+      const float* kr = kb + (8 * c + u) * 64;
+#pragma unroll 16
+      for (int q = 0; q < 64; ++q) d = fmaf(qv[q], kr[q], d);
+      lg[u] = u < n_block ? d * scale : -3.0e38f;
+      mx = fmaxf(mx, lg[u]);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      lg[u] = u < n_block ? __expf(lg[u] - mx) : 0.f;
+      sum += lg[u];
+    }
+    const float inv = 1.f / sum;
+    const bool active = i < n_block;
+    // column means of P over the candidate's valid rows: reduce over the 8 lanes
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      float pu = active ? lg[u] * inv : 0.f;
+      pu += __shfl_xor_sync(0xffffffffu, pu, 1);
+      pu += __shfl_xor_sync(0xffffffffu, pu, 2);
+      pu += __shfl_xor_sync(0xffffffffu, pu, 4);
+      lg[u] = pu / (float)n_block;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = 8 * i + q;
+      float s = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s = fmaf(lg[u], u < n_block ? vb[(8 * c + u) * 64 + j] : 0.f, s);
+      cat[c * 128 + 64 + j] = s;
+    }
+  }
+  __syncthreads();
+  // ---- head: tanh([s|d] W1h + b1h) . w2h + b2h ----
+  {
+    const float* hw1 = (const float*)(wp + kOffHw1);
+    const float* hb1 = (const float*)(wp + kOffHb1);
+    const float* hw2 = (const float*)(wp + kOffHw2);
+    float g[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) g[q] = hb1[8 * i + q];
+    const float* cr = cat + c * 128;
+    for (int m = 0; m < 128; ++m) {
+      const float x = cr[m];
+      const float4 w0 = *(const float4*)(hw1 + m * 64 + 8 * i);
+      const float4 w1 = *(const float4*)(hw1 + m * 64 + 8 * i + 4);
+      g[0] = fmaf(x, w0.x, g[0]), g[1] = fmaf(x, w0.y, g[1]), g[2] = fmaf(x, w0.z, g[2]), g[3] = fmaf(x, w0.w, g[3]);
+      g[4] = fmaf(x, w1.x, g[4]), g[5] = fmaf(x, w1.y, g[5]), g[6] = fmaf(x, w1.z, g[6]), g[7] = fmaf(x, w1.w, g[7]);
+    }
+    float part = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) part = fmaf(tanhf(g[q]), hw2[8 * i + q], part);
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    part += __shfl_xor_sync(0xffffffffu, part, 4);
+    if (i == 0 && pos < count) score_out[pos] = (double)(part + *(const float*)(wp + kOffHb2));
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+template <int NSP, int NRED>
+static void run_tc(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                   const void* packed, double* score_out, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_pacm_tc<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmTotal);
+    init = true;
+  }
+  const unsigned grid = (unsigned)((k_max + kTcCand - 1) / kTcCand);
+  tt::note_launch();
+  k_pacm_tc<NSP, NRED><<<grid, kTcThreads, kSmTotal, st>>>(S, D, ref, count_dev, k_max, (const uint8_t*)packed,
+                                                           score_out);
+}
+
+int launch_pacm_tc(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                   const void* packed, int h, double* score_out, cudaStream_t st) {
+  if (h != kTcH || k_max <= 0) return k_max <= 0 ? 0 : -1;
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_tc<NSP, NRED>(S, D, ref, count_dev, k_max, packed, score_out, st)));
 }
 
 }  // namespace tt
