@@ -359,10 +359,18 @@ def round_local_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: 
                                          seed & (2**64 - 1), _p(out[0]), _p(out[1]), _p(out[2])))
 
 
+def unpack_gathered(gathered: torch.Tensor, world: int, k: int) -> torch.Tensor:
+    """The all-gather output (world consecutive [3, k] payloads) as one
+    [3, world * k] table: row 0 cost bits, row 1 global index, row 2 identity."""
+    if gathered.numel() != world * 3 * k:
+        raise TTError("E_STATE", f"gathered {gathered.numel()} entries, expected {world * 3 * k}")
+    return gathered.reshape(world, 3, k).permute(1, 0, 2).contiguous().reshape(3, world * k)
+
+
 def round_finish_merged_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, gathered: torch.Tensor, n: int, k: int,
                               b: int, precision: int = TT_PREC_FP64, band: float = 0.0):
     """Verify half of a sharded round over the all-gathered [R, 3, k] lists."""
-    g = gathered.reshape(-1, 3, k).permute(1, 0, 2).contiguous().reshape(3, -1)
+    g = unpack_gathered(gathered, gathered.numel() // (3 * k), k)
     cfg = _round_cfg(n, k, b, precision, band, 0, TT_TOGGLES_ALL)
     ctx._merged = g  # keep alive until collected
     ctx.check(lib().tt_round_finish_merged_async(ctx.h, C.byref(sketch), C.byref(dev), C.byref(cfg), _p(g[0]),
