@@ -1,24 +1,36 @@
-// k_pacm64.cu — fp64 PaCM forward on CUDA cores ("parity mode").
+// k_pacm64.cu — K3-fp64: PaCM forward on CUDA cores ("parity mode").
 //
-// Restates run_forward (ranker.cpp:159-209) with the reference's exact
-// accumulation order — affine() accumulates k in order from +0.0 skipping
-// zero inputs, then adds the bias (ranker.cpp:59-75); attention logits are
-// full dot products scaled afterwards, softmax subtracts the row max and
-// divides by the sequential sum; pooling sums rows in order — so scores
-// agree with the reference to the last bit except where CUDA's fp64
-// tanh/exp/log1p differ from glibc by an ulp. It serves as the exact
-// scorer for small K and as the certification rescorer for the
-// tensor-core path (rescoring only the candidates near the selection
-// boundary).
+// Restates run_forward (ranker.cpp:159-209) on fp64 feature rows produced
+// by k_feat_rows, with the reference's exact accumulation order: affine()
+// (ranker.cpp:59-75) accumulates k = 0..m-1 from +0.0 and adds the bias
+// last (its skip of zero inputs cannot change a finite sum that starts at
+// +0.0); matmul_nt's logits are full dot products scaled afterwards;
+// softmax subtracts the row max and divides by the sequential sum; pooling
+// sums rows in order. No FMA (__dmul_rn/__dadd_rn), so scores agree with
+// the reference to the last bit except where CUDA's fp64 tanh/exp differ
+// from glibc by an ulp.
 //
-// One CTA per candidate; the candidate's hybrid feature (features.cpp) is
-// built in shared memory one row per thread, never touching HBM.
+// Design: the round scores K = 512 candidates, ~3.5 per SM, and the fp64
+// pipe (64 DMUL/DADD lanes per SM) bounds the whole set at ~9 us, while the
+// certification rescoring of a few candidates is bound by one candidate's
+// dependent chain. One CTA of 128 threads per candidate, up to three per
+// SM. Activations are stored transposed, X^T[k][row] (rows padded to a
+// multiple of 4), so a thread owns one output column for a group of 4 rows:
+// each k step is one shared-memory weight load, two 16-byte activation loads
+// and 4 independent mul/add chains (ILP 4, every weight reused 4x). The
+// layer weights (<= 32 KB each at h = 64: W1, W2, We, Wq, Wk, Wv and the
+// head's W1 in two halves) are staged into shared memory by 1-D bulk TMA
+// copies, double buffered, so the next layer's weights stream in while the
+// current layer computes. A device-side sublist restricts scoring to the
+// certification band of the tensor-core path.
 #include <cstdint>
 
-#include "tt_features.cuh"
 #include "tt_kernels.h"
+#include "tt_tc.cuh"
 
 namespace tt {
+
+constexpr int kT64 = 128;
 
 struct Params64 {
   const double *w1, *b1, *w2, *b2, *we, *be, *wq, *bq, *wk, *bk, *wv, *bv, *hw1, *hb1, *hw2, *hb2;
@@ -33,315 +45,264 @@ __host__ __device__ inline Params64 split_params(const double* p, int h) {
   return P;
 }
 
-constexpr int kThreads64 = 192;  // 3 x 64: the fused Q|K|V layer has 192 columns at h = 64
-constexpr int kMaxRows = 20;     // dataflow blocks of a 6-input op (3 * 6 + 2)
+constexpr int kRG = 4;  // rows per thread work item
 
-// Y_s (n x q) = act(X (n x m) · W_s (m x q) + b_s) for up to three weight
-// sets s laid side by side (Q|K|V). Work item = (column, row group): each
-// thread keeps one accumulator per row in registers, so one weight load
-// feeds every row and the row chains run in parallel. Every (row, column)
-// still accumulates k = 0..m-1 in order from +0.0 and adds the bias last —
-// the reference's affine() order (ranker.cpp:59-75). Skipping zero inputs,
-// as the reference does, cannot change a finite sum (x*w = ±0 and the
-// running sum starts at +0.0), so the branch is dropped.
-// Weights are read straight from L2 (every CTA of the launch shares them);
-// chunks of kPre loads are issued before any is consumed so one L2 round
-// trip covers kPre steps of the k loop. MAXR bounds the rows per thread.
-constexpr int kPre = 16;
+__host__ __device__ inline int pad4(int n) { return (n + kRG - 1) / kRG * kRG; }
 
-template <int MAXR>
-__device__ __forceinline__ void affine64(const double* x, int n, int m, const double* __restrict__ w0,
-                                         const double* __restrict__ w1, const double* __restrict__ w2,
-                                         const double* __restrict__ b0, const double* __restrict__ b1,
-                                         const double* __restrict__ b2, int q, int sets, bool act, double* y0,
-                                         double* y1, double* y2) {
-  const int p = q * sets;
-  const int G = p >= kThreads64 ? 1 : kThreads64 / p;
-  for (int item = threadIdx.x; item < p * G; item += blockDim.x) {
-    const int g = item / p, j = item % p;
-    const int s = j / q, col = j % q;
-    const double* __restrict__ w = s == 0 ? w0 : (s == 1 ? w1 : w2);
-    const double bj = __ldg((s == 0 ? b0 : (s == 1 ? b1 : b2)) + col);
-    double* y = s == 0 ? y0 : (s == 1 ? y1 : y2);
-    double acc[MAXR];
+// Y^T[j][i] = act(init^T[j][i] + sum_k X^T[k][i] * W[k][j] + b[j]) for rows
+// i < pad4(n), columns j < q, in the reference's order (k ascending from
+// +0.0, bias last). init == nullptr starts from +0.0; b == nullptr stores
+// the partial sum (a split k range continues from it bit-exactly). Padding
+// rows compute harmless finite values that no consumer reads.
+__device__ __forceinline__ void dense64(int lt, const double* __restrict__ xt, int ldx, int n, int m,
+                                        const double* __restrict__ W, int q, const double* __restrict__ init,
+                                        const double* __restrict__ b, bool act, double* __restrict__ yt, int ldy) {
+  const int groups = (n + kRG - 1) / kRG;
+  for (int item = lt; item < q * groups; item += kT64) {
+    const int j = item % q, r0 = (item / q) * kRG;
+    double a[kRG];
 #pragma unroll
-    for (int r = 0; r < MAXR; ++r) acc[r] = 0.0;
-    for (int k0 = 0; k0 < m; k0 += kPre) {
-      double wv[kPre];
+    for (int r = 0; r < kRG; ++r) a[r] = init ? init[j * ldy + r0 + r] : 0.0;
+    const double* xp = xt + r0;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) {
+      const double w = W[k * q + j];
+      const double2 x01 = *(const double2*)(xp + k * ldx);
+      const double2 x23 = *(const double2*)(xp + k * ldx + 2);
+      a[0] = __dadd_rn(a[0], __dmul_rn(x01.x, w));
+      a[1] = __dadd_rn(a[1], __dmul_rn(x01.y, w));
+      a[2] = __dadd_rn(a[2], __dmul_rn(x23.x, w));
+      a[3] = __dadd_rn(a[3], __dmul_rn(x23.y, w));
+    }
+    const double bj = b ? __ldg(b + j) : 0.0;
 #pragma unroll
-      for (int u = 0; u < kPre; ++u) wv[u] = k0 + u < m ? __ldg(w + (k0 + u) * q + col) : 0.0;
-#pragma unroll
-      for (int u = 0; u < kPre; ++u) {
-        if (k0 + u < m) {
-#pragma unroll
-          for (int r = 0; r < MAXR; ++r) {
-            const int i = g + r * G;
-            if (i < n) acc[r] = __dadd_rn(acc[r], __dmul_rn(x[i * m + k0 + u], wv[u]));
-          }
+    for (int r = 0; r < kRG; ++r) {
+      double z = a[r];
+      if (b) {
+        z = __dadd_rn(z, bj);
+        if (act) z = tanh(z);
+      }
+      yt[j * ldy + r0 + r] = z;
+    }
+  }
+}
+
+// y[j] = act(init[j] + sum_{k<m} x[k] * W[k][j] (+ b[j])) for one row.
+__device__ __forceinline__ void dense_row64(int lt, const double* __restrict__ x, int m, const double* __restrict__ W,
+                                            int q, const double* init, const double* __restrict__ b, bool act,
+                                            double* y) {
+  for (int j = lt; j < q; j += kT64) {
+    double a = init[j];
+#pragma unroll 8
+    for (int k = 0; k < m; ++k) a = __dadd_rn(a, __dmul_rn(x[k], W[k * q + j]));
+    if (b) {
+      a = __dadd_rn(a, __ldg(b + j));
+      if (act) a = tanh(a);
+    }
+    y[j] = a;
+  }
+}
+
+// shared-memory doubles: transposed activations (rows padded to 4)
+__host__ __device__ inline size_t act64_doubles(int S, int B, int h) {
+  const int sp = pad4(S), bp = pad4(B);
+  // xs^T, xb^T, z1^T, z2^T, e^T, q^T, k^T, v^T, ao^T, pr, cat, gp, g, s
+  return (size_t)24 * sp + 23 * bp + 2 * h * sp + 5 * h * bp + B * B + 2 * h + 2 * h + 2;
+}
+__host__ __device__ inline size_t wbuf64_doubles(int h) { return (size_t)(h * h > 24 * h ? h * h : 24 * h); }
+
+// weight blocks streamed per candidate, in consumption order
+struct WStages {
+  const double* src[8];
+  uint32_t bytes[8];
+  int n;
+};
+
+__device__ __forceinline__ WStages weight_stages(const Params64& P, int h, bool identity) {
+  WStages w;
+  int n = 0;
+  auto add = [&](const double* p, int count) { w.src[n] = p, w.bytes[n] = (uint32_t)count * 8u, ++n; };
+  add(P.w1, 24 * h);
+  add(P.w2, h * h);
+  add(P.we, 23 * h);
+  if (!identity) add(P.wq, h * h), add(P.wk, h * h), add(P.wv, h * h);
+  add(P.hw1, h * h);
+  add(P.hw1 + h * h, h * h);
+  w.n = n;
+  return w;
+}
+
+// G candidate groups of kT64 threads per CTA share each staged weight block
+// (G = 4 for whole drafted sets, 1 for the short certification sublists).
+__global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ stmt,
+                                                     const double* __restrict__ block, int n_stmt, int n_block,
+                                                     const int64_t* __restrict__ count_dev, int64_t k_max,
+                                                     const int32_t* __restrict__ sublist,
+                                                     const int* __restrict__ sublist_count,
+                                                     const double* __restrict__ params, int h, int identity,
+                                                     double* __restrict__ score_out) {
+  extern __shared__ __align__(128) double sm64[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const int S = n_stmt, B = n_block, t = threadIdx.x;
+  const int G = blockDim.x / kT64, grp = t / kT64, lt = t - grp * kT64;
+  const int sp = pad4(S), bp = pad4(B);
+  const int wd = (int)wbuf64_doubles(h);
+  double* xs = sm64 + 2 * wd + (size_t)grp * act64_doubles(S, B, h);  // [24][sp]
+  double* xb = xs + 24 * sp;    // [23][bp]
+  double* z1 = xb + 23 * bp;    // [h][sp]
+  double* z2 = z1 + h * sp;     // [h][sp]
+  double* e = z2 + h * sp;      // [h][bp]
+  double* qm = e + h * bp;      // [h][bp]
+  double* km = qm + h * bp;
+  double* vm = km + h * bp;
+  double* ao = vm + h * bp;
+  double* pr = ao + h * bp;     // [B][B]
+  double* cat = pr + B * B;     // [2h]
+  double* gp = cat + 2 * h;     // [h]
+  double* g = gp + h;           // [h]
+  const Params64 P = split_params(params, h);
+  const WStages W = weight_stages(P, h, identity != 0);
+  int64_t count = k_max;
+  if (sublist) count = *sublist_count;
+  else if (count_dev) count = *count_dev < k_max ? *count_dev : k_max;
+  if ((int64_t)blockIdx.x * G >= count) return;
+  if (t == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  // gs counts the weight stages this CTA consumed; stage s of the current
+  // pass lives in buffer (base + s) & 1 and completes phase ((base + s) >> 1) & 1
+  uint32_t gs = 0, base = 0;
+  auto issue = [&](int s) {
+    if (t == 0 && s < W.n) {
+      const uint32_t bb = (base + (uint32_t)s) & 1u;
+      tc::fence_async_smem();
+      tc::mbar_expect_tx(&bars[bb], W.bytes[s]);
+      tc::bulk_g2s(sm64 + bb * wd, W.src[s], W.bytes[s], &bars[bb]);
+    }
+  };
+  for (int64_t e0 = (int64_t)blockIdx.x * G; e0 < count; e0 += (int64_t)gridDim.x * G) {
+    const int64_t ent = e0 + grp;
+    const bool live = ent < count;
+    const int64_t pos = live ? (sublist ? sublist[ent] : ent) : 0;
+    base = gs;
+    issue(0);
+    issue(1);
+    if (live) {  // feature rows -> transposed, zero padded
+      for (int u = lt; u < 24 * sp; u += kT64) {
+        const int k = u / sp, i = u - k * sp;
+        xs[u] = i < S ? stmt[(pos * S + i) * 24 + k] : 0.0;
+      }
+      for (int u = lt; u < 23 * bp; u += kT64) {
+        const int k = u / bp, i = u - k * bp;
+        xb[u] = i < B ? block[(pos * B + i) * 23 + k] : 0.0;
+      }
+    }
+    __syncthreads();
+    int s = 0;
+    // one weight stage: wait for its buffer, compute, release, prefetch s + 2
+#define TT_STAGE(CALL)                                 \
+  do {                                                 \
+    tc::mbar_wait(&bars[gs & 1u], (gs >> 1) & 1u);     \
+    const double* Wm = sm64 + (gs & 1u) * wd;          \
+    if (live) CALL;                                    \
+    __syncthreads();                                   \
+    ++gs;                                              \
+    issue(s + 2);                                      \
+    ++s;                                               \
+  } while (0)
+    TT_STAGE(dense64(lt, xs, sp, S, 24, Wm, h, nullptr, P.b1, true, z1, sp));
+    TT_STAGE(dense64(lt, z1, sp, S, h, Wm, h, nullptr, P.b2, true, z2, sp));
+    TT_STAGE(dense64(lt, xb, bp, B, 23, Wm, h, nullptr, P.be, true, e, bp));
+    const double* pooled = e;
+    if (!identity) {
+      TT_STAGE(dense64(lt, e, bp, B, h, Wm, h, nullptr, P.bq, false, qm, bp));
+      TT_STAGE(dense64(lt, e, bp, B, h, Wm, h, nullptr, P.bk, false, km, bp));
+      TT_STAGE(dense64(lt, e, bp, B, h, Wm, h, nullptr, P.bv, false, vm, bp));
+      const double scale = __ddiv_rn(1.0, sqrt((double)h));
+      if (live)
+        for (int u = lt; u < B * B; u += kT64) {  // matmul_nt (ranker.cpp:102-111), then scale
+          const int i = u / B, j = u - (u / B) * B;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < h; ++c) acc = __dadd_rn(acc, __dmul_rn(qm[c * bp + i], km[c * bp + j]));
+          pr[u] = __dmul_rn(acc, scale);
         }
+      __syncthreads();
+      if (live && lt < B) {  // softmax rows (ranker.cpp:181-191)
+        double* row = pr + lt * B;
+        double mx = row[0];
+        for (int j = 1; j < B; ++j) mx = row[j] > mx ? row[j] : mx;
+        double sum = 0.0;
+        for (int j = 0; j < B; ++j) {
+          const double ex = exp(__dadd_rn(row[j], -mx));
+          row[j] = ex;
+          sum = __dadd_rn(sum, ex);
+        }
+        for (int j = 0; j < B; ++j) row[j] = __ddiv_rn(row[j], sum);
       }
+      __syncthreads();
+      if (live)
+        for (int u = lt; u < B * h; u += kT64) {  // matmul (ranker.cpp:113-122)
+          const int j = u / B, i = u - j * B;
+          double acc = 0.0;
+          for (int r = 0; r < B; ++r) acc = __dadd_rn(acc, __dmul_rn(pr[i * B + r], vm[j * bp + r]));
+          ao[j * bp + i] = acc;
+        }
+      __syncthreads();
+      pooled = ao;
     }
-#pragma unroll
-    for (int r = 0; r < MAXR; ++r) {
-      const int i = g + r * G;
-      if (i < n) {
-        const double z = __dadd_rn(acc[r], bj);
-        y[i * q + col] = act ? tanh(z) : z;
+    const double inv_n = __ddiv_rn(1.0, (double)B);
+    if (live)
+      for (int j = lt; j < 2 * h; j += kT64) {  // concat (ranker.cpp:196-200)
+        double v = 0.0;
+        if (j < h) {
+          for (int i = 0; i < S; ++i) v = __dadd_rn(v, z2[j * sp + i]);
+        } else {
+          for (int i = 0; i < B; ++i) v = __dadd_rn(v, __dmul_rn(pooled[(j - h) * bp + i], inv_n));
+        }
+        cat[j] = v;
+        if (j < h) gp[j] = 0.0;
       }
-    }
-  }
-  __syncthreads();
-}
-
-template <int MAXR>
-__device__ __forceinline__ void affine64(const double* x, int n, int m, const double* __restrict__ w,
-                                         const double* __restrict__ b, int p, bool act, double* y) {
-  affine64<MAXR>(x, n, m, w, w, w, b, b, b, p, 1, act, y, y, y);
-}
-
-struct Smem64 {
-  double *xs, *xb, *z1, *z2, *e, *q, *k, *v, *pr, *ao, *cat, *g, *s;
-};
-
-__host__ __device__ inline size_t smem64_doubles(int S, int B, int h) {
-  return (size_t)S * 24 + B * 23 + 2 * S * h + 5 * B * h + B * B + 2 * h + h + 1;
-}
-
-__device__ inline Smem64 carve64(double* base, int S, int B, int h) {
-  Smem64 m;
-  m.xs = base;
-  m.xb = m.xs + S * 24;
-  m.z1 = m.xb + B * 23;
-  m.z2 = m.z1 + S * h;
-  m.e = m.z2 + S * h;
-  m.q = m.e + B * h;
-  m.k = m.q + B * h;
-  m.v = m.k + B * h;
-  m.ao = m.v + B * h;
-  m.pr = m.ao + B * h;
-  m.cat = m.pr + B * B;
-  m.g = m.cat + 2 * h;
-  m.s = m.g + h;
-  return m;
-}
-
-// run_forward on the rows already in m.xs / m.xb. RS / RB / RQ bound the
-// rows one thread owns in the statement layers, the block layers and the
-// fused Q|K|V layer (chosen by the launcher from n_in and h).
-template <int RS, int RB, int RQ>
-__device__ double forward64(const Params64& P, int h, int S, int B, bool identity, Smem64& m) {
-  affine64<RS>(m.xs, S, 24, P.w1, P.b1, h, true, m.z1);
-  affine64<RS>(m.z1, S, h, P.w2, P.b2, h, true, m.z2);
-  affine64<RB>(m.xb, B, 23, P.we, P.be, h, true, m.e);
-  const double* pooled = m.e;
-  if (!identity) {
-    affine64<RQ>(m.e, B, h, P.wq, P.wk, P.wv, P.bq, P.bk, P.bv, h, 3, false, m.q, m.k, m.v);
-    const double scale = __ddiv_rn(1.0, sqrt((double)h));
-    for (int t = threadIdx.x; t < B * B; t += blockDim.x) {  // matmul_nt (ranker.cpp:102-111)
-      const int i = t / B, j = t % B;
+    __syncthreads();
+    // head layer 1 over k = 0..2h-1 (1 row), split in two weight stages
+    TT_STAGE(dense_row64(lt, cat, h, Wm, h, gp, nullptr, false, gp));
+    TT_STAGE(dense_row64(lt, cat + h, h, Wm, h, gp, P.hb1, true, g));
+#undef TT_STAGE
+    if (live && lt == 0) {  // head layer 2: 1 x h -> 1, one chain
       double acc = 0.0;
-      for (int c = 0; c < h; ++c) acc = __dadd_rn(acc, __dmul_rn(m.q[i * h + c], m.k[j * h + c]));
-      m.pr[t] = __dmul_rn(acc, scale);
+      for (int k = 0; k < h; ++k) acc = __dadd_rn(acc, __dmul_rn(g[k], __ldg(P.hw2 + k)));
+      score_out[pos] = __dadd_rn(acc, __ldg(P.hb2));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < B; i += blockDim.x) {  // softmax rows (ranker.cpp:181-191)
-      double* row = m.pr + i * B;
-      double mx = row[0];
-      for (int j = 1; j < B; ++j) mx = row[j] > mx ? row[j] : mx;
-      double sum = 0.0;
-      for (int j = 0; j < B; ++j) {
-        const double ex = exp(__dadd_rn(row[j], -mx));
-        row[j] = ex;
-        sum = __dadd_rn(sum, ex);
-      }
-      for (int j = 0; j < B; ++j) row[j] = __ddiv_rn(row[j], sum);
-    }
-    __syncthreads();
-    {  // matmul (ranker.cpp:113-122); (column, row) items spread over the CTA
-      for (int item = threadIdx.x; item < h * B; item += blockDim.x) {
-        const int j = item % h, i = item / h;
-        double acc = 0.0;
-        for (int t = 0; t < B; ++t) acc = __dadd_rn(acc, __dmul_rn(m.pr[i * B + t], m.v[t * h + j]));
-        m.ao[i * h + j] = acc;
-      }
-    }
-    __syncthreads();
-    pooled = m.ao;
-  }
-  const double inv_n = __ddiv_rn(1.0, (double)B);
-  for (int j = threadIdx.x; j < h; j += blockDim.x) {  // concat (ranker.cpp:196-200)
-    double s = 0.0;
-    for (int i = 0; i < S; ++i) s = __dadd_rn(s, m.z2[i * h + j]);
-    m.cat[j] = s;
-    double d = 0.0;
-    for (int i = 0; i < B; ++i) d = __dadd_rn(d, __dmul_rn(pooled[i * h + j], inv_n));
-    m.cat[h + j] = d;
-  }
-  __syncthreads();
-  affine64<1>(m.cat, 1, 2 * h, P.hw1, P.hb1, h, true, m.g);
-  affine64<1>(m.g, 1, h, P.hw2, P.hb2, 1, false, m.s);
-  return m.s[0];
-}
-
-// row bounds per variant: 0 = (n_in <= 2, h <= 64), 1 = (n_in <= 6, h <= 64), 2 = generic
-template <int V>
-struct Rows;
-template <>
-struct Rows<0> {
-  static constexpr int S = 2, B = 3, Q = 8;
-};
-template <>
-struct Rows<1> {
-  static constexpr int S = 5, B = 7, Q = 20;
-};
-template <>
-struct Rows<2> {
-  static constexpr int S = 14, B = 20, Q = 20;
-};
-
-__host__ inline int rows_variant(int n_in, int h) {
-  if (h > 64) return 2;
-  return n_in <= 2 ? 0 : 1;
-}
-
-template <int V>
-__device__ __forceinline__ double forward64v(const Params64& P, int h, int S, int B, bool identity, Smem64& m) {
-  return forward64<Rows<V>::S, Rows<V>::B, Rows<V>::Q>(P, h, S, B, identity, m);
-}
-
-template <int NSP, int NRED>
-__device__ __forceinline__ void load_ref(const DevSketch& S, const CandRef& r, int64_t pos, Factors<NSP, NRED>& F) {
-  if (r.soa) {
-    load_factors<NSP, NRED>(r.soa, r.ld, r.idx[pos] - r.index_base, F, true);
-  } else if (r.seeded) {
-    generate<NSP, NRED>(S, r.s0, (uint64_t)r.idx[pos], F);
-  } else {
-    from_identity<NSP, NRED>(S, r.id[pos], F);
   }
 }
 
-template <int NSP, int NRED>
-__device__ __forceinline__ void rows64(const DevSketch& S, const DevDevice& D, const CandRef& r, int64_t pos,
-                                       double* xs, double* xb) {
-  const int n_stmt = 2 * S.n_in + 2;
-  const int n_block = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
-  if (threadIdx.x < n_stmt + n_block) {
-    Factors<NSP, NRED> F;
-    load_ref<NSP, NRED>(S, r, pos, F);
-    CandInfo<NSP, NRED> C;
-    cand_info<NSP, NRED>(S, D, F, C);
-    const int row = threadIdx.x;
-    double* out = row < n_stmt ? xs + row * 24 : xb + (row - n_stmt) * 23;
-    feature_row<double, NSP, NRED>(S, D, C, row, out);
-  }
-  __syncthreads();
-}
-
-template <int NSP, int NRED>
-__global__ void __launch_bounds__(64) k_features64(DevSketch S, DevDevice D, CandRef r, int64_t k,
-                                                   double* __restrict__ stmt_out, double* __restrict__ block_out) {
-  const int n_stmt = 2 * S.n_in + 2;
-  const int n_block = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
-  for (int64_t pos = blockIdx.x; pos < k; pos += gridDim.x) {
-    if (threadIdx.x < n_stmt + n_block) {
-      Factors<NSP, NRED> F;
-      load_ref<NSP, NRED>(S, r, pos, F);
-      CandInfo<NSP, NRED> C;
-      cand_info<NSP, NRED>(S, D, F, C);
-      const int row = threadIdx.x;
-      double* out = row < n_stmt ? stmt_out + (pos * n_stmt + row) * 24 : block_out + (pos * n_block + row - n_stmt) * 23;
-      feature_row<double, NSP, NRED>(S, D, C, row, out);
-    }
-  }
-}
-
-template <int NSP, int NRED, int V>
-__global__ void __launch_bounds__(kThreads64) k_pacm64(DevSketch S, DevDevice D, CandRef r, const int64_t* count_dev,
-                                                       const int32_t* sublist, const int* sublist_count,
-                                                       const double* __restrict__ params, int h, int identity,
-                                                       double* __restrict__ score_out) {
-  extern __shared__ __align__(16) double sm64[];
-  const int n_stmt = 2 * S.n_in + 2;
-  const int n_block = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
-  int64_t pos = blockIdx.x;
-  if (sublist) {
-    if ((int)blockIdx.x >= *sublist_count) return;
-    pos = sublist[blockIdx.x];
-  }
-  if (count_dev && pos >= *count_dev) return;
-  Smem64 m = carve64(sm64, n_stmt, n_block, h);
-  rows64<NSP, NRED>(S, D, r, pos, m.xs, m.xb);
-  const Params64 P = split_params(params, h);
-  const double s = forward64v<V>(P, h, n_stmt, n_block, identity != 0, m);
-  if (threadIdx.x == 0) score_out[pos] = s;
-}
-
-template <int V>
-__global__ void __launch_bounds__(kThreads64) k_pacm64_feats(const double* __restrict__ stmt, const double* __restrict__ block,
-                                                             int n_stmt, int n_block, const double* __restrict__ params,
-                                                             int h, int identity, double* __restrict__ score_out) {
-  extern __shared__ __align__(16) double sm64[];
-  const int64_t pos = blockIdx.x;
-  Smem64 m = carve64(sm64, n_stmt, n_block, h);
-  for (int t = threadIdx.x; t < n_stmt * 24; t += blockDim.x) m.xs[t] = stmt[pos * n_stmt * 24 + t];
-  for (int t = threadIdx.x; t < n_block * 23; t += blockDim.x) m.xb[t] = block[pos * n_block * 23 + t];
-  __syncthreads();
-  const Params64 P = split_params(params, h);
-  const double s = forward64v<V>(P, h, n_stmt, n_block, identity != 0, m);
-  if (threadIdx.x == 0) score_out[pos] = s;
-}
-
-template <int NSP, int NRED, int V>
-static void run_pacm64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
-                       const int32_t* sublist, const int* sublist_count, const double* params, int h, int identity,
-                       double* score_out, size_t sm, cudaStream_t st) {
-  static size_t set = 0;
-  if (sm > set) {
-    cudaFuncSetAttribute(k_pacm64<NSP, NRED, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    set = sm;
-  }
-  tt::note_launch();
-  k_pacm64<NSP, NRED, V><<<(unsigned)k_max, kThreads64, sm, st>>>(S, D, ref, count_dev, sublist, sublist_count, params,
-                                                                  h, identity, score_out);
-}
-
-static int n_blocks_of(const DevSketch& S) { return S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2; }
-
-int launch_features64(const DevSketch& S, const DevDevice& D, CandRef ref, int64_t k, double* stmt_out,
-                      double* block_out, cudaStream_t st) {
-  if (k <= 0) return 0;
-  const int g = (int)(k < 148 * 64 ? k : 148 * 64);
-  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_features64<NSP, NRED><<<g, 64, 0, st>>>(S, D, ref, k, stmt_out, block_out)));
-}
-
-int launch_pacm64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
-                  const int32_t* sublist, const int* sublist_count, const double* params, int h,
+int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_block, const int64_t* count_dev,
+                  int64_t k_max, const int32_t* sublist, const int* sublist_count, const double* params, int h,
                   int attention_identity, double* score_out, cudaStream_t st) {
   if (k_max <= 0) return 0;
-  const int n_stmt = 2 * S.n_in + 2, n_block = n_blocks_of(S);
-  const size_t sm = smem64_doubles(n_stmt, n_block, h) * sizeof(double);
-  const int v = rows_variant(S.n_in, h);
-#define TT_PACM64_ARGS S, D, ref, count_dev, k_max, sublist, sublist_count, params, h, attention_identity, score_out, sm, st
-  if (v == 0) return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_pacm64<NSP, NRED, 0>(TT_PACM64_ARGS)));
-  if (v == 1) return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_pacm64<NSP, NRED, 1>(TT_PACM64_ARGS)));
-  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_pacm64<NSP, NRED, 2>(TT_PACM64_ARGS)));
-#undef TT_PACM64_ARGS
-}
-
-int launch_pacm64_feats(const double* stmt, const double* block, int n_stmt, int n_block, int64_t k,
-                        const double* params, int h, int attention_identity, double* score_out, cudaStream_t st) {
-  if (k <= 0) return 0;
-  if (n_stmt > 14 || n_block > 20) return -1;
-  const size_t sm = smem64_doubles(n_stmt, n_block, h) * sizeof(double);
-  const int v = h > 64 ? 2 : (n_stmt <= 6 && n_block <= 8 ? 0 : 1);
-  auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    tt::note_launch();
-    kern<<<(unsigned)k, kThreads64, sm, st>>>(stmt, block, n_stmt, n_block, params, h, attention_identity, score_out);
-  };
-  if (v == 0) go(k_pacm64_feats<0>);
-  else if (v == 1) go(k_pacm64_feats<1>);
-  else go(k_pacm64_feats<2>);
+  if (h % 2) return -1;  // bulk copies need 16-byte aligned weight blocks
+  const size_t wbytes = 2 * wbuf64_doubles(h) * sizeof(double);
+  const size_t abytes = act64_doubles(n_stmt, n_block, h) * sizeof(double);
+  const size_t budget = 227 * 1024 - 64;
+  if (wbytes + abytes > budget) return -1;
+  int G = (int)((budget - wbytes) / abytes);
+  G = G > 4 ? 4 : G;
+  if (sublist) G = 1;  // a few candidates: one per CTA, latency first
+  const size_t sm = wbytes + (size_t)G * abytes;
+  static size_t set = 0;
+  if (sm > 48 * 1024 && sm > set) {
+    cudaFuncSetAttribute(k_pacm64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = sm;
+  }
+  const int64_t ctas = (k_max + G - 1) / G, cap = sublist ? 64 : 8 * 148;
+  const unsigned grid = (unsigned)(ctas < cap ? ctas : cap);
+  tt::note_launch();
+  k_pacm64<<<grid, G * kT64, sm, st>>>(stmt, block, n_stmt, n_block, count_dev, k_max, sublist, sublist_count, params,
+                                      h, attention_identity, score_out);
   return 0;
 }
 

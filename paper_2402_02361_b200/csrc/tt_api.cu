@@ -45,6 +45,11 @@ struct tt_ctx {
   int64_t n_params = 0;
   void* d_packed = nullptr;
   bool packed_ok = false;
+  // feature rows of the drafted set (fp64) and the bf16 tensor-core tile image
+  int64_t feat_cap = 0;
+  double* d_xs = nullptr;
+  double* d_xb = nullptr;
+  uint8_t* d_tiles = nullptr;
   // merge inputs
   int64_t m_cap = 0;
   // last async round
@@ -326,6 +331,23 @@ int ensure_b(tt_ctx* ctx, int64_t b) {
 
 int ensure_cost(tt_ctx* ctx, int64_t n) { return grow(ctx, ctx->sel.cost, ctx->sel.cost_cap, n); }
 
+// room for the feature rows of k candidates (statement rows <= 14, dataflow
+// blocks <= 20: ops with up to 6 inputs) and their tensor-core tile image
+int ensure_feat(tt_ctx* ctx, int64_t k) {
+  if (k <= ctx->feat_cap) return TT_OK;
+  cudaFree(ctx->d_xs), cudaFree(ctx->d_xb), cudaFree(ctx->d_tiles);
+  ctx->d_xs = nullptr, ctx->d_xb = nullptr, ctx->d_tiles = nullptr;
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_xs, sizeof(double) * 14 * TT_STMT_WIDTH * k));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_xb, sizeof(double) * 20 * TT_BLOCK_WIDTH * k));
+  // k_feat_rows writes whole 32-candidate passes = 2 tiles
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_tiles, (size_t)kFeatTileBytes * 2 * ((k + 31) / 32)));
+  ctx->feat_cap = k;
+  return TT_OK;
+}
+
+int n_stmt_of(const DevSketch& S) { return 2 * S.n_in + 2; }
+int n_block_of(const DevSketch& S) { return S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2; }
+
 int sync_check(tt_ctx* ctx) {
   TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   TT_CUDA(ctx, cudaGetLastError());
@@ -444,7 +466,8 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->sel.invalid,
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
-                  c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed};
+                  c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
+                  c->d_tiles};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_record) cudaFreeHost(c->h_record);
@@ -608,7 +631,8 @@ int tt_features(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, con
   if (rc) return rc;
   if ((rc = compile_device(ctx, dev, D))) return rc;
   CandRef r{nullptr, 0, nullptr, 0, id};
-  if (launch_features64(S, D, r, k, stmt, block, ctx->stream)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  if (launch_feat_rows(S, D, r, nullptr, k, nullptr, nullptr, stmt, block, nullptr, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
   TT_LAUNCHED(ctx);
   return TT_OK;
 }
@@ -622,7 +646,8 @@ int tt_features_soa(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev,
   if (rc) return rc;
   if ((rc = compile_device(ctx, dev, D))) return rc;
   CandRef r{soa, ld, idx, 0, nullptr};
-  if (launch_features64(S, D, r, k, stmt, block, ctx->stream)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  if (launch_feat_rows(S, D, r, nullptr, k, nullptr, nullptr, stmt, block, nullptr, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
   TT_LAUNCHED(ctx);
   return TT_OK;
 }
@@ -661,40 +686,53 @@ int ensure_packed(tt_ctx* ctx) {
   return TT_OK;
 }
 
-// Scores the drafted set (positions [0, *count_dev)) into ctx->d_score.
+// Scores the drafted set (positions [0, *count_dev)) into ctx->d_score:
+// features (k_feat_rows) -> PaCM. fp64: exact scores. bf16: tensor-core
+// scores, then certified selection — the top-b by the fast score and every
+// candidate within `band` of the b-th fast score are rescored in fp64 (their
+// rows rebuilt in fp64 for just that sublist); the final select_top only
+// considers exactly rescored candidates (d_excluded marks the rest).
 int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef ref, int64_t k_max, int precision,
                   int64_t b, double band, const int64_t* count_dev) {
+  const int ns = n_stmt_of(S), nb = n_block_of(S);
+  int rc = ensure_feat(ctx, k_max);
+  if (rc) return rc;
   if (precision == TT_PREC_FP64) {
     prof_begin(ctx, 1);
-    if (launch_pacm64(S, D, ref, count_dev, k_max, nullptr, nullptr, ctx->d_params, ctx->h, 0, ctx->d_score,
-                      ctx->stream))
+    if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, ctx->d_xs, ctx->d_xb, nullptr, ctx->stream))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    if (launch_pacm64(ctx->d_xs, ctx->d_xb, ns, nb, count_dev, k_max, nullptr, nullptr, ctx->d_params, ctx->h, 0,
+                      ctx->d_score, ctx->stream))
+      return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");
     prof_end(ctx, 1);
     TT_LAUNCHED(ctx);
     TT_CUDA(ctx, cudaMemsetAsync(ctx->d_sublist_count, 0, sizeof(int), ctx->stream));
     return TT_OK;
   }
   if (precision != TT_PREC_BF16) return fail(ctx, TT_E_CONFIG, "unknown precision");
-  if (!pacm_tc_supported(S, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
-  int rc = ensure_packed(ctx);
-  if (rc) return rc;
+  if (!pacm_tc_supported(ns, nb, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
+  if ((rc = ensure_packed(ctx))) return rc;
   prof_begin(ctx, 1);
-  if (launch_pacm_tc(S, D, ref, count_dev, k_max, ctx->d_packed, ctx->h, ctx->d_score_fast, ctx->stream))
+  if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, nullptr, nullptr, ctx->d_tiles, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  if (launch_pacm_tc(ctx->d_tiles, ns, nb, count_dev, k_max, ctx->d_packed, ctx->h, ctx->d_score_fast, ctx->stream))
     return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
   prof_end(ctx, 1);
   TT_LAUNCHED(ctx);
   if (b > 0) {
     prof_begin(ctx, 2);
-    // certified selection: exact fp64 rescoring of the boundary band
     launch_select_top(ctx->d_score_fast, ctx->d_cost, nullptr, k_max, count_dev, b, ctx->d_pos_fast,
                       ctx->d_pos_fast_count, ctx->d_status + 1, ctx->stream);
     launch_band(ctx->d_score_fast, count_dev, k_max, ctx->d_pos_fast, ctx->d_pos_fast_count, band, ctx->d_sublist,
                 ctx->d_sublist_count, ctx->d_excluded, ctx->stream);
     TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_score, ctx->d_score_fast, sizeof(double) * k_max, cudaMemcpyDeviceToDevice,
                                  ctx->stream));
-    if (launch_pacm64(S, D, ref, count_dev, k_max, ctx->d_sublist, ctx->d_sublist_count, ctx->d_params, ctx->h, 0,
-                      ctx->d_score, ctx->stream))
+    if (launch_feat_rows(S, D, ref, count_dev, k_max, ctx->d_sublist, ctx->d_sublist_count, ctx->d_xs, ctx->d_xb,
+                         nullptr, ctx->stream))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    if (launch_pacm64(ctx->d_xs, ctx->d_xb, ns, nb, count_dev, k_max, ctx->d_sublist, ctx->d_sublist_count,
+                      ctx->d_params, ctx->h, 0, ctx->d_score, ctx->stream))
+      return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");
     prof_end(ctx, 2);
     TT_LAUNCHED(ctx);
   } else {
@@ -858,17 +896,31 @@ int tt_pacm_score(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   if ((rc = compile_device(ctx, dev, D))) return rc;
   if (!ctx->d_params) return fail(ctx, TT_E_STATE, "score: tt_pacm_load first");
   if (k <= 0) return TT_OK;
-  CandRef ref{nullptr, 0, nullptr, 0, id};
-  if (precision == TT_PREC_FP64) {
-    if (launch_pacm64(S, D, ref, nullptr, k, nullptr, nullptr, ctx->d_params, ctx->h, 0, score, ctx->stream))
-      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
-  } else if (precision == TT_PREC_BF16) {
-    if (!pacm_tc_supported(S, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
+  const int ns = n_stmt_of(S), nb = n_block_of(S);
+  if (precision == TT_PREC_BF16) {
+    if (!pacm_tc_supported(ns, nb, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
     if ((rc = ensure_packed(ctx))) return rc;
-    if (launch_pacm_tc(S, D, ref, nullptr, k, ctx->d_packed, ctx->h, score, ctx->stream))
-      return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
-  } else {
+  } else if (precision != TT_PREC_FP64) {
     return fail(ctx, TT_E_CONFIG, "unknown precision");
+  }
+  // chunks bound the feature scratch (fp64 rows ~6.4 KB, bf16 tiles 1 KB per candidate)
+  const int64_t chunk = precision == TT_PREC_FP64 ? (int64_t)1 << 16 : (int64_t)1 << 20;
+  if ((rc = ensure_feat(ctx, k < chunk ? k : chunk))) return rc;
+  for (int64_t off = 0; off < k; off += chunk) {
+    const int64_t m = k - off < chunk ? k - off : chunk;
+    CandRef ref{nullptr, 0, nullptr, 0, id + off};
+    if (precision == TT_PREC_FP64) {
+      if (launch_feat_rows(S, D, ref, nullptr, m, nullptr, nullptr, ctx->d_xs, ctx->d_xb, nullptr, ctx->stream))
+        return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+      if (launch_pacm64(ctx->d_xs, ctx->d_xb, ns, nb, nullptr, m, nullptr, nullptr, ctx->d_params, ctx->h, 0,
+                        score + off, ctx->stream))
+        return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");
+    } else {
+      if (launch_feat_rows(S, D, ref, nullptr, m, nullptr, nullptr, nullptr, nullptr, ctx->d_tiles, ctx->stream))
+        return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+      if (launch_pacm_tc(ctx->d_tiles, ns, nb, nullptr, m, ctx->d_packed, ctx->h, score + off, ctx->stream))
+        return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
+    }
   }
   TT_LAUNCHED(ctx);
   g_forward_calls.fetch_add((uint64_t)k, std::memory_order_relaxed);
@@ -881,9 +933,10 @@ int tt_pacm_score_features(tt_ctx* ctx, const double* stmt, const double* block,
   if (!ctx->d_params) return fail(ctx, TT_E_STATE, "score: tt_pacm_load first");
   if (n_stmt < 1 || n_block < 1)
     return fail(ctx, TT_E_STATE, "feature must have at least one statement and one dataflow block");
-  if (launch_pacm64_feats(stmt, block, n_stmt, n_block, k, ctx->d_params, ctx->h, attention_identity, score,
-                          ctx->stream))
-    return fail(ctx, TT_E_STATE, "score launch");
+  if (n_stmt > 14 || n_block > 20) return fail(ctx, TT_E_STATE, "at most 14 statements and 20 dataflow blocks");
+  if (launch_pacm64(stmt, block, n_stmt, n_block, nullptr, k, nullptr, nullptr, ctx->d_params, ctx->h,
+                    attention_identity, score, ctx->stream))
+    return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");
   TT_LAUNCHED(ctx);
   g_forward_calls.fetch_add((uint64_t)(k > 0 ? k : 0), std::memory_order_relaxed);
   return TT_OK;

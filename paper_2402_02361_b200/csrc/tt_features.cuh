@@ -13,15 +13,21 @@
 
 namespace tt {
 
+// log1p is ~80 SASS instructions; a feature row calls it up to 17 times, so
+// one out-of-line copy keeps the row code small enough to stay in the
+// instruction cache (the kernels that build rows are latency-bound).
+static __device__ __noinline__ double log1p_ool(double x) { return log1p(x); }
+static __device__ __noinline__ float log1pf_ool(float x) { return log1pf(x); }
+
 template <typename R>
 __device__ __forceinline__ R lg(R x);
 template <>
 __device__ __forceinline__ double lg<double>(double x) {
-  return log1p(x);
+  return log1p_ool(x);
 }
 template <>
 __device__ __forceinline__ float lg<float>(float x) {
-  return log1pf(x);
+  return log1pf_ool(x);
 }
 
 template <typename R>

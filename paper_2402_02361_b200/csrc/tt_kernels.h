@@ -65,8 +65,7 @@ int launch_selected_identity(const DevSketch& S, const int32_t* soa, int64_t ld,
                              bool seeded, const int64_t* pos, const int64_t* pos_count, const int64_t* idx, int64_t b,
                              uint64_t* out, cudaStream_t st);
 
-// k_pacm64.cu — fp64 PaCM (parity mode / certification rescoring)
-// Candidates are addressed by identity (population-independent) or by
+// How a kernel finds drafted candidate `pos`. Candidates are addressed by identity (population-independent) or by
 // (soa, ld, local index). `list`/`count` optionally restrict scoring to a
 // device-side sublist of positions (count read on device).
 struct CandRef {
@@ -79,19 +78,23 @@ struct CandRef {
   int32_t seeded;
   int32_t _pad;
 };
-int launch_features64(const DevSketch& S, const DevDevice& D, CandRef ref, int64_t k, double* stmt_out,
-                      double* block_out, cudaStream_t st);
-int launch_pacm64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
-                  const int32_t* sublist, const int* sublist_count, const double* params, int h,
+// k_feat.cu — feature rows of the drafted set (fp64 rows and/or the bf16
+// tensor-core tile image, kFeatTileBytes per 16 candidates)
+constexpr int64_t kFeatTileBytes = 16384;
+int launch_feat_rows(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                     const int32_t* sublist, const int* sublist_count, double* stmt, double* block, uint8_t* tiles,
+                     cudaStream_t st);
+
+// k_pacm64.cu — fp64 PaCM on feature rows (parity mode / certification)
+int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_block, const int64_t* count_dev,
+                  int64_t k_max, const int32_t* sublist, const int* sublist_count, const double* params, int h,
                   int attention_identity, double* score_out, cudaStream_t st);
-int launch_pacm64_feats(const double* stmt, const double* block, int n_stmt, int n_block, int64_t k,
-                        const double* params, int h, int attention_identity, double* score_out, cudaStream_t st);
 
 // k_pacm_tc.cu — tcgen05/TMEM fast path (bf16 operands, fp32 accumulators)
-bool pacm_tc_supported(const DevSketch& S, int h);
+bool pacm_tc_supported(int n_stmt, int n_block, int h);
 size_t pacm_tc_packed_bytes(int h);
 int launch_pacm_tc_pack(const double* params, int h, void* packed, cudaStream_t st);
-int launch_pacm_tc(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+int launch_pacm_tc(const uint8_t* tiles, int n_stmt, int n_block, const int64_t* count_dev, int64_t k_max,
                    const void* packed, int h, double* score_out, cudaStream_t st);
 
 // k_select.cu

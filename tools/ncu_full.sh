@@ -5,7 +5,7 @@
 TAG=${1:-full}; KRE=${2:-"k_pacm64|k_pacm_tc|k_draft_cost|k_sel_finalize"}; CNT=${3:-8}; shift 3
 mkdir -p gpurun_out
 REP=/tmp/$TAG
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"$KRE" -c $CNT \
+timeout 1200 ncu --set full --import-source on --clock-control none $NCU_EXTRA -k regex:"$KRE" -c $CNT \
   -o $REP -f python bench.py --steps 1 --warmup 3 --no-cpu "$@" > gpurun_out/ncu_$TAG.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_$TAG.log
 ncu -i $REP.ncu-rep --page raw --csv > gpurun_out/${TAG}_raw.csv 2>>gpurun_out/ncu_$TAG.log
