@@ -37,6 +37,18 @@ constexpr int kTableCap = 16384;       // hash slots of the fallback path
 constexpr int kSortE = 4;              // keys per thread in the 4096-entry sorts
 constexpr int kFinalE = 1;             // keys per thread in the 1024-entry sorts (1024 threads)
 constexpr uint64_t kEmpty = ~0ull;
+constexpr int kFastCap = 4096;  // survivors the fast path's last CTA sorts
+
+static int grid_for(int64_t n, int threads, int max_blocks) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > max_blocks) g = max_blocks;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <typename F>
+static void set_smem(F* f, size_t bytes) {
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 struct Src {
   const int32_t* soa;
@@ -404,6 +416,292 @@ __global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Sr
   }
 }
 
+// ------------------------------------------- fast path (sampled threshold) ----
+// N > 1024, four short kernels and no CTA-wide sorting network (a bitonic
+// sort of 4096 keys costs ~60 us on one SM; everything here is either
+// grid-wide or O(log) passes):
+//   k_fsel_cost:    K1 over the population, costs to HBM, a strided sample of
+//                   <= 4096 cost keys; the last CTA (ticket) radix-selects the
+//                   sample key of rank 2 * ceil(need * ns / n) + 16 as the
+//                   survivor threshold (~2.5x need survivors expected).
+//   k_fsel_compact: keys <= threshold appended (warp-aggregated) with a
+//                   schedule fingerprint (seeded: the exact identity the
+//                   generator returns; explicit: a 64-bit hash of the factor
+//                   columns, confirmed column by column on a match).
+//   k_fsel_rank:    all-pairs over the <= 4096 survivors, spread over the GPU:
+//                   each (survivor, 256-chunk) thread counts the keys below
+//                   it ((cost, index) order) and flags a duplicate when an
+//                   equal-cost survivor with a lower index is the same
+//                   schedule ("first discovery wins", draft.cpp:200-203).
+//   k_fsel_emit:    one CTA scatters survivors to their ranks and emits the K
+//                   lowest unique in ascending (cost, index) order.
+// Exactness never depends on the sample: every key <= threshold survives,
+// so whenever >= K unique schedules survive they include the true top-K;
+// otherwise NEED_MORE (the host retries with a larger need); > 4096
+// survivors report OVERFLOW (the identity-keyed hash path takes over).
+constexpr int kFastThreads = 1024;
+constexpr int kFastE = kFastCap / kFastThreads;  // 4 keys per thread
+constexpr int kRankChunk = 256;
+
+__device__ __forceinline__ bool last_cta(SelState* st) {
+  __shared__ int am_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    am_last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last != 0;
+}
+
+// Key of rank r (0-based) among keys[0..n) in shared memory: MSB-first
+// radix select, 8 bits per pass. Whole CTA; returns the key to every thread.
+__device__ uint64_t block_radix_select(const uint64_t* keys, int n, int r, int* hist) {
+  __shared__ uint64_t s_prefix;
+  __shared__ int s_r;
+  uint64_t prefix = 0, mask = 0;
+  int rr = r;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const uint64_t k = keys[e];
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one warp scans 256 bins, 8 per lane
+      const int lane = threadIdx.x;
+      int c[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q] = hist[lane * 8 + q], tot += c[q];
+      int incl = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      int run = incl - tot;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (run <= rr && rr < run + c[q]) s_prefix = (uint64_t)(lane * 8 + q), s_r = rr - run;
+        run += c[q];
+      }
+    }
+    __syncthreads();
+    prefix |= s_prefix << shift;
+    mask |= 255ull << shift;
+    rr = s_r;
+    __syncthreads();
+  }
+  return prefix;
+}
+
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevice D, Src src, int64_t n,
+                                                            int toggles, int64_t need, double* __restrict__ cost,
+                                                            uint64_t* __restrict__ sample, SelState* __restrict__ st,
+                                                            int* __restrict__ rank_acc, int* __restrict__ dup,
+                                                            int* __restrict__ invalid) {
+  __shared__ uint64_t keys[kFastCap];
+  __shared__ int hist[256];
+  const int64_t stride = (n + kFastCap - 1) / kFastCap;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    Factors<NSP, NRED> F;
+    load_cand<NSP, NRED, SEED>(S, src, i, F, false);
+    if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
+    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles);
+    cost[i] = c;
+    if (i % stride == 0) sample[i / stride] = cost_key(c);
+  }
+  // zero the rank kernel's accumulators for this round
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kFastCap; e += gridDim.x * blockDim.x)
+    rank_acc[e] = 0, dup[e] = 0;
+  if (bad) atomicOr(invalid, 1);
+  if (!last_cta(st)) return;
+  const int ns = (int)((n + stride - 1) / stride);
+  for (int e = threadIdx.x; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
+  __syncthreads();
+  int64_t r = 2 * ((need * ns + n - 1) / n) + 16;
+  const bool all = r >= ns - 1;
+  const uint64_t thr = all ? ~0ull : block_radix_select(keys, ns, (int)r, hist);
+  if (threadIdx.x == 0) {
+    st->prefix = thr;
+    st->shift = 0;
+    st->all = all ? 1 : 0;
+    st->need = need;
+    st->nsurv = 0;
+    st->status = 0;
+    st->count = 0;
+    st->done = 1;
+    st->ticket = 0;
+  }
+}
+
+// 64-bit fingerprint of a schedule's factor columns (explicit populations)
+template <int NSP, int NRED>
+__device__ __forceinline__ uint64_t fingerprint(const Factors<NSP, NRED>& F) {
+  uint64_t h = scramble64((uint64_t)(uint32_t)F.unroll + kGolden);
+#pragma unroll
+  for (int q = 0; q < Factors<NSP, NRED>::kN; ++q) h = scramble64(h ^ ((uint64_t)(uint32_t)F.f[q] + kGolden));
+  return h;
+}
+
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(256) k_fsel_compact(DevSketch S, Src src, const double* __restrict__ cost,
+                                                      int64_t n, SelState* __restrict__ st,
+                                                      uint64_t* __restrict__ skey, int64_t* __restrict__ sidx,
+                                                      uint64_t* __restrict__ sfp) {
+  const uint64_t thr = st->prefix;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint64_t key = 0;
+    bool keep = false;
+    if (i < n) {
+      key = cost_key(__ldcg(cost + i));
+      keep = key <= thr;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    uint32_t pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&st->nsurv, (uint32_t)__popc(m));
+    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+    if (keep) {
+      const uint32_t p = pos0 + __popc(m & ((1u << lane) - 1u));
+      if (p < (uint32_t)kFastCap) {
+        Factors<NSP, NRED> F;
+        const uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, true);
+        skey[p] = key, sidx[p] = i;
+        sfp[p] = SEED ? id : fingerprint<NSP, NRED>(F);
+      }
+    }
+  }
+}
+
+template <int NSP, int NRED, bool SEED>
+__device__ __forceinline__ bool same_schedule(const DevSketch& S, const Src& src, int64_t i, int64_t j) {
+  if constexpr (SEED) return true;  // seeded fingerprints are exact identities
+  Factors<NSP, NRED> Fi, Fj;
+  load_cand<NSP, NRED, SEED>(S, src, i, Fi, true);
+  load_cand<NSP, NRED, SEED>(S, src, j, Fj, true);
+  bool same = Fj.unroll == Fi.unroll;
+#pragma unroll
+  for (int q = 0; q < Factors<NSP, NRED>::kN; ++q) same &= Fj.f[q] == Fi.f[q];
+  return same;
+}
+
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(kRankChunk) k_fsel_rank(DevSketch S, Src src, const SelState* __restrict__ st,
+                                                          const uint64_t* __restrict__ skey,
+                                                          const int64_t* __restrict__ sidx,
+                                                          const uint64_t* __restrict__ sfp,
+                                                          int* __restrict__ rank_acc, int* __restrict__ dup) {
+  __shared__ uint64_t ck[kRankChunk], cf[kRankChunk];
+  __shared__ int64_t ci[kRankChunk];
+  const int m = (int)min(*(volatile const uint32_t*)&st->nsurv, (uint32_t)kFastCap);
+  const int chunks = (m + kRankChunk - 1) / kRankChunk;
+  for (int blk = blockIdx.x; blk < chunks * chunks; blk += gridDim.x) {
+    const int ce = blk / chunks, cj = blk - ce * chunks;  // element chunk, comparison chunk
+    const int j0 = cj * kRankChunk;
+    __syncthreads();
+    if (j0 + (int)threadIdx.x < m) {
+      ck[threadIdx.x] = skey[j0 + threadIdx.x];
+      ci[threadIdx.x] = sidx[j0 + threadIdx.x];
+      cf[threadIdx.x] = sfp[j0 + threadIdx.x];
+    }
+    __syncthreads();
+    const int e = ce * kRankChunk + threadIdx.x;
+    if (e >= m) continue;
+    const uint64_t ke = skey[e], fe = sfp[e];
+    const int64_t ie = sidx[e];
+    const int jn = min(kRankChunk, m - j0);
+    int below = 0;
+    bool d = false;
+    for (int q = 0; q < jn; ++q) {
+      const uint64_t kq = ck[q];
+      const int64_t iq = ci[q];
+      const bool lt = kq < ke || (kq == ke && iq < ie);
+      below += lt;
+      if (kq == ke && iq < ie && cf[q] == fe && !d) d = same_schedule<NSP, NRED, SEED>(S, src, ie, iq);
+    }
+    if (below) atomicAdd(rank_acc + e, below);
+    if (d) atomicOr(dup + e, 1);
+  }
+}
+
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src, int64_t n, int64_t k,
+                                                            SelState* __restrict__ st,
+                                                            const uint64_t* __restrict__ skey,
+                                                            const int64_t* __restrict__ sidx,
+                                                            const int* __restrict__ rank_acc,
+                                                            const int* __restrict__ dup,
+                                                            int64_t* __restrict__ out_idx,
+                                                            double* __restrict__ out_cost,
+                                                            uint64_t* __restrict__ out_id,
+                                                            int64_t* __restrict__ out_count) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* a = (uint64_t*)smem;
+  int64_t* bi = (int64_t*)(a + kFastCap);
+  int* flag = (int*)(bi + kFastCap);
+  int* pos = flag + kFastCap;
+  __shared__ int wt[32];
+  const uint32_t nsurv = st->nsurv;
+  if (nsurv > (uint32_t)kFastCap) {
+    if (threadIdx.x == 0) st->status |= TT_SEL_OVERFLOW, *out_count = 0;
+    return;
+  }
+  const int m = (int)nsurv;
+  for (int e = threadIdx.x; e < kFastCap; e += blockDim.x) flag[e] = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < m; e += blockDim.x) {
+    const int r = rank_acc[e];  // a permutation of 0..m-1: (cost, index) keys are distinct
+    a[r] = skey[e];
+    bi[r] = sidx[e];
+    flag[r] = dup[e] ? 0 : 1;
+  }
+  __syncthreads();
+  const int total = block_exclusive_scan(flag, pos, kFastCap, wt);
+  for (int e = threadIdx.x; e < m; e += blockDim.x) {
+    if (flag[e] && pos[e] < k) {
+      const int o = pos[e];
+      out_idx[o] = bi[e] + src.index_base;
+      out_cost[o] = key_cost(a[e]);
+      if (out_id) out_id[o] = identity_at<NSP, NRED, SEED>(S, src, bi[e]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int64_t cnt = total < k ? total : k;
+    *out_count = cnt;
+    st->count = cnt;
+    const bool everything = st->all || (int64_t)m >= n;
+    if (cnt < k && !everything) st->status |= TT_SEL_NEED_MORE;  // duplicates ate the margin
+  }
+}
+
+template <int NSP, int NRED, bool SEED>
+static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
+                     int64_t need, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
+                     int64_t* out_count, cudaStream_t st) {
+  const int g = grid_for(n, kFastThreads, 148);
+  tt::note_launch();
+  k_fsel_cost<NSP, NRED, SEED><<<g, kFastThreads, 0, st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
+                                                          w.rank, w.dup, w.invalid);
+  tt::note_launch();
+  k_fsel_compact<NSP, NRED, SEED><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(S, src, w.cost, n, w.state, w.skey,
+                                                                             w.sidx, w.sfp);
+  tt::note_launch();
+  k_fsel_rank<NSP, NRED, SEED><<<148, kRankChunk, 0, st>>>(S, src, w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup);
+  constexpr size_t emit_smem = (size_t)kFastCap * (2 * sizeof(uint64_t) + 2 * sizeof(int));
+  static bool init = false;
+  if (!init) set_smem(k_fsel_emit<NSP, NRED, SEED>, emit_smem), init = true;
+  tt::note_launch();
+  k_fsel_emit<NSP, NRED, SEED><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
+                                                          out_idx, out_cost, out_id, out_count);
+}
+
 // ---------------------------------------------- hash fallback (ties) ----
 __device__ __forceinline__ uint64_t slot_hash(uint64_t id) { return scramble64(id + kGolden); }
 
@@ -539,17 +837,6 @@ __global__ void __launch_bounds__(1024) k_merge(const double* __restrict__ cost,
 }
 
 // ------------------------------------------------------------ launchers ----
-static int grid_for(int64_t n, int threads, int max_blocks) {
-  int64_t g = (n + threads - 1) / threads;
-  if (g > max_blocks) g = max_blocks;
-  return (int)(g < 1 ? 1 : g);
-}
-
-template <typename F>
-static void set_smem(F* f, size_t bytes) {
-  static_assert(sizeof(F*) > 0, "");
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
 
 int launch_generate(const DevSketch& S, uint64_t s0, int64_t first, int64_t n, int32_t* soa, int64_t ld,
                     uint64_t* id_out, cudaStream_t st) {
@@ -628,6 +915,11 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
       return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, true>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
     return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, false>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
   }
+  if (!hash) {
+    if (seeded)
+      return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_fast<NSP, NRED, true>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)));
+    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_fast<NSP, NRED, false>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)));
+  }
   {
     int rc = launch_draft_cost(S, D, soa, ld, s0, first, seeded, n, toggles, w.cost, w.hist, w.invalid, st);
     if (rc) return rc;
@@ -644,6 +936,30 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
   if (seeded)
     return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_tail<NSP, NRED, true>(S, src, n, k, hash, w, out_idx, out_cost, out_id, out_count, st)));
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_tail<NSP, NRED, false>(S, src, n, k, hash, w, out_idx, out_cost, out_id, out_count, st)));
+}
+
+// Identities of the drafted set (positions [0, *count)), written to id[].
+// Runs on the context's side stream, overlapped with features + PaCM: the
+// exact identity (mixed-radix composition ranks) is a long serial chain per
+// candidate and only the b selections' identities are reported.
+template <int NSP, int NRED, bool SEED>
+__global__ void __launch_bounds__(128) k_drafted_identity(DevSketch S, Src src, const int64_t* __restrict__ idx,
+                                                          const int64_t* __restrict__ count_dev, int64_t k_max,
+                                                          uint64_t* __restrict__ out) {
+  const int64_t cnt = count_dev ? (*count_dev < k_max ? *count_dev : k_max) : k_max;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < cnt; p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = identity_at<NSP, NRED, SEED>(S, src, idx[p] - src.index_base);
+}
+
+int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
+                            bool seeded, const int64_t* idx, const int64_t* count_dev, int64_t k_max, uint64_t* out,
+                            cudaStream_t st) {
+  if (k_max <= 0) return 0;
+  Src src{soa, ld, s0, first, first};
+  const int g = grid_for(k_max, 128, 148);
+  if (seeded)
+    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, true><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
 }
 
 // Identities of the b selected candidates, written into the round record

@@ -275,6 +275,105 @@ int launch_momentum(double* phi, const double* target, int64_t n, double m, cuda
   return 0;
 }
 
+// ------------------------------------------------------------ finish ----
+// The round's select_top (ranker.cpp:514-532: score desc, draft cost asc,
+// position asc; excluded never chosen) fused with the record gather for the
+// single device->host copy: [0] selected, [1] drafted, [2] status, [3]
+// rescored, then b population indices, b scores, b draft costs, b
+// identities. n <= 1024, b <= 32: every warp sorts its 32 keys with
+// shuffles (15 exchange steps, no shared-memory network), then warp 0 runs a
+// b-step tournament over the warps' sorted lists.
+__device__ __forceinline__ void warp_sort32(Key3& k) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const Key3 o = k.shfl_xor(stride);
+      const bool lower = (lane & stride) == 0, up = (lane & size) == 0;
+      const bool take = (lower == up) ? o.lt(k) : k.lt(o);
+      if (take) k = o;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scores, const double* __restrict__ drafts,
+                                                 const uint8_t* __restrict__ excluded, int64_t n_max,
+                                                 const int64_t* __restrict__ n_dev, int64_t b,
+                                                 const int64_t* __restrict__ idx, const uint64_t* __restrict__ id,
+                                                 const SelState* __restrict__ sel, const int* __restrict__ rescored,
+                                                 int64_t* __restrict__ out) {
+  __shared__ Key3 lists[32][33];
+  __shared__ int avail;
+  __shared__ uint32_t win[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int64_t n = n_dev ? (*n_dev < n_max ? *n_dev : n_max) : n_max;
+  if (t == 0) avail = 0;
+  __syncthreads();
+  const bool ok = t < n && !(excluded && excluded[t]);
+  Key3 k;
+  k.a = ok ? ~ordered(scores[t]) : kAll;
+  k.b = ok ? ordered(drafts[t]) : kAll;
+  k.c = ok ? (uint32_t)t : 0xffffffffu;
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  if (lane == 0 && bal) atomicAdd(&avail, __popc(bal));
+  warp_sort32(k);
+  lists[warp][lane] = k;
+  if (lane == 0) lists[warp][32].a = kAll, lists[warp][32].b = kAll, lists[warp][32].c = 0xffffffffu;
+  __syncthreads();
+  const int64_t keep = b < avail ? b : avail;
+  if (warp == 0) {  // tournament: lane w holds the head of warp w's list
+    int head = 0;
+    for (int it = 0; it < keep; ++it) {
+      Key3 h;
+      if (lane < nw) h = lists[lane][head];
+      else h.a = kAll, h.b = kAll, h.c = 0xffffffffu;
+      Key3 m = h;
+      int who = lane;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const Key3 o = m.shfl_xor(off);
+        const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+        if (o.lt(m)) m = o, who = ow;
+      }
+      if (lane == 0) win[it] = m.c;
+      if (lane == who) ++head;
+    }
+  }
+  __syncthreads();
+  int64_t* ix = out + 4;
+  double* sc = (double*)(ix + b);
+  double* co = sc + b;
+  uint64_t* ids = (uint64_t*)(co + b);
+  if (t < b) {
+    if (t < keep) {
+      const uint32_t q = win[t];
+      ix[t] = idx[q];
+      sc[t] = scores[q];
+      co[t] = drafts[q];
+      ids[t] = id ? id[q] : 0;
+    } else {
+      ix[t] = -1, sc[t] = 0.0, co[t] = 0.0, ids[t] = 0;
+    }
+  }
+  if (t == 0) {
+    out[0] = keep;
+    out[1] = n;
+    out[2] = (int64_t)(sel ? sel->status : 0);
+    out[3] = rescored ? *rescored : 0;
+  }
+}
+
+int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
+                  const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
+                  const int* rescored, int64_t* out, cudaStream_t st) {
+  if (n_max > 1024 || b > 32 || b > n_max) return -1;
+  const int nt = (int)((n_max + 31) / 32 * 32);
+  tt::note_launch();
+  k_finish<<<1, nt, 0, st>>>(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, out);
+  return 0;
+}
+
 // ------------------------------------------------- result gathering ----
 // Packs the round's b selections into one record for a single
 // device->host copy. Layout (8-byte words): [0] selected, [1] drafted,

@@ -17,6 +17,8 @@ struct tt_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // identities of the drafted set, overlapped with verify
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   SelScratch sel;
   // drafted set of the current round
@@ -433,11 +435,18 @@ int tt_ctx_create(int device, tt_ctx** out) {
     return false;
   };
   if (bad(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking))) return TT_E_CUDA;
+  if (bad(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking))) return TT_E_CUDA;
+  if (bad(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming))) return TT_E_CUDA;
+  if (bad(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming))) return TT_E_CUDA;
   c->stream = c->own;
   if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.hist, 0, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.skey, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.sidx, 4096 * sizeof(int64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.sample, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.sfp, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.rank, 4096 * sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.dup, 4096 * sizeof(int)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.tkeys, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.tvals, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.tkeys, 0xff, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
@@ -462,7 +471,7 @@ void tt_ctx_destroy(tt_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (auto& pr : c->ev_live) cudaEventDestroy(pr.second.first), cudaEventDestroy(pr.second.second);
-  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.skey, c->sel.sidx, c->sel.tkeys, c->sel.tvals, c->sel.state,
+  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.skey, c->sel.sidx, c->sel.sample, c->sel.sfp, c->sel.rank, c->sel.dup, c->sel.tkeys, c->sel.tvals, c->sel.state,
                   c->sel.invalid,
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
@@ -471,6 +480,9 @@ void tt_ctx_destroy(tt_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_record) cudaFreeHost(c->h_record);
+  if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -748,20 +760,32 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
 // rounds, otherwise they are computed for those b only.
 int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg,
                       CandRef ref) {
+  const bool by_id = ref.id != nullptr;
+  if (!by_id) {  // fork: identities of the drafted set on the side stream
+    TT_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+    TT_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    if (launch_drafted_identity(S, ref.soa, ref.ld, ref.s0, ref.seeded ? cfg->first : ref.index_base,
+                                ref.seeded != 0, ctx->d_idx, ctx->d_count, cfg->k, ctx->d_id, ctx->side))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    TT_LAUNCHED(ctx);
+    TT_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+  }
   int rc = score_drafted(ctx, S, D, ref, cfg->k, cfg->precision, cfg->b, cfg->band > 0 ? cfg->band : 0.05,
                          ctx->d_count);
   if (rc) return rc;
   const bool certified = cfg->precision != TT_PREC_FP64;
   prof_begin(ctx, 3);
-  launch_select_top(ctx->d_score, ctx->d_cost, certified ? ctx->d_excluded : nullptr, cfg->k, ctx->d_count, cfg->b,
-                    ctx->d_pos, ctx->d_pos_count, ctx->d_status, ctx->stream);
-  const bool by_id = ref.id != nullptr;
-  launch_gather(ctx->d_pos, ctx->d_pos_count, ctx->d_count, ctx->sel.state, nullptr, ctx->d_sublist_count,
-                ctx->d_idx, ctx->d_cost, by_id ? ctx->d_id : nullptr, ctx->d_score, cfg->b, ctx->d_record, ctx->stream);
-  if (!by_id)
-    launch_selected_identity(S, ref.soa, ref.ld, ref.s0, ref.seeded ? cfg->first : ref.index_base, ref.seeded != 0,
-                             ctx->d_pos, ctx->d_pos_count, ctx->d_idx, cfg->b,
-                             (uint64_t*)(ctx->d_record + 4 + 3 * cfg->b), ctx->stream);
+  if (!by_id) TT_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));  // join
+  const uint8_t* excl = certified ? ctx->d_excluded : nullptr;
+  if (launch_finish(ctx->d_score, ctx->d_cost, excl, cfg->k, ctx->d_count, cfg->b, ctx->d_idx, ctx->d_id,
+                    ctx->sel.state, ctx->d_sublist_count, ctx->d_record, ctx->stream)) {
+    // large draft sets / batches: tiled select_top, then the record gather
+    if (launch_select_top(ctx->d_score, ctx->d_cost, excl, cfg->k, ctx->d_count, cfg->b, ctx->d_pos,
+                          ctx->d_pos_count, ctx->d_status, ctx->stream))
+      return fail(ctx, TT_E_CONFIG, "select_top: draft_size too large for the batch");
+    launch_gather(ctx->d_pos, ctx->d_pos_count, ctx->d_count, ctx->sel.state, nullptr, ctx->d_sublist_count,
+                  ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, cfg->b, ctx->d_record, ctx->stream);
+  }
   prof_end(ctx, 3);
   TT_LAUNCHED(ctx);
   TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_record, ctx->d_record, sizeof(int64_t) * (4 + 4 * cfg->b),

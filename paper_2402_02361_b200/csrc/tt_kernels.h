@@ -29,8 +29,8 @@ struct SelState {
   uint32_t survivors;
   uint32_t unique;
   int64_t count;
-  uint32_t nsurv;  // appended survivors
-  uint32_t _pad;
+  uint32_t nsurv;   // appended survivors
+  uint32_t ticket;  // CTAs finished in the current fast-select kernel (last one finalises)
 };
 
 struct SelScratch {
@@ -39,6 +39,10 @@ struct SelScratch {
   uint32_t* hist = nullptr;  // 4096 bins, zero between uses
   uint64_t* skey = nullptr;  // 4096 survivor keys
   int64_t* sidx = nullptr;   // 4096 survivor indices
+  uint64_t* sample = nullptr;  // 4096 sampled cost keys (fast path threshold)
+  uint64_t* sfp = nullptr;     // 4096 survivor fingerprints (fast path)
+  int* rank = nullptr;         // 4096 survivor ranks (fast path, zeroed per round)
+  int* dup = nullptr;          // 4096 survivor duplicate flags
   uint64_t* tkeys = nullptr;  // hash table (tie fallback), all-ones between uses
   uint64_t* tvals = nullptr;
   SelState* state = nullptr;
@@ -61,6 +65,10 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
                   int64_t* out_count, cudaStream_t st, bool hash = false);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);
+// identities of the drafted set (side stream)
+int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
+                            bool seeded, const int64_t* idx, const int64_t* count_dev, int64_t k_max, uint64_t* out,
+                            cudaStream_t st);
 int launch_selected_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
                              bool seeded, const int64_t* pos, const int64_t* pos_count, const int64_t* idx, int64_t b,
                              uint64_t* out, cudaStream_t st);
@@ -106,6 +114,10 @@ int launch_band(const double* fast, const int64_t* n_dev, int64_t n_max, const i
                 cudaStream_t st);
 int launch_gd_step(double* params, const double* grads, int64_t n, double lr, cudaStream_t st);
 int launch_momentum(double* phi, const double* target, int64_t n, double m, cudaStream_t st);
+// select_top + the round record in one CTA (n <= 1024, b <= 32); -1 otherwise
+int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
+                  const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
+                  const int* rescored, int64_t* out, cudaStream_t st);
 int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
                   const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
                   const uint64_t* id, const double* scores, int64_t b, int64_t* out, cudaStream_t st);
