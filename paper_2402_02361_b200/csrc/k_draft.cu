@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Sr
 // survivors report OVERFLOW (the identity-keyed hash path takes over).
 constexpr int kFastThreads = 1024;
 constexpr int kFastE = kFastCap / kFastThreads;  // 4 keys per thread
-constexpr int kRankChunk = 256;
+constexpr int kRankChunk = 128;
 
 __device__ __forceinline__ bool last_cta(SelState* st) {
   __shared__ int am_last;
@@ -455,14 +455,15 @@ __device__ __forceinline__ bool last_cta(SelState* st) {
   return am_last != 0;
 }
 
-// Key of rank r (0-based) among keys[0..n) in shared memory: MSB-first
-// radix select, 8 bits per pass. Whole CTA; returns the key to every thread.
+// Upper bound of the key of rank r (0-based) among keys[0..n) in shared
+// memory: MSB-first radix select over the top 24 bits, 8 bits per pass
+// (three passes), low bits filled with ones. Whole CTA; every thread gets it.
 __device__ uint64_t block_radix_select(const uint64_t* keys, int n, int r, int* hist) {
   __shared__ uint64_t s_prefix;
   __shared__ int s_r;
   uint64_t prefix = 0, mask = 0;
   int rr = r;
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  for (int shift = 56; shift >= 40; shift -= 8) {
     for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
     __syncthreads();
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
@@ -494,7 +495,9 @@ __device__ uint64_t block_radix_select(const uint64_t* keys, int n, int r, int* 
     rr = s_r;
     __syncthreads();
   }
-  return prefix;
+  // the top 24 bits (sign, exponent, 12 mantissa bits) of the rank-r key,
+  // rounded up: a threshold >= that key, loose by < 2^-12 relative
+  return prefix | ((1ull << 40) - 1);
 }
 
 template <int NSP, int NRED, bool SEED>
@@ -685,15 +688,14 @@ template <int NSP, int NRED, bool SEED>
 static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
                      int64_t need, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
                      int64_t* out_count, cudaStream_t st) {
-  const int g = grid_for(n, kFastThreads, 148);
   tt::note_launch();
-  k_fsel_cost<NSP, NRED, SEED><<<g, kFastThreads, 0, st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
+  k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, kFastThreads, 148), kFastThreads, 0, st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
                                                           w.rank, w.dup, w.invalid);
   tt::note_launch();
   k_fsel_compact<NSP, NRED, SEED><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(S, src, w.cost, n, w.state, w.skey,
                                                                              w.sidx, w.sfp);
   tt::note_launch();
-  k_fsel_rank<NSP, NRED, SEED><<<148, kRankChunk, 0, st>>>(S, src, w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup);
+  k_fsel_rank<NSP, NRED, SEED><<<2 * 148, kRankChunk, 0, st>>>(S, src, w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup);
   constexpr size_t emit_smem = (size_t)kFastCap * (2 * sizeof(uint64_t) + 2 * sizeof(int));
   static bool init = false;
   if (!init) set_smem(k_fsel_emit<NSP, NRED, SEED>, emit_smem), init = true;

@@ -36,7 +36,7 @@ namespace tt {
 constexpr int kTcH = 64;            // hidden width of the tensor-core path
 constexpr int kTcCand = 16;         // candidates per CTA tile
 constexpr int kTcRows = 128;        // 16 candidates x 8 rows
-constexpr int kTcThreads = 128;     // one thread per row / TMEM lane
+constexpr int kTcThreads = 256;     // two threads per row / TMEM lane (column halves)
 
 // packed weight image (bytes), built once per tt_pacm_load by k_tc_pack
 constexpr uint32_t kOffW1 = 0;                        // bf16 [64 n][32 k]
@@ -105,12 +105,21 @@ constexpr uint32_t kSmX0 = (kPackBytes + 1023) / 1024 * 1024;  // feature tile b
 constexpr uint32_t kSmX1 = kSmX0 + kFeatTileBytes;            // feature tile buffer 1
 constexpr uint32_t kSmA2 = kSmX1 + kFeatTileBytes;            // tanh(D1 + b1), bf16 [128 x 64]
 constexpr uint32_t kSmA3 = kSmA2 + kTcRows * 64 * 2;          // tanh(D2 + be), bf16 [128 x 64]
-constexpr uint32_t kSmK = kSmA3 + kTcRows * 64 * 2;           // K rows, f32 [128 x 64]
-constexpr uint32_t kSmV = kSmK + kTcRows * 64 * 4;            // V rows, f32 [128 x 64]
-constexpr uint32_t kSmCat = kSmV + kTcRows * 64 * 4;          // [s | d] per candidate, f32 [16 x 128]
-constexpr uint32_t kSmBar = kSmCat + kTcCand * 128 * 4;
+constexpr int kLd = 65;                                        // padded row stride: conflict-free row writes
+constexpr uint32_t kSmK = kSmA3 + kTcRows * 64 * 2;           // K rows, f32 [128 x 65]
+constexpr uint32_t kSmV = kSmK + kTcRows * kLd * 4;           // V rows, f32 [128 x 65]
+constexpr uint32_t kSmCat = kSmV + kTcRows * kLd * 4;         // [s | d] per candidate, f32 [16 x 128]
+constexpr uint32_t kSmPart = kSmCat + kTcCand * 128 * 4;      // partial logits exchange, f32 [256 x 9]
+constexpr uint32_t kSmBar = kSmPart + kTcThreads * 9 * 4;
 constexpr uint32_t kSmTotal = kSmBar + 64;
 static_assert(kSmTotal <= 227 * 1024, "shared memory budget");
+
+// clock64 marks of CTA 0's first tile (phase latency probe, ttdbg_pacm_tc_clocks)
+__device__ long long g_clk_tc[16];
+#define TC_MARK(i)                                       \
+  do {                                                   \
+    if (blockIdx.x == 0 && t == 0 && it == 0) g_clk_tc[i] = clock64(); \
+  } while (0)
 
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;
@@ -141,6 +150,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
   float* kb = (float*)(sm + kSmK);
   float* vb = (float*)(sm + kSmV);
   float* cat = (float*)(sm + kSmCat);
+  float* part = (float*)(sm + kSmPart);
   uint64_t* bars = (uint64_t*)(sm + kSmBar);  // [0] weights, [1] MMA done, [2]/[3] feature buffers
   uint32_t* tslot = (uint32_t*)(sm + kSmBar + 32);
 
@@ -161,8 +171,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
     tc::bulk_g2s(sm + kSmX0, tiles + blockIdx.x * kFeatTileBytes, kFeatTileBytes, &bars[2]);
   }
   const float* bias = (const float*)(wp + kOffBias);
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const int c = t >> 3, i = t & 7;
+  // two threads per TMEM lane / row: warps w and w + 4 share lanes 32(w%4).., halves of the columns
+  const int row = t & 127, hf = t >> 7;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const int c = row >> 3, i = row & 7;
   constexpr uint32_t LBO_A = kTcRows * 16;  // 2048: next 8-wide K chunk of a 128-row tile
   const uint32_t sa2 = tc::smem_u32(a2), sa3 = tc::smem_u32(a3), sw = tc::smem_u32(wp);
   uint32_t mma_phase = 0;
@@ -171,6 +183,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
     const int buf = it & 1;
     uint8_t* xs = sm + (buf ? kSmX1 : kSmX0);
     const uint32_t sxs = tc::smem_u32(xs), sxb = sxs + kFeatTileBytes / 2;
+    TC_MARK(0);
     if (t == 0) {
       if (tile + stride < ntiles) {  // prefetch the next tile into the other buffer
         tc::mbar_expect_tx(&bars[2 + (buf ^ 1)], kFeatTileBytes);
@@ -193,26 +206,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
     tc::mbar_wait(&bars[1], mma_phase & 1u);
     ++mma_phase;
     tc::tc_fence_after();
+    TC_MARK(1);
 
-    // ---- epilogue 1: tanh(D1 + b1) -> A2, tanh(D2 + be) -> A3 (bf16) ----
-#pragma unroll 1
-    for (int ch = 0; ch < 4; ++ch) {
+    // ---- epilogue 1: tanh(D1 + b1) -> A2, tanh(D2 + be) -> A3 (bf16); half hf does columns 32hf.. ----
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int ch = 2 * hf + cc;
       float v[16];
       tc::tmem_ld16(trow + 16 * ch, v);
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = tanh_fast(v[q] + bias[16 * ch + q]);
-      st_bf16x8(a2, tc::kmaj_off(t, 16 * ch, kTcRows), v);
-      st_bf16x8(a2, tc::kmaj_off(t, 16 * ch + 8, kTcRows), v + 8);
+      st_bf16x8(a2, tc::kmaj_off(row, 16 * ch, kTcRows), v);
+      st_bf16x8(a2, tc::kmaj_off(row, 16 * ch + 8, kTcRows), v + 8);
       tc::tmem_ld16(trow + 64 + 16 * ch, v);
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = tanh_fast(v[q] + bias[64 + 16 * ch + q]);
-      st_bf16x8(a3, tc::kmaj_off(t, 16 * ch, kTcRows), v);
-      st_bf16x8(a3, tc::kmaj_off(t, 16 * ch + 8, kTcRows), v + 8);
+      st_bf16x8(a3, tc::kmaj_off(row, 16 * ch, kTcRows), v);
+      st_bf16x8(a3, tc::kmaj_off(row, 16 * ch + 8, kTcRows), v + 8);
     }
     tc::fence_async_smem();
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
+    TC_MARK(2);
     if (t == 0) {
       const uint32_t id64 = tc::idesc_bf16_f32(128, 64), id192 = tc::idesc_bf16_f32(128, 192);
 #pragma unroll
@@ -227,55 +243,71 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
     tc::mbar_wait(&bars[1], mma_phase & 1u);
     ++mma_phase;
     tc::tc_fence_after();
+    TC_MARK(3);
 
     // ---- epilogue 2a: statement branch, tanh(D3 + b2), masked sum over rows ----
     {
       float* z = vb;  // staging (V is written later)
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int ch = 2 * hf + cc;
         float v[16];
         tc::tmem_ld16(trow + 128 + 16 * ch, v);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) z[t * 64 + 16 * ch + q] = i < n_stmt ? tanh_fast(v[q] + bias[128 + 16 * ch + q]) : 0.f;
+        for (int q = 0; q < 16; ++q)
+          z[row * kLd + 16 * ch + q] = i < n_stmt ? tanh_fast(v[q] + bias[128 + 16 * ch + q]) : 0.f;
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {  // candidate c, columns 8i..8i+7 (concat[0:h] = sum of rows)
-        const int j = 8 * i + q;
-        float s = 0.f;
-        for (int rr = 0; rr < n_stmt; ++rr) s += z[(8 * c + rr) * 64 + j];
-        cat[c * 128 + j] = s;
+      for (int q = 0; q < 4; ++q) {  // candidate c, columns 8i + 4hf + q (concat[0:h] = sum of rows)
+        const int j = 8 * i + 4 * hf + q;
+        float acc = 0.f;
+        for (int rr = 0; rr < n_stmt; ++rr) acc += z[(8 * c + rr) * kLd + j];
+        cat[c * 128 + j] = acc;
       }
       __syncthreads();
     }
-    // ---- epilogue 2b: Q (registers), K and V (shared) with biases ----
-    float qv[64];
+    TC_MARK(4);
+    // ---- epilogue 2b: Q half (registers), K and V halves (shared) with biases ----
+    float qv[32];
 #pragma unroll
-    for (int ch = 0; ch < 4; ++ch) {
+    for (int cc = 0; cc < 2; ++cc) {
+      const int ch = 2 * hf + cc;
       float v[16];
       tc::tmem_ld16(trow + 192 + 16 * ch, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) qv[16 * ch + q] = v[q] + bias[192 + 16 * ch + q];
+      for (int q = 0; q < 16; ++q) qv[16 * cc + q] = v[q] + bias[192 + 16 * ch + q];
       tc::tmem_ld16(trow + 256 + 16 * ch, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) kb[t * 64 + 16 * ch + q] = v[q] + bias[256 + 16 * ch + q];
+      for (int q = 0; q < 16; ++q) kb[row * kLd + 16 * ch + q] = v[q] + bias[256 + 16 * ch + q];
       tc::tmem_ld16(trow + 320 + 16 * ch, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) vb[t * 64 + 16 * ch + q] = v[q] + bias[320 + 16 * ch + q];
+      for (int q = 0; q < 16; ++q) vb[row * kLd + 16 * ch + q] = v[q] + bias[320 + 16 * ch + q];
     }
     tc::tc_fence_before();  // TMEM reads of this tile done before the next tile's MMAs
     __syncthreads();
+    TC_MARK(5);
     // ---- attention within the candidate (rows 8c .. 8c+B-1) ----
     {
       const float scale = 0.125f;  // 1 / sqrt(64)
       float lg[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) lg[u] = 0.f;
+      // partial logits over this half's 32 dimensions, 8 independent chains
+#pragma unroll 4
+      for (int q = 0; q < 32; ++q) {
+        const float x = qv[q];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) lg[u] = fmaf(x, kb[(8 * c + u) * kLd + 32 * hf + q], lg[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) part[t * 9 + u] = lg[u];
+      __syncthreads();
+      const int pt = t ^ 128;  // the partner thread: same row, other half
       float mx = -3.0e38f;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        float d = 0.f;
-        const float* kr = kb + (8 * c + u) * 64;
-#pragma unroll 16
-        for (int q = 0; q < 64; ++q) d = fmaf(qv[q], kr[q], d);
+        const float d = hf == 0 ? lg[u] + part[pt * 9 + u] : part[pt * 9 + u] + lg[u];
         lg[u] = u < n_block ? d * scale : -3.0e38f;
         mx = fmaxf(mx, lg[u]);
       }
@@ -297,42 +329,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
         lg[u] = pu / (float)n_block;
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int j = 8 * i + q;
-        float s = 0.f;
+      for (int q = 0; q < 4; ++q) {
+        const int j = 8 * i + 4 * hf + q;
+        float acc = 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s = fmaf(lg[u], u < n_block ? vb[(8 * c + u) * 64 + j] : 0.f, s);
-        cat[c * 128 + 64 + j] = s;
+        for (int u = 0; u < 8; ++u) acc = fmaf(lg[u], u < n_block ? vb[(8 * c + u) * kLd + j] : 0.f, acc);
+        cat[c * 128 + 64 + j] = acc;
       }
     }
     __syncthreads();
-    // ---- head: tanh([s|d] W1h + b1h) . w2h + b2h ----
+    TC_MARK(6);
+    // ---- head: tanh([s|d] W1h + b1h) . w2h + b2h; thread (c, i, hf) owns columns 8i + 4hf .. +3 ----
     {
       const float* hw1 = (const float*)(wp + kOffHw1);
       const float* hb1 = (const float*)(wp + kOffHb1);
       const float* hw2 = (const float*)(wp + kOffHw2);
-      float g[8];
+      const int j0 = 8 * i + 4 * hf;
+      float g[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) g[q] = hb1[8 * i + q];
+      for (int q = 0; q < 4; ++q) g[q] = hb1[j0 + q];
       const float* cr = cat + c * 128;
-#pragma unroll 4
+#pragma unroll 8
       for (int m = 0; m < 128; ++m) {
         const float x = cr[m];
-        const float4 w0 = *(const float4*)(hw1 + m * 64 + 8 * i);
-        const float4 w1 = *(const float4*)(hw1 + m * 64 + 8 * i + 4);
+        const float4 w0 = *(const float4*)(hw1 + m * 64 + j0);
         g[0] = fmaf(x, w0.x, g[0]), g[1] = fmaf(x, w0.y, g[1]), g[2] = fmaf(x, w0.z, g[2]), g[3] = fmaf(x, w0.w, g[3]);
-        g[4] = fmaf(x, w1.x, g[4]), g[5] = fmaf(x, w1.y, g[5]), g[6] = fmaf(x, w1.z, g[6]), g[7] = fmaf(x, w1.w, g[7]);
       }
-      float part = 0.f;
+      float pp = 0.f;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) part = fmaf(tanh_fast(g[q]), hw2[8 * i + q], part);
-      part += __shfl_xor_sync(0xffffffffu, part, 1);
-      part += __shfl_xor_sync(0xffffffffu, part, 2);
-      part += __shfl_xor_sync(0xffffffffu, part, 4);
+      for (int q = 0; q < 4; ++q) pp = fmaf(tanh_fast(g[q]), hw2[j0 + q], pp);
+      pp += __shfl_xor_sync(0xffffffffu, pp, 1);
+      pp += __shfl_xor_sync(0xffffffffu, pp, 2);
+      pp += __shfl_xor_sync(0xffffffffu, pp, 4);
+      if (hf == 1 && i == 0) part[t * 9] = pp;
+      __syncthreads();
       const int64_t pos = tile * kTcCand + c;
-      if (i == 0 && pos < count) score_out[pos] = (double)(part + *(const float*)(wp + kOffHb2));
+      if (hf == 0 && i == 0 && pos < count)
+        score_out[pos] = (double)((pp + part[(t ^ 128) * 9]) + *(const float*)(wp + kOffHb2));
+      TC_MARK(7);
     }
-    __syncthreads();  // cat / kb / vb reused by the next tile
+    __syncthreads();  // cat / kb / vb / part reused by the next tile
     tc::tc_fence_after();
   }
   tc::tc_fence_before();
@@ -358,3 +394,7 @@ int launch_pacm_tc(const uint8_t* tiles, int n_stmt, int n_block, const int64_t*
 }
 
 }  // namespace tt
+
+extern "C" int ttdbg_pacm_tc_clocks(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_clk_tc, sizeof(long long) * (n < 16 ? n : 16));
+}

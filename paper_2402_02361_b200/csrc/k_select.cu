@@ -364,6 +364,72 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
   }
 }
 
+// Certification band for the tensor-core path, one CTA (n <= 1024,
+// b <= 32): the b-th best fast key by select_top's order (warp sorts + a
+// tournament, as k_finish), then every candidate whose fast score is within
+// 2 * band of it goes on the fp64 rescoring sublist; the rest are excluded
+// from the final selection. If every fast error is below `band`, excluded
+// candidates are provably outside the true top-b.
+__global__ void __launch_bounds__(1024) k_cert_band(const double* __restrict__ fast,
+                                                    const double* __restrict__ drafts, int64_t n_max,
+                                                    const int64_t* __restrict__ n_dev, int64_t b, double band,
+                                                    int32_t* __restrict__ sublist, int* __restrict__ sublist_count,
+                                                    uint8_t* __restrict__ excluded) {
+  __shared__ Key3 lists[32][33];
+  __shared__ double thr;
+  __shared__ int cnt;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int64_t n = n_dev ? (*n_dev < n_max ? *n_dev : n_max) : n_max;
+  const bool ok = t < n;
+  Key3 k;
+  k.a = ok ? ~ordered(fast[t]) : kAll;
+  k.b = ok ? ordered(drafts[t]) : kAll;
+  k.c = ok ? (uint32_t)t : 0xffffffffu;
+  warp_sort32(k);
+  lists[warp][lane] = k;
+  if (lane == 0) lists[warp][32].a = kAll, lists[warp][32].b = kAll, lists[warp][32].c = 0xffffffffu, cnt = 0;
+  if (t == 0) thr = -1.0e300;
+  __syncthreads();
+  if (warp == 0) {
+    int head = 0;
+    uint32_t last = 0xffffffffu;
+    const int64_t keep = b < n ? b : n;
+    for (int it = 0; it < keep; ++it) {
+      Key3 h;
+      if (lane < nw) h = lists[lane][head];
+      else h.a = kAll, h.b = kAll, h.c = 0xffffffffu;
+      Key3 m = h;
+      int who = lane;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const Key3 o = m.shfl_xor(off);
+        const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+        if (o.lt(m)) m = o, who = ow;
+      }
+      last = m.c;
+      if (lane == who) ++head;
+    }
+    if (lane == 0 && last != 0xffffffffu) thr = fast[last] - 2.0 * band;
+  }
+  __syncthreads();
+  if (t < n_max) {
+    const bool in = ok && fast[t] >= thr;
+    excluded[t] = in ? 0 : 1;
+    if (in) sublist[atomicAdd(&cnt, 1)] = t;
+  }
+  __syncthreads();
+  if (t == 0) *sublist_count = cnt;
+}
+
+int launch_cert_band(const double* fast, const double* drafts, int64_t n_max, const int64_t* n_dev, int64_t b,
+                     double band, int32_t* sublist, int* sublist_count, uint8_t* excluded, cudaStream_t st) {
+  if (n_max > 1024 || b > 32) return -1;
+  const int nt = (int)((n_max + 31) / 32 * 32);
+  tt::note_launch();
+  k_cert_band<<<1, nt, 0, st>>>(fast, drafts, n_max, n_dev, b, band, sublist, sublist_count, excluded);
+  return 0;
+}
+
 int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
                   const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
                   const int* rescored, int64_t* out, cudaStream_t st) {

@@ -725,7 +725,9 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
   if (!pacm_tc_supported(ns, nb, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
   if ((rc = ensure_packed(ctx))) return rc;
   prof_begin(ctx, 1);
-  if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, nullptr, nullptr, ctx->d_tiles, ctx->stream))
+  // fp64 rows as well: the certification rescoring reads them (no second feature pass)
+  if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, b > 0 ? ctx->d_xs : nullptr,
+                       b > 0 ? ctx->d_xb : nullptr, ctx->d_tiles, ctx->stream))
     return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
   if (launch_pacm_tc(ctx->d_tiles, ns, nb, count_dev, k_max, ctx->d_packed, ctx->h, ctx->d_score_fast, ctx->stream))
     return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
@@ -733,15 +735,15 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
   TT_LAUNCHED(ctx);
   if (b > 0) {
     prof_begin(ctx, 2);
-    launch_select_top(ctx->d_score_fast, ctx->d_cost, nullptr, k_max, count_dev, b, ctx->d_pos_fast,
-                      ctx->d_pos_fast_count, ctx->d_status + 1, ctx->stream);
-    launch_band(ctx->d_score_fast, count_dev, k_max, ctx->d_pos_fast, ctx->d_pos_fast_count, band, ctx->d_sublist,
-                ctx->d_sublist_count, ctx->d_excluded, ctx->stream);
+    if (launch_cert_band(ctx->d_score_fast, ctx->d_cost, k_max, count_dev, b, band, ctx->d_sublist,
+                         ctx->d_sublist_count, ctx->d_excluded, ctx->stream)) {
+      launch_select_top(ctx->d_score_fast, ctx->d_cost, nullptr, k_max, count_dev, b, ctx->d_pos_fast,
+                        ctx->d_pos_fast_count, ctx->d_status + 1, ctx->stream);
+      launch_band(ctx->d_score_fast, count_dev, k_max, ctx->d_pos_fast, ctx->d_pos_fast_count, band, ctx->d_sublist,
+                  ctx->d_sublist_count, ctx->d_excluded, ctx->stream);
+    }
     TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_score, ctx->d_score_fast, sizeof(double) * k_max, cudaMemcpyDeviceToDevice,
                                  ctx->stream));
-    if (launch_feat_rows(S, D, ref, count_dev, k_max, ctx->d_sublist, ctx->d_sublist_count, ctx->d_xs, ctx->d_xb,
-                         nullptr, ctx->stream))
-      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     if (launch_pacm64(ctx->d_xs, ctx->d_xb, ns, nb, count_dev, k_max, ctx->d_sublist, ctx->d_sublist_count,
                       ctx->d_params, ctx->h, 0, ctx->d_score, ctx->stream))
       return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");

@@ -118,6 +118,9 @@ int launch_momentum(double* phi, const double* target, int64_t n, double m, cuda
 int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
                   const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
                   const int* rescored, int64_t* out, cudaStream_t st);
+// fast top-b + certification band in one CTA (n <= 1024, b <= 32); -1 otherwise
+int launch_cert_band(const double* fast, const double* drafts, int64_t n_max, const int64_t* n_dev, int64_t b,
+                     double band, int32_t* sublist, int* sublist_count, uint8_t* excluded, cudaStream_t st);
 int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
                   const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
                   const uint64_t* id, const double* scores, int64_t b, int64_t* out, cudaStream_t st);
