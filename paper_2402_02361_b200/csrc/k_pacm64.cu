@@ -155,8 +155,8 @@ __device__ __forceinline__ void dense_row64(int lt, const double* __restrict__ x
 // shared-memory doubles: transposed activations (rows padded to 4)
 __host__ __device__ inline size_t act64_doubles(int S, int B, int h) {
   const int sp = pad4(S), bp = pad4(B);
-  // xs^T, xb^T, z1^T, z2^T, e^T, q^T, k^T, v^T, ao^T, pr, cat, gp, g, s
-  return (size_t)24 * sp + 23 * bp + 2 * h * sp + 5 * h * bp + B * B + 2 * h + 2 * h + 2;
+  // xs^T, xb^T, z1^T, z2^T, e^T, q^T, k^T, v^T, ao^T, pr, cat, gp, g, hw2
+  return (size_t)24 * sp + 23 * bp + 2 * h * sp + 5 * h * bp + B * B + 2 * h + 2 * h + h + 2;
 }
 __host__ __device__ inline size_t wbuf64_doubles(int h) { return (size_t)(h * h > 24 * h ? h * h : 24 * h); }
 
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
   double* cat = pr + B * B;     // [2h]
   double* gp = cat + 2 * h;     // [h]
   double* g = gp + h;           // [h]
+  double* hw2s = g + h;         // [h] head layer-2 weights (staged per pass)
   const Params64 P = split_params(params, h);
   const WStages W = weight_stages(P, h, identity != 0);
   int64_t count = k_max;
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
         const int k = u / bp, i = u - k * bp;
         xb[u] = i < B ? block[(pos * B + i) * 23 + k] : 0.0;
       }
+      for (int u = lt; u < h; u += kT64) hw2s[u] = __ldg(P.hw2 + u);
     }
     __syncthreads();
     int s = 0;
@@ -322,7 +324,8 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
 #undef TT_STAGE
     if (live && lt == 0) {  // head layer 2: 1 x h -> 1, one chain
       double acc = 0.0;
-      for (int k = 0; k < h; ++k) acc = __dadd_rn(acc, __dmul_rn(g[k], __ldg(P.hw2 + k)));
+#pragma unroll 8
+      for (int k = 0; k < h; ++k) acc = __dadd_rn(acc, __dmul_rn(g[k], hw2s[k]));
       score_out[pos] = __dadd_rn(acc, __ldg(P.hb2));
     }
     __syncthreads();

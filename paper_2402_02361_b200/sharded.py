@@ -55,11 +55,11 @@ class ShardedRound:
             self._bufs[k] = (self.ctx.empty((3, k), torch.int64), self.ctx.empty((self.world * 3 * k,), torch.int64))
         return self._bufs[k]
 
-    def local(self, sketch: Sketch, dev: DeviceSpec, first: int, n: int, k: int, seed: int = 0,
+    def local(self, sketch: Sketch, dev: DeviceSpec, first: int, n: int, k: int, b: int = 1, seed: int = 0,
               soa: torch.Tensor | None = None, toggles: int = TT_TOGGLES_ALL) -> torch.Tensor:
         """Draft half: this rank's [3, k] payload (async on the ctx stream)."""
         payload, _ = self._buffers(k)
-        tt.round_local_async(self.ctx, sketch, dev, n, k, 0, first, payload, seed=seed, soa=soa, toggles=toggles)
+        tt.round_local_async(self.ctx, sketch, dev, n, k, b, first, payload, seed=seed, soa=soa, toggles=toggles)
         return payload
 
     def run_async(self, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, seed: int = 0,
@@ -70,9 +70,13 @@ class ShardedRound:
             n_total = n
         else:
             first, n_local, n_total = self.rank * n, n, n * self.world
-        payload = self.local(sketch, dev, first, n_local, k, seed=seed, soa=soa, toggles=toggles)
+        payload = self.local(sketch, dev, first, n_local, k, b, seed=seed, soa=soa, toggles=toggles)
         _, gathered = self._buffers(k)
-        self.dist.all_gather_into_tensor(gathered, payload.reshape(-1), group=self.group)
+        if self.dist.get_backend(self.group) == "nccl":
+            self.dist.all_gather_into_tensor(gathered, payload.reshape(-1), group=self.group)
+        else:  # gloo (CPU tests, single-GPU multi-rank emulation): list form
+            parts = list(gathered.view(self.world, -1).unbind(0))
+            self.dist.all_gather(parts, payload.reshape(-1).contiguous(), group=self.group)
         tt.round_finish_merged_async(self.ctx, sketch, dev, gathered, n_total, k, b, precision=precision, band=band)
 
     def run(self, *a, **kw) -> tt.RoundOutput:

@@ -106,9 +106,10 @@ def schedule_identity(ctx: Context, sketch: Sketch, soa: torch.Tensor) -> torch.
     return ids
 
 
-def schedule_from_identity(ctx: Context, sketch: Sketch, ids: torch.Tensor) -> torch.Tensor:
+def schedule_from_identity(ctx: Context, sketch: Sketch, ids: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """schedule_from_key's replacement: exact identities -> SoA factor columns (async)."""
     n = ids.shape[0]
-    soa = ctx.empty((sketch.cols, n), torch.int32)
+    soa = ctx.empty((sketch.cols, n), torch.int32) if out is None else out
     ctx.check(lib().tt_schedule_from_identity(ctx.h, C.byref(sketch), _p(ids), n, _p(soa), n))
     return soa
 
