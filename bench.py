@@ -265,28 +265,59 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+FLOP_PER_CAND = 320640  # PaCM forward at h = 64, S = 6, B = 8
+
+
+def _traffic():
+    """dram read+write bytes per launch from the committed ncu capture (profiles/), or {}."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
 def roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec):
-    """Roofline of the dominant stage, from the live per-stage event timings."""
+    """Roofline of the round's dominant kernel from live CUDA-event timings
+    (per launch, on the context stream), plus the other hot kernels."""
     if not stage_ms:
         return None
-    dom = max(stage_ms, key=stage_ms.get)
-    if dom == "select":
-        # SA draft + top-K: algorithmic bytes = factor columns read + cost
-        # write + cost re-reads (compaction); SURVEY §8d per-candidate
-        per = [4 * (4 * sk.op.n_spatial + 3 * sk.op.n_reduction) + 8 + 8 for sk in sketches]
+    traffic = _traffic()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    out = {}
+    if "draft_cost" in stage_ms:
+        # K1: factor columns read (unroll column not read) + fp64 cost written, per candidate
+        per = [4 * (4 * sk.op.n_spatial + 3 * sk.op.n_reduction) + 8 for sk in sketches]
         byts = args.n * sum(per) / len(per)
-        ach = byts / (stage_ms[dom] * 1e-3) / 1e9
-        peak = peaks["hbm_gbs"]
-        return {"bound": "hbm", "kernel": "draft select (K1 cost+hist, K2 scan/compact/finalize)",
-                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
-                "peak_source": peaks_kind, "stage_ms": stage_ms[dom]}
-    flops = args.k * 320640.0
-    ach = flops / (stage_ms[dom] * 1e-3) / 1e12
-    peak = peaks["bf16_tflops"]
-    return {"bound": "tensor", "kernel": f"PaCM verify ({'tcgen05 bf16' if prec else 'fp64 CUDA cores'})",
-            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-            "peak_source": peaks_kind + " bf16 dense (burst)", "stage_ms": stage_ms[dom],
-            "flop_per_candidate": 320640}
+        ms = stage_ms["draft_cost"]
+        ach = byts / (ms * 1e-3) / 1e9
+        out["draft_cost"] = {"bound": "hbm", "kernel": "k_fsel_cost (K1 SA draft cost + sample threshold)",
+                             "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": ach / peaks["hbm_gbs"], "traffic": traffic.get("k_fsel_cost"),
+                             "algorithmic_bytes": byts, "ms": ms, "peak_source": peaks_kind}
+    if "pacm_kernel" in stage_ms:
+        ms = stage_ms["pacm_kernel"]
+        ach = args.k * FLOP_PER_CAND / (ms * 1e-3) / 1e12
+        if prec:
+            peak = peaks["bf16_tflops"]
+            out["pacm_kernel"] = {"bound": "tensor", "kernel": "k_pacm_tc (tcgen05 bf16, TMEM accumulators)",
+                                  "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                                  "traffic": traffic.get("k_pacm_tc"), "flop_per_candidate": FLOP_PER_CAND,
+                                  "ms": ms, "peak_source": peaks_kind + " bf16 dense (burst)"}
+        else:
+            # CUDA-core fp64, no FMA contraction (bit-exact sums): 64 DMUL/DADD lanes/clk/SM measured
+            # (tools/fp64_bench.cu) -> each multiply-add costs 2 lane-ops
+            peak = 64 * 148 * sm_mhz * 1e6 / 1e12
+            out["pacm_kernel"] = {"bound": "fp64", "kernel": "k_pacm64 (fp64 CUDA cores, reference order)",
+                                  "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                                  "traffic": traffic.get("k_pacm64"), "flop_per_candidate": FLOP_PER_CAND,
+                                  "ms": ms, "peak_source": "measured fp64 lane rate x 148 SMs x max SM clock"}
+    if not out:
+        return None
+    dom = max(out, key=lambda k: out[k]["ms"])
+    res = dict(out[dom])
+    res["others"] = {k: v for k, v in out.items() if k != dom}
+    return res
 
 
 # ------------------------------------------------------------------------------------ reference --

@@ -195,7 +195,8 @@ int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_
                                  const tt_round_config* cfg, const double* cost_dev, const int64_t* gidx_dev,
                                  const uint64_t* identity_dev, int64_t m);
 /* Stage timing with CUDA events on the context stream (0 draft select,
- * 1 PaCM, 2 certification rescoring, 3 select_top + gather, 4 merge).
+ * 1 PaCM (features + model), 2 certification rescoring, 3 select_top + record, 4 merge, 5 PaCM kernel
+ * alone, 6 feature rows alone, 7 the K1 draft-cost kernel alone).
  * tt_profile_read synchronises, returns per-stage summed ms and counts
  * since the last read. */
 int tt_profile_enable(tt_ctx* ctx, int on);

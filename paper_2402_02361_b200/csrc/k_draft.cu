@@ -37,7 +37,8 @@ constexpr int kTableCap = 16384;       // hash slots of the fallback path
 constexpr int kSortE = 4;              // keys per thread in the 4096-entry sorts
 constexpr int kFinalE = 1;             // keys per thread in the 1024-entry sorts (1024 threads)
 constexpr uint64_t kEmpty = ~0ull;
-constexpr int kFastCap = 4096;  // survivors the fast path's last CTA sorts
+constexpr int kFastCap = 4096;               // survivors the fast path ranks
+constexpr int64_t kFastMaxN = int64_t{2} << 20;  // fast path population limit
 
 static int grid_for(int64_t n, int threads, int max_blocks) {
   int64_t g = (n + threads - 1) / threads;
@@ -422,8 +423,8 @@ __global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Sr
 // grid-wide or O(log) passes):
 //   k_fsel_cost:    K1 over the population, costs to HBM, a strided sample of
 //                   <= 4096 cost keys; the last CTA (ticket) radix-selects the
-//                   sample key of rank 2 * ceil(need * ns / n) + 16 as the
-//                   survivor threshold (~2.5x need survivors expected).
+//                   sample key of rank 2 * ceil(need * ns / n) + 4 as the
+//                   survivor threshold (~2x need survivors expected).
 //   k_fsel_compact: keys <= threshold appended (warp-aggregated) with a
 //                   schedule fingerprint (seeded: the exact identity the
 //                   generator returns; explicit: a 64-bit hash of the factor
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
   const int ns = (int)((n + stride - 1) / stride);
   for (int e = threadIdx.x; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
   __syncthreads();
-  int64_t r = 2 * ((need * ns + n - 1) / n) + 16;
+  int64_t r = 2 * ((need * ns + n - 1) / n) + 4;
   const bool all = r >= ns - 1;
   const uint64_t thr = all ? ~0ull : block_radix_select(keys, ns, (int)r, hist);
   if (threadIdx.x == 0) {
@@ -688,9 +689,11 @@ template <int NSP, int NRED, bool SEED>
 static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
                      int64_t need, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
                      int64_t* out_count, cudaStream_t st) {
+  if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);
   tt::note_launch();
   k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, kFastThreads, 148), kFastThreads, 0, st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
                                                           w.rank, w.dup, w.invalid);
+  if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
   tt::note_launch();
   k_fsel_compact<NSP, NRED, SEED><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(S, src, w.cost, n, w.state, w.skey,
                                                                              w.sidx, w.sfp);
@@ -877,9 +880,11 @@ static void run_small(const DevSketch& S, const DevDevice& D, const Src& src, in
   const size_t sm = sort_smem_bytes(kFinalCap);
   static bool init = false;
   if (!init) set_smem(k_sel_small<NSP, NRED, SEED>, sm), init = true;
+  if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);  // the whole one-CTA selection stands in for K1
   tt::note_launch();
   k_sel_small<NSP, NRED, SEED><<<1, kFinalCap / kFinalE, sm, st>>>(S, D, src, n, toggles, k, w.state, out_idx,
                                                                    out_cost, out_id, out_count, w.invalid);
+  if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
 }
 
 template <int NSP, int NRED, bool SEED>
@@ -917,13 +922,17 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
       return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, true>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
     return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, false>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
   }
-  if (!hash) {
+  // sampled threshold keeps ~(r + 1) * n / 4096 survivors >= 7 n / 4096: within the
+  // 4096-entry cap up to ~2M candidates; larger populations use the histogram path
+  if (!hash && n <= kFastMaxN) {
     if (seeded)
       return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_fast<NSP, NRED, true>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)));
     return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_fast<NSP, NRED, false>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)));
   }
   {
+    if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);
     int rc = launch_draft_cost(S, D, soa, ld, s0, first, seeded, n, toggles, w.cost, w.hist, w.invalid, st);
+    if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
     if (rc) return rc;
   }
   tt::note_launch();

@@ -93,6 +93,18 @@ void prof_begin(tt_ctx* c, int stage) {
   cudaEventRecord(c->ev_open[stage], c->stream);
 }
 
+// K1 events handed to the selector (recorded around its cost kernel)
+void prof_k1_arm(tt_ctx* c) {
+  if (!c->prof) return;
+  c->sel.k1_ev[0] = ev_get(c);
+  c->sel.k1_ev[1] = ev_get(c);
+}
+void prof_k1_collect(tt_ctx* c) {
+  if (!c->sel.k1_ev[0]) return;
+  c->ev_live.push_back({7, {c->sel.k1_ev[0], c->sel.k1_ev[1]}});
+  c->sel.k1_ev[0] = c->sel.k1_ev[1] = nullptr;
+}
+
 void prof_end(tt_ctx* c, int stage) {
   if (!c->prof || !c->ev_open[stage]) return;
   cudaEvent_t e = ev_get(c);
@@ -711,11 +723,15 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
   if (rc) return rc;
   if (precision == TT_PREC_FP64) {
     prof_begin(ctx, 1);
+    prof_begin(ctx, 6);
     if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, ctx->d_xs, ctx->d_xb, nullptr, ctx->stream))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    prof_end(ctx, 6);
+    prof_begin(ctx, 5);
     if (launch_pacm64(ctx->d_xs, ctx->d_xb, ns, nb, count_dev, k_max, nullptr, nullptr, ctx->d_params, ctx->h, 0,
                       ctx->d_score, ctx->stream))
       return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");
+    prof_end(ctx, 5);
     prof_end(ctx, 1);
     TT_LAUNCHED(ctx);
     TT_CUDA(ctx, cudaMemsetAsync(ctx->d_sublist_count, 0, sizeof(int), ctx->stream));
@@ -725,12 +741,16 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
   if (!pacm_tc_supported(ns, nb, ctx->h)) return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: unsupported shape/width");
   if ((rc = ensure_packed(ctx))) return rc;
   prof_begin(ctx, 1);
+  prof_begin(ctx, 6);
   // fp64 rows as well: the certification rescoring reads them (no second feature pass)
   if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, b > 0 ? ctx->d_xs : nullptr,
                        b > 0 ? ctx->d_xb : nullptr, ctx->d_tiles, ctx->stream))
     return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  prof_end(ctx, 6);
+  prof_begin(ctx, 5);
   if (launch_pacm_tc(ctx->d_tiles, ns, nb, count_dev, k_max, ctx->d_packed, ctx->h, ctx->d_score_fast, ctx->stream))
     return fail(ctx, TT_E_CONFIG, "tensor-core PaCM launch");
+  prof_end(ctx, 5);
   prof_end(ctx, 1);
   TT_LAUNCHED(ctx);
   if (b > 0) {
@@ -820,9 +840,11 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
   if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
   prof_begin(ctx, 0);
+  prof_k1_arm(ctx);
   if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k, need, cfg->toggles,
                     cfg->first, ctx->sel, ctx->d_idx, ctx->d_cost, nullptr, ctx->d_count, ctx->stream, hash))
     return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  prof_k1_collect(ctx);
   prof_end(ctx, 0);
   TT_LAUNCHED(ctx);
   // the verifier re-derives each drafted candidate from its population

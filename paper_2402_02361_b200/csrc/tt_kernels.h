@@ -47,6 +47,7 @@ struct SelScratch {
   uint64_t* tvals = nullptr;
   SelState* state = nullptr;
   int* invalid = nullptr;
+  cudaEvent_t k1_ev[2] = {nullptr, nullptr};  // optional: recorded around the K1 cost kernel (profiling)
 };
 
 // k_draft.cu

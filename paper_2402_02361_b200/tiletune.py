@@ -378,7 +378,7 @@ def round_finish_merged_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, gat
                                                  _p(g[1]), _p(g[2]), g.shape[1]))
 
 
-STAGES = ["select", "pacm", "certify", "finish", "merge"]
+STAGES = ["select", "pacm", "certify", "finish", "merge", "pacm_kernel", "features", "draft_cost"]
 
 
 def profile_enable(ctx: Context, on: bool = True):
