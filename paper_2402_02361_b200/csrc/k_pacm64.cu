@@ -30,7 +30,6 @@
 
 namespace tt {
 
-constexpr int kT64 = 128;
 
 struct Params64 {
   const double *w1, *b1, *w2, *b2, *we, *be, *wq, *bq, *wk, *bk, *wv, *bv, *hw1, *hb1, *hw2, *hb2;
@@ -45,9 +44,9 @@ __host__ __device__ inline Params64 split_params(const double* p, int h) {
   return P;
 }
 
-constexpr int kRG = 4;  // rows per thread work item
-
-__host__ __device__ inline int pad4(int n) { return (n + kRG - 1) / kRG * kRG; }
+// Rows are padded to a multiple of 4 (16-byte activation loads); a thread
+// work item covers RG rows of one output column (RG independent chains).
+__host__ __device__ inline int pad4(int n) { return (n + 3) / 4 * 4; }
 
 // Branch-free fp64 exp and tanh. CUDA's tanh/exp take data-dependent
 // branches (range reduction special cases, division slow paths) that
@@ -103,29 +102,32 @@ __device__ __forceinline__ double tanh64(double x) {
 // +0.0, bias last). init == nullptr starts from +0.0; b == nullptr stores
 // the partial sum (a split k range continues from it bit-exactly). Padding
 // rows compute harmless finite values that no consumer reads.
+template <int RG, int T>
 __device__ __forceinline__ void dense64(int lt, const double* __restrict__ xt, int ldx, int n, int m,
                                         const double* __restrict__ W, int q, const double* __restrict__ init,
                                         const double* __restrict__ b, bool act, double* __restrict__ yt, int ldy) {
-  const int groups = (n + kRG - 1) / kRG;
-  for (int item = lt; item < q * groups; item += kT64) {
-    const int j = item % q, r0 = (item / q) * kRG;
-    double a[kRG];
+  const int groups = (n + RG - 1) / RG;
+  for (int item = lt; item < q * groups; item += T) {
+    const int j = item % q, r0 = (item / q) * RG;
+    double a[RG];
 #pragma unroll
-    for (int r = 0; r < kRG; ++r) a[r] = init ? init[j * ldy + r0 + r] : 0.0;
+    for (int r = 0; r < RG; ++r) a[r] = init ? init[j * ldy + r0 + r] : 0.0;
     const double* xp = xt + r0;
 #pragma unroll 4
     for (int k = 0; k < m; ++k) {
       const double w = W[k * q + j];
       const double2 x01 = *(const double2*)(xp + k * ldx);
-      const double2 x23 = *(const double2*)(xp + k * ldx + 2);
       a[0] = __dadd_rn(a[0], __dmul_rn(x01.x, w));
       a[1] = __dadd_rn(a[1], __dmul_rn(x01.y, w));
-      a[2] = __dadd_rn(a[2], __dmul_rn(x23.x, w));
-      a[3] = __dadd_rn(a[3], __dmul_rn(x23.y, w));
+      if constexpr (RG == 4) {
+        const double2 x23 = *(const double2*)(xp + k * ldx + 2);
+        a[2] = __dadd_rn(a[2], __dmul_rn(x23.x, w));
+        a[3] = __dadd_rn(a[3], __dmul_rn(x23.y, w));
+      }
     }
     const double bj = b ? __ldg(b + j) : 0.0;
 #pragma unroll
-    for (int r = 0; r < kRG; ++r) {
+    for (int r = 0; r < RG; ++r) {
       double z = a[r];
       if (b) {
         z = __dadd_rn(z, bj);
@@ -137,10 +139,11 @@ __device__ __forceinline__ void dense64(int lt, const double* __restrict__ xt, i
 }
 
 // y[j] = act(init[j] + sum_{k<m} x[k] * W[k][j] (+ b[j])) for one row.
+template <int T>
 __device__ __forceinline__ void dense_row64(int lt, const double* __restrict__ x, int m, const double* __restrict__ W,
                                             int q, const double* init, const double* __restrict__ b, bool act,
                                             double* y) {
-  for (int j = lt; j < q; j += kT64) {
+  for (int j = lt; j < q; j += T) {
     double a = init[j];
 #pragma unroll 8
     for (int k = 0; k < m; ++k) a = __dadd_rn(a, __dmul_rn(x[k], W[k * q + j]));
@@ -156,7 +159,8 @@ __device__ __forceinline__ void dense_row64(int lt, const double* __restrict__ x
 __host__ __device__ inline size_t act64_doubles(int S, int B, int h) {
   const int sp = pad4(S), bp = pad4(B);
   // xs^T, xb^T, z1^T, z2^T, e^T, q^T, k^T, v^T, ao^T, pr, cat, gp, g, hw2
-  return (size_t)24 * sp + 23 * bp + 2 * h * sp + 5 * h * bp + B * B + 2 * h + 2 * h + h + 2;
+  const size_t d = (size_t)24 * sp + 23 * bp + 2 * h * sp + 5 * h * bp + B * B + 2 * h + 2 * h + h + 2;
+  return (d + 3) & ~(size_t)3;  // keeps every group's 16-byte activation loads aligned
 }
 __host__ __device__ inline size_t wbuf64_doubles(int h) { return (size_t)(h * h > 24 * h ? h * h : 24 * h); }
 
@@ -183,6 +187,7 @@ __device__ __forceinline__ WStages weight_stages(const Params64& P, int h, bool 
 
 // G candidate groups of kT64 threads per CTA share each staged weight block
 // (G = 4 for whole drafted sets, 1 for the short certification sublists).
+template <int RG, int kT64>
 __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ stmt,
                                                      const double* __restrict__ block, int n_stmt, int n_block,
                                                      const int64_t* __restrict__ count_dev, int64_t k_max,
@@ -264,14 +269,14 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
     issue(s + 2);                                      \
     ++s;                                               \
   } while (0)
-    TT_STAGE(dense64(lt, xs, sp, S, 24, Wm, h, nullptr, P.b1, true, z1, sp));
-    TT_STAGE(dense64(lt, z1, sp, S, h, Wm, h, nullptr, P.b2, true, z2, sp));
-    TT_STAGE(dense64(lt, xb, bp, B, 23, Wm, h, nullptr, P.be, true, e, bp));
+    TT_STAGE((dense64<RG, kT64>(lt, xs, sp, S, 24, Wm, h, nullptr, P.b1, true, z1, sp)));
+    TT_STAGE((dense64<RG, kT64>(lt, z1, sp, S, h, Wm, h, nullptr, P.b2, true, z2, sp)));
+    TT_STAGE((dense64<RG, kT64>(lt, xb, bp, B, 23, Wm, h, nullptr, P.be, true, e, bp)));
     const double* pooled = e;
     if (!identity) {
-      TT_STAGE(dense64(lt, e, bp, B, h, Wm, h, nullptr, P.bq, false, qm, bp));
-      TT_STAGE(dense64(lt, e, bp, B, h, Wm, h, nullptr, P.bk, false, km, bp));
-      TT_STAGE(dense64(lt, e, bp, B, h, Wm, h, nullptr, P.bv, false, vm, bp));
+      TT_STAGE((dense64<RG, kT64>(lt, e, bp, B, h, Wm, h, nullptr, P.bq, false, qm, bp)));
+      TT_STAGE((dense64<RG, kT64>(lt, e, bp, B, h, Wm, h, nullptr, P.bk, false, km, bp)));
+      TT_STAGE((dense64<RG, kT64>(lt, e, bp, B, h, Wm, h, nullptr, P.bv, false, vm, bp)));
       const double scale = __ddiv_rn(1.0, sqrt((double)h));
       if (live)
         for (int u = lt; u < B * B; u += kT64) {  // matmul_nt (ranker.cpp:102-111), then scale
@@ -319,8 +324,8 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
       }
     __syncthreads();
     // head layer 1 over k = 0..2h-1 (1 row), split in two weight stages
-    TT_STAGE(dense_row64(lt, cat, h, Wm, h, gp, nullptr, false, gp));
-    TT_STAGE(dense_row64(lt, cat + h, h, Wm, h, gp, P.hb1, true, g));
+    TT_STAGE((dense_row64<kT64>(lt, cat, h, Wm, h, gp, nullptr, false, gp)));
+    TT_STAGE((dense_row64<kT64>(lt, cat + h, h, Wm, h, gp, P.hb1, true, g)));
 #undef TT_STAGE
     if (live && lt == 0) {  // head layer 2: 1 x h -> 1, one chain
       double acc = 0.0;
@@ -345,16 +350,18 @@ int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_blo
   G = G > 4 ? 4 : G;
   if (sublist) G = 1;  // a few candidates: one per CTA, latency first
   const size_t sm = wbytes + (size_t)G * abytes;
-  static size_t set = 0;
-  if (sm > 48 * 1024 && sm > set) {
-    cudaFuncSetAttribute(k_pacm64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    set = sm;
-  }
   const int64_t ctas = (k_max + G - 1) / G, cap = sublist ? 64 : 8 * 148;
   const unsigned grid = (unsigned)(ctas < cap ? ctas : cap);
-  tt::note_launch();
-  k_pacm64<<<grid, G * kT64, sm, st>>>(stmt, block, n_stmt, n_block, count_dev, k_max, sublist, sublist_count, params,
-                                      h, attention_identity, score_out);
+  auto go = [&](auto kern, int threads) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tt::note_launch();
+    kern<<<grid, G * threads, sm, st>>>(stmt, block, n_stmt, n_block, count_dev, k_max, sublist, sublist_count,
+                                        params, h, attention_identity, score_out);
+  };
+  // whole drafted sets: 4 chains per thread, 128 threads per candidate (throughput);
+  // certification sublists: 2 chains per thread, 256 threads per candidate (latency)
+  if (sublist) go(k_pacm64<2, 256>, 256);
+  else go(k_pacm64<4, 128>, 128);
   return 0;
 }
 
