@@ -22,16 +22,12 @@
 // Identical schedules have identical costs, so the threshold never splits
 // a duplicate group; selection is exact for any input.
 #include <cstdint>
-#include <cstdlib>
-
-#include <cooperative_groups.h>
 
 #include "tt_block.cuh"
 #include "tt_device.cuh"
 #include "tt_kernels.h"
 
 namespace tt {
-namespace cg = cooperative_groups;
 
 constexpr int kHistBins = 4096;
 constexpr int kSurvivorTarget = 1024;  // refine while more keys survive
@@ -42,7 +38,8 @@ constexpr int kSortE = 4;              // keys per thread in the 4096-entry sort
 constexpr int kFinalE = 1;             // keys per thread in the 1024-entry sorts (1024 threads)
 constexpr uint64_t kEmpty = ~0ull;
 constexpr int kFastCap = 4096;               // survivors the fast path ranks
-constexpr int64_t kFastMaxN = int64_t{2} << 20;  // fast path population limit
+constexpr int kSampleMax = 32768;            // sampled cost keys (top 32 bits) for the threshold
+constexpr int64_t kFastMaxN = int64_t{16} << 20;  // fast path population limit
 
 static int grid_for(int64_t n, int threads, int max_blocks) {
   int64_t g = (n + threads - 1) / threads;
@@ -426,9 +423,9 @@ __global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Sr
 // sort of 4096 keys costs ~60 us on one SM; everything here is either
 // grid-wide or O(log) passes):
 //   k_fsel_cost:    K1 over the population, costs to HBM, a strided sample of
-//                   <= 4096 cost keys; the last CTA (ticket) radix-selects the
-//                   sample key of rank 2 * ceil(need * ns / n) + 4 as the
-//                   survivor threshold (~2x need survivors expected).
+//                   4096..32768 cost keys (top 32 bits); the last CTA (ticket) radix-selects the
+//                   sample key of rank ceil(1.5 need ns / n) + 3 as the
+//                   survivor threshold (~1.5x need survivors expected).
 //   k_fsel_compact: keys <= threshold appended (warp-aggregated) with a
 //                   schedule fingerprint (seeded: the exact identity the
 //                   generator returns; explicit: a 64-bit hash of the factor
@@ -460,19 +457,19 @@ __device__ __forceinline__ bool last_cta(SelState* st) {
   return am_last != 0;
 }
 
-// Upper bound of the key of rank r (0-based) among keys[0..n) in shared
-// memory: MSB-first radix select over the top 24 bits, 8 bits per pass
-// (three passes), low bits filled with ones. Whole CTA; every thread gets it.
-__device__ uint64_t block_radix_select(const uint64_t* keys, int n, int r, int* hist) {
-  __shared__ uint64_t s_prefix;
+// Upper bound of the 64-bit cost key whose top 32 bits have rank r (0-based)
+// among keys[0..n) in shared memory: MSB-first radix select, 8 bits per pass
+// (four passes), the low 32 bits filled with ones. Whole CTA.
+__device__ uint64_t block_radix_select(const uint32_t* keys, int n, int r, int* hist) {
+  __shared__ uint32_t s_prefix;
   __shared__ int s_r;
-  uint64_t prefix = 0, mask = 0;
+  uint32_t prefix = 0, mask = 0;
   int rr = r;
-  for (int shift = 56; shift >= 40; shift -= 8) {
+  for (int shift = 24; shift >= 0; shift -= 8) {
     for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d] = 0;
     __syncthreads();
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      const uint64_t k = keys[e];
+      const uint32_t k = keys[e];
       if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1);
     }
     __syncthreads();
@@ -490,30 +487,35 @@ __device__ uint64_t block_radix_select(const uint64_t* keys, int n, int r, int* 
       int run = incl - tot;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        if (run <= rr && rr < run + c[q]) s_prefix = (uint64_t)(lane * 8 + q), s_r = rr - run;
+        if (run <= rr && rr < run + c[q]) s_prefix = (uint32_t)(lane * 8 + q), s_r = rr - run;
         run += c[q];
       }
     }
     __syncthreads();
     prefix |= s_prefix << shift;
-    mask |= 255ull << shift;
+    mask |= 255u << shift;
     rr = s_r;
     __syncthreads();
   }
-  // the top 24 bits (sign, exponent, 12 mantissa bits) of the rank-r key,
-  // rounded up: a threshold >= that key, loose by < 2^-12 relative
-  return prefix | ((1ull << 40) - 1);
+  // the top 32 bits (sign, exponent, 20 mantissa bits) of the rank-r key,
+  // rounded up: a threshold >= that key, loose by < 2^-20 relative
+  return ((uint64_t)prefix << 32) | 0xffffffffull;
 }
 
 template <int NSP, int NRED, bool SEED>
 __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevice D, Src src, int64_t n,
                                                             int toggles, int64_t need, double* __restrict__ cost,
-                                                            uint64_t* __restrict__ sample, SelState* __restrict__ st,
+                                                            uint32_t* __restrict__ sample, SelState* __restrict__ st,
                                                             int* __restrict__ rank_acc, int* __restrict__ dup,
                                                             int* __restrict__ invalid) {
-  __shared__ uint64_t keys[kFastCap];
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* keys = (uint32_t*)smem;  // the last CTA's copy of the sample
   __shared__ int hist[256];
-  const int64_t stride = (n + kFastCap - 1) / kFastCap;
+  // n / 256 samples, clamped to [4096, 32768]: each sample stands for <= 512
+  // candidates, so the rank-r threshold keeps ~(r + 1) * stride survivors
+  const int64_t want = n / 256 > kFastCap ? (n / 256 < kSampleMax ? n / 256 : kSampleMax) : kFastCap;
+  int64_t stride = 1;  // a power of two: the per-candidate sample test is a mask, not a 64-bit modulo
+  while (stride * want < n) stride <<= 1;
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     Factors<NSP, NRED> F;
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
     if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
     const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles);
     cost[i] = c;
-    if (i % stride == 0) sample[i / stride] = cost_key(c);
+    if ((i & (stride - 1)) == 0) sample[i / stride] = (uint32_t)(cost_key(c) >> 32);
   }
   // zero the rank kernel's accumulators for this round
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kFastCap; e += gridDim.x * blockDim.x)
@@ -531,7 +533,9 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
   const int ns = (int)((n + stride - 1) / stride);
   for (int e = threadIdx.x; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
   __syncthreads();
-  int64_t r = 2 * ((need * ns + n - 1) / n) + 4;
+  // expected survivors ~1.5x need (+3 samples): below need only ~3.5 sigma out
+  // (then NEED_MORE and a retry with a larger need)
+  int64_t r = (3 * need * ns + 2 * n - 1) / (2 * n) + 3;
   const bool all = r >= ns - 1;
   const uint64_t thr = all ? ~0ull : block_radix_select(keys, ns, (int)r, hist);
   if (threadIdx.x == 0) {
@@ -695,7 +699,9 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
                      int64_t* out_count, cudaStream_t st) {
   if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);
   tt::note_launch();
-  k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, kFastThreads, 148), kFastThreads, 0, st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
+  static bool init_cost = false;
+  if (!init_cost) set_smem(k_fsel_cost<NSP, NRED, SEED>, kSampleMax * sizeof(uint32_t)), init_cost = true;
+  k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, kFastThreads, 148), kFastThreads, kSampleMax * sizeof(uint32_t), st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
                                                           w.rank, w.dup, w.invalid);
   if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
   tt::note_launch();
@@ -709,195 +715,6 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   tt::note_launch();
   k_fsel_emit<NSP, NRED, SEED><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
                                                           out_idx, out_cost, out_id, out_count);
-}
-
-// The same four phases as ONE cooperative kernel (grid-wide barriers instead
-// of kernel boundaries): phase A = K1 costs + sample, B = threshold (CTA 0),
-// C = compaction + fingerprints, D = all-pairs ranking in 128-thread
-// sub-groups (named barriers), E = emit (CTA 0). Used when the grid fits
-// co-resident (one 1024-thread CTA per SM); run_fast above is the fallback.
-template <int NSP, int NRED, bool SEED>
-__global__ void __launch_bounds__(kFastThreads) k_fsel_fused(DevSketch S, DevDevice D, Src src, int64_t n,
-                                                             int toggles, int64_t need, int64_t k,
-                                                             double* __restrict__ cost, uint64_t* __restrict__ sample,
-                                                             SelState* __restrict__ st, int* __restrict__ rank_acc,
-                                                             int* __restrict__ dup, int* __restrict__ invalid,
-                                                             uint64_t* __restrict__ skey, int64_t* __restrict__ sidx,
-                                                             uint64_t* __restrict__ sfp, int64_t* __restrict__ out_idx,
-                                                             double* __restrict__ out_cost,
-                                                             uint64_t* __restrict__ out_id,
-                                                             int64_t* __restrict__ out_count) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int hist[256];
-  __shared__ int wt[32];
-  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  // ---- A: costs + sample; reset per-round accumulators
-  const int64_t stride = (n + kFastCap - 1) / kFastCap;
-  bool bad = false;
-  for (int64_t i = gt; i < n; i += gsz) {
-    Factors<NSP, NRED> F;
-    load_cand<NSP, NRED, SEED>(S, src, i, F, false);
-    if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
-    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles);
-    cost[i] = c;
-    if (i % stride == 0) sample[i / stride] = cost_key(c);
-  }
-  for (int64_t e = gt; e < kFastCap; e += gsz) rank_acc[e] = 0, dup[e] = 0;
-  if (bad) atomicOr(invalid, 1);
-  if (gt == 0) st->nsurv = 0;
-  grid.sync();
-  // ---- B: survivor threshold (CTA 0)
-  if (blockIdx.x == 0) {
-    uint64_t* keys = (uint64_t*)smem;
-    const int ns = (int)((n + stride - 1) / stride);
-    for (int e = threadIdx.x; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
-    __syncthreads();
-    int64_t r = 2 * ((need * ns + n - 1) / n) + 4;
-    const bool all = r >= ns - 1;
-    const uint64_t thr = all ? ~0ull : block_radix_select(keys, ns, (int)r, hist);
-    if (threadIdx.x == 0) {
-      st->prefix = thr, st->shift = 0, st->all = all ? 1 : 0, st->need = need;
-      st->status = 0, st->count = 0, st->done = 1, st->ticket = 0;
-    }
-  }
-  grid.sync();
-  // ---- C: compaction (+ fingerprints)
-  {
-    const uint64_t thr = *(volatile uint64_t*)&st->prefix;
-    for (int64_t base = gt - lane; base < n; base += gsz) {
-      const int64_t i = base + lane;
-      uint64_t key = 0;
-      bool keep = false;
-      if (i < n) {
-        key = cost_key(__ldcg(cost + i));
-        keep = key <= thr;
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (!m) continue;
-      uint32_t pos0 = 0;
-      if (lane == 0) pos0 = atomicAdd(&st->nsurv, (uint32_t)__popc(m));
-      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
-      if (keep) {
-        const uint32_t p = pos0 + __popc(m & ((1u << lane) - 1u));
-        if (p < (uint32_t)kFastCap) {
-          Factors<NSP, NRED> F;
-          const uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, true);
-          skey[p] = key, sidx[p] = i;
-          sfp[p] = SEED ? id : fingerprint<NSP, NRED>(F);
-        }
-      }
-    }
-  }
-  grid.sync();
-  // ---- D: all-pairs ranking, 8 sub-groups of 128 threads per CTA
-  const uint32_t nsurv = *(volatile uint32_t*)&st->nsurv;
-  if (nsurv <= (uint32_t)kFastCap) {
-    const int m = (int)nsurv;
-    const int chunks = (m + kRankChunk - 1) / kRankChunk;
-    const int sg = threadIdx.x / kRankChunk, vt = threadIdx.x - sg * kRankChunk;
-    uint64_t* ck = (uint64_t*)smem + sg * 3 * kRankChunk;
-    uint64_t* cf = ck + kRankChunk;
-    int64_t* ci = (int64_t*)(cf + kRankChunk);
-    const int nsg = kFastThreads / kRankChunk;
-    for (int blk = blockIdx.x * nsg + sg; blk < chunks * chunks; blk += gridDim.x * nsg) {
-      const int ce = blk / chunks, cj = blk - ce * chunks;
-      const int j0 = cj * kRankChunk;
-      asm volatile("bar.sync %0, %1;" ::"r"(sg + 1), "r"(kRankChunk));
-      if (j0 + vt < m) ck[vt] = skey[j0 + vt], ci[vt] = sidx[j0 + vt], cf[vt] = sfp[j0 + vt];
-      asm volatile("bar.sync %0, %1;" ::"r"(sg + 1), "r"(kRankChunk));
-      const int e = ce * kRankChunk + vt;
-      if (e >= m) continue;
-      const uint64_t ke = skey[e], fe = sfp[e];
-      const int64_t ie = sidx[e];
-      const int jn = min(kRankChunk, m - j0);
-      int below = 0;
-      bool d = false;
-      for (int q = 0; q < jn; ++q) {
-        const uint64_t kq = ck[q];
-        const int64_t iq = ci[q];
-        below += kq < ke || (kq == ke && iq < ie);
-        if (kq == ke && iq < ie && cf[q] == fe && !d) d = same_schedule<NSP, NRED, SEED>(S, src, ie, iq);
-      }
-      if (below) atomicAdd(rank_acc + e, below);
-      if (d) atomicOr(dup + e, 1);
-    }
-  }
-  grid.sync();
-  // ---- E: emit (CTA 0)
-  if (blockIdx.x != 0) return;
-  if (nsurv > (uint32_t)kFastCap) {
-    if (threadIdx.x == 0) st->status |= TT_SEL_OVERFLOW, *out_count = 0;
-    return;
-  }
-  const int m = (int)nsurv;
-  uint64_t* a = (uint64_t*)smem;
-  int64_t* bi = (int64_t*)(a + kFastCap);
-  int* flag = (int*)(bi + kFastCap);
-  int* pos = flag + kFastCap;
-  for (int e = threadIdx.x; e < kFastCap; e += blockDim.x) flag[e] = 0;
-  __syncthreads();
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    const int r = __ldcg(rank_acc + e);
-    a[r] = __ldcg(skey + e);
-    bi[r] = __ldcg(sidx + e);
-    flag[r] = __ldcg(dup + e) ? 0 : 1;
-  }
-  __syncthreads();
-  const int total = block_exclusive_scan(flag, pos, kFastCap, wt);
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    if (flag[e] && pos[e] < k) {
-      const int o = pos[e];
-      out_idx[o] = bi[e] + src.index_base;
-      out_cost[o] = key_cost(a[e]);
-      if (out_id) out_id[o] = identity_at<NSP, NRED, SEED>(S, src, bi[e]);
-    }
-  }
-  if (threadIdx.x == 0) {
-    const int64_t cnt = total < k ? total : k;
-    *out_count = cnt;
-    st->count = cnt;
-    const bool everything = st->all || (int64_t)m >= n;
-    if (cnt < k && !everything) st->status |= TT_SEL_NEED_MORE;
-  }
-}
-
-template <int NSP, int NRED, bool SEED>
-static bool run_fused(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
-                      int64_t need, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
-                      int64_t* out_count, cudaStream_t st) {
-  constexpr size_t smem = (size_t)kFastCap * (2 * sizeof(uint64_t) + 2 * sizeof(int));  // emit; >= the others
-  static int max_ctas = -1;
-  if (max_ctas < 0) {
-    set_smem(k_fsel_fused<NSP, NRED, SEED>, smem);
-    int per_sm = 0, sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fsel_fused<NSP, NRED, SEED>, kFastThreads, smem);
-    max_ctas = per_sm * sms;
-  }
-  if (max_ctas < 1) return false;
-  int g = grid_for(n, kFastThreads, max_ctas);
-  DevSketch s_ = S;
-  DevDevice d_ = D;
-  Src src_ = src;
-  int64_t n_ = n, need_ = need, k_ = k;
-  int tg_ = toggles;
-  double* cost = w.cost;
-  uint64_t* sample = w.sample;
-  SelState* state = w.state;
-  int *rank = w.rank, *dupp = w.dup, *inv = w.invalid;
-  uint64_t *skey = w.skey, *sfp = w.sfp;
-  int64_t* sidx = w.sidx;
-  void* args[] = {&s_, &d_, &src_, &n_, &tg_, &need_, &k_, &cost, &sample, &state, &rank, &dupp, &inv,
-                  &skey, &sidx, &sfp, &out_idx, &out_cost, &out_id, &out_count};
-  if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);
-  tt::note_launch();
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_fsel_fused<NSP, NRED, SEED>, dim3(g),
-                                                    dim3(kFastThreads), args, smem, st);
-  if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
-  return e == cudaSuccess;
 }
 
 // ---------------------------------------------- hash fallback (ties) ----
@@ -1105,18 +922,6 @@ static void run_tail(const DevSketch& S, const Src& src, int64_t n, int64_t k, b
   }
 }
 
-// TT_SELECT_FUSED=1 selects the cooperative single-kernel variant. Measured
-// on B200 at N = 65,536 it is not faster than the four kernels (the grid
-// barriers cost what the launch gaps did), so the four kernels are default.
-static bool fused_ok() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TT_SELECT_FUSED");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, int64_t ld, uint64_t s0,
                   int64_t first, bool seeded, int64_t n, int64_t k, int64_t need, int toggles,
                   int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
@@ -1127,15 +932,8 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
       return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, true>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
     return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_small<NSP, NRED, false>(S, D, src, n, toggles, k, w, out_idx, out_cost, out_id, out_count, st)));
   }
-  // sampled threshold keeps ~(r + 1) * n / 4096 survivors >= 7 n / 4096: within the
-  // 4096-entry cap up to ~2M candidates; larger populations use the histogram path
-  if (!hash && n <= kFastMaxN && fused_ok()) {
-    bool ok = true;
-    int rc = seeded ? TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (ok = run_fused<NSP, NRED, true>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)))
-                    : TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (ok = run_fused<NSP, NRED, false>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)));
-    if (rc == 0 && ok) return 0;
-    cudaGetLastError();  // fall through to the multi-kernel fast path
-  }
+  // the sampled threshold keeps ~(r + 1) * n / ns survivors: within the 4096-entry
+  // cap up to ~16M candidates; larger populations use the histogram path
   if (!hash && n <= kFastMaxN) {
     if (seeded)
       return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (run_fast<NSP, NRED, true>(S, D, src, n, toggles, k, need, w, out_idx, out_cost, out_id, out_count, st)));

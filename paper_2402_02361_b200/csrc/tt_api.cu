@@ -455,7 +455,7 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaMemset(c->sel.hist, 0, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.skey, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.sidx, 4096 * sizeof(int64_t)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->sel.sample, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.sample, 32768 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.sfp, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.rank, 4096 * sizeof(int)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.dup, 4096 * sizeof(int)))) return TT_E_CUDA;

@@ -39,7 +39,7 @@ struct SelScratch {
   uint32_t* hist = nullptr;  // 4096 bins, zero between uses
   uint64_t* skey = nullptr;  // 4096 survivor keys
   int64_t* sidx = nullptr;   // 4096 survivor indices
-  uint64_t* sample = nullptr;  // 4096 sampled cost keys (fast path threshold)
+  uint32_t* sample = nullptr;  // <= 32768 sampled cost keys, top 32 bits (fast path threshold)
   uint64_t* sfp = nullptr;     // 4096 survivor fingerprints (fast path)
   int* rank = nullptr;         // 4096 survivor ranks (fast path, zeroed per round)
   int* dup = nullptr;          // 4096 survivor duplicate flags
