@@ -4,8 +4,10 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "../../include/tt/tt.h"
@@ -66,6 +68,11 @@ struct tt_ctx {
   uint64_t last_seed = 0;
   int64_t last_need = 0;
   bool last_hash = false;
+  // CUDA graphs of whole rounds, keyed by every argument that shapes the
+  // enqueued work (sketch, device, config, population pointer, seed, need);
+  // cleared whenever scratch is reallocated
+  bool graphs = true;
+  std::map<std::string, std::pair<cudaGraphExec_t, uint64_t>> graph_cache;  // exec, kernel launches
   // stage profiling with CUDA events on the ctx stream
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -306,9 +313,15 @@ int compile_device(tt_ctx* ctx, const tt_device_spec* d, DevDevice& D) {
   return TT_OK;
 }
 
+void graphs_clear(tt_ctx* ctx) {
+  for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.first);
+  ctx->graph_cache.clear();
+}
+
 template <typename T>
 int grow(tt_ctx* ctx, T*& p, int64_t& cap, int64_t want) {
   if (want <= cap && p) return TT_OK;
+  graphs_clear(ctx);
   if (p) cudaFree(p);
   p = nullptr;
   TT_CUDA(ctx, cudaMalloc((void**)&p, sizeof(T) * (size_t)(want > 0 ? want : 1)));
@@ -318,6 +331,7 @@ int grow(tt_ctx* ctx, T*& p, int64_t& cap, int64_t want) {
 
 int ensure_k(tt_ctx* ctx, int64_t k) {
   if (k <= ctx->k_cap) return TT_OK;
+  graphs_clear(ctx);
   cudaFree(ctx->d_idx), cudaFree(ctx->d_cost), cudaFree(ctx->d_id), cudaFree(ctx->d_score);
   cudaFree(ctx->d_score_fast), cudaFree(ctx->d_excluded), cudaFree(ctx->d_sublist);
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_idx, sizeof(int64_t) * k));
@@ -333,6 +347,7 @@ int ensure_k(tt_ctx* ctx, int64_t k) {
 
 int ensure_b(tt_ctx* ctx, int64_t b) {
   if (b <= ctx->b_cap) return TT_OK;
+  graphs_clear(ctx);
   cudaFree(ctx->d_pos), cudaFree(ctx->d_pos_fast), cudaFree(ctx->d_record);
   if (ctx->h_record) cudaFreeHost(ctx->h_record);
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos, sizeof(int64_t) * b));
@@ -349,6 +364,7 @@ int ensure_cost(tt_ctx* ctx, int64_t n) { return grow(ctx, ctx->sel.cost, ctx->s
 // blocks <= 20: ops with up to 6 inputs) and their tensor-core tile image
 int ensure_feat(tt_ctx* ctx, int64_t k) {
   if (k <= ctx->feat_cap) return TT_OK;
+  graphs_clear(ctx);
   cudaFree(ctx->d_xs), cudaFree(ctx->d_xb), cudaFree(ctx->d_tiles);
   ctx->d_xs = nullptr, ctx->d_xb = nullptr, ctx->d_tiles = nullptr;
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_xs, sizeof(double) * 14 * TT_STMT_WIDTH * k));
@@ -451,6 +467,7 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming))) return TT_E_CUDA;
   if (bad(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming))) return TT_E_CUDA;
   c->stream = c->own;
+  if (const char* g = getenv("TT_GRAPHS")) c->graphs = g[0] != '0';
   if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.hist, 0, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.skey, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
@@ -492,6 +509,7 @@ void tt_ctx_destroy(tt_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_record) cudaFreeHost(c->h_record);
+  graphs_clear(c);
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -681,6 +699,7 @@ int tt_pacm_load(tt_ctx* ctx, const double* params, int h) {
   if (h < 1 || h > 512) return fail(ctx, TT_E_STATE, "hidden width must be in [1, 512]");
   const int64_t np = tt_param_count(h);
   if (ctx->h != h) {
+    graphs_clear(ctx);
     if (ctx->d_params) cudaFree(ctx->d_params);
     if (ctx->d_packed) cudaFree(ctx->d_packed);
     ctx->d_params = nullptr, ctx->d_packed = nullptr;
@@ -702,7 +721,10 @@ namespace {
 
 int ensure_packed(tt_ctx* ctx) {
   if (ctx->packed_ok) return TT_OK;
-  if (!ctx->d_packed) TT_CUDA(ctx, cudaMalloc(&ctx->d_packed, pacm_tc_packed_bytes(ctx->h)));
+  if (!ctx->d_packed) {
+    graphs_clear(ctx);
+    TT_CUDA(ctx, cudaMalloc(&ctx->d_packed, pacm_tc_packed_bytes(ctx->h)));
+  }
   if (launch_pacm_tc_pack(ctx->d_params, ctx->h, ctx->d_packed, ctx->stream))
     return fail(ctx, TT_E_CONFIG, "tensor-core PaCM: packing failed");
   TT_LAUNCHED(ctx);
@@ -825,19 +847,12 @@ int check_round_cfg(tt_ctx* ctx, const tt_round_config* cfg) {
   return TT_OK;
 }
 
-int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
-                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need, bool hash = false) {
-  DevSketch S;
-  DevDevice D;
-  int rc = compile_sketch(ctx, sk, S);
-  if (rc) return rc;
-  if ((rc = compile_device(ctx, dev, D))) return rc;
-  if ((rc = check_round_cfg(ctx, cfg))) return rc;
-  if (!S.id_exact) return fail(ctx, TT_E_STATE, "round: schedule space exceeds 2^64 identities");
-  if ((rc = ensure_k(ctx, cfg->k))) return rc;
-  if ((rc = ensure_b(ctx, cfg->b))) return rc;
+// The device work of one round (select -> verify -> finish -> record copy),
+// enqueued on ctx->stream. Scratch must already be sized (no allocation
+// here), so the sequence can be captured into a CUDA graph.
+int round_body(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg, const int32_t* soa,
+               int64_t ld, uint64_t seed, int64_t need, bool hash) {
   const bool seeded = soa == nullptr;
-  if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
   if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
   prof_begin(ctx, 0);
   prof_k1_arm(ctx);
@@ -851,7 +866,56 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   // index: a SoA gather, or a counter-based regeneration
   CandRef ref = seeded ? CandRef{nullptr, 0, ctx->d_idx, 0, nullptr, seed_state(seed), 1, 0}
                        : CandRef{soa, ld, ctx->d_idx, cfg->first, nullptr, 0, 0, 0};
-  if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  return verify_and_select(ctx, S, D, cfg, ref);
+}
+
+int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need, bool hash = false) {
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if ((rc = check_round_cfg(ctx, cfg))) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "round: schedule space exceeds 2^64 identities");
+  if ((rc = ensure_k(ctx, cfg->k))) return rc;
+  if ((rc = ensure_b(ctx, cfg->b))) return rc;
+  if ((rc = ensure_feat(ctx, cfg->k))) return rc;
+  if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
+  if (cfg->precision == TT_PREC_BF16 && (rc = ensure_packed(ctx))) return rc;
+  if (!ctx->graphs || ctx->prof) {
+    if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash))) return rc;
+  } else {
+    // graph cache: the key is every byte that shapes the enqueued work
+    std::string key;
+    auto put = [&](const void* p, size_t n) { key.append((const char*)p, n); };
+    put(sk, sizeof(*sk)), put(dev, sizeof(*dev)), put(cfg, sizeof(*cfg)), put(&soa, sizeof(soa)), put(&ld, 8);
+    put(&seed, 8), put(&need, 8), put(&hash, 1), put(&ctx->h, sizeof(ctx->h));
+    auto it = ctx->graph_cache.find(key);
+    if (it == ctx->graph_cache.end()) {
+      cudaStream_t launch = ctx->stream;
+      const uint64_t l0 = tt_kernel_launches();
+      TT_CUDA(ctx, cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeRelaxed));
+      ctx->stream = ctx->own;
+      rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash);
+      ctx->stream = launch;
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(ctx->own, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ec != cudaSuccess) return fail(ctx, TT_E_CUDA, std::string("round capture: ") + cudaGetErrorString(ec));
+      cudaGraphExec_t ex = nullptr;
+      const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) return fail(ctx, TT_E_CUDA, std::string("round graph: ") + cudaGetErrorString(ei));
+      it = ctx->graph_cache.emplace(key, std::make_pair(ex, tt_kernel_launches() - l0)).first;
+    } else {
+      for (uint64_t q = 0; q < it->second.second; ++q) tt::note_launch();  // the replay launches them again
+    }
+    TT_CUDA(ctx, cudaGraphLaunch(it->second.first, ctx->stream));
+  }
   ctx->last_hash = hash;
   ctx->pending = true;
   ctx->last_b = cfg->b;
