@@ -442,6 +442,16 @@ __global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Sr
 // otherwise NEED_MORE (the host retries with a larger need); > 4096
 // survivors report OVERFLOW (the identity-keyed hash path takes over).
 constexpr int kFastThreads = 1024;
+
+// %globaltimer marks (ns) of the fast selector's phases, read by ttdbg_select_clocks:
+// [0] first CTA start, [1] K1 done (last CTA begins the threshold), [2] threshold done,
+// [3] compact start, [4] rank start, [5] emit start, [6] emit end
+__device__ unsigned long long g_sel_ns[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kFastE = kFastCap / kFastThreads;  // 4 keys per thread
 constexpr int kRankChunk = 128;
 
@@ -502,6 +512,41 @@ __device__ uint64_t block_radix_select(const uint32_t* keys, int n, int r, int* 
   return ((uint64_t)prefix << 32) | 0xffffffffull;
 }
 
+// Survivor threshold from the sample, in one histogram pass: the keys'
+// range [min, max] is cut into <= 4096 bins of width 2^shift (data-adaptive,
+// so equal high bytes do not pile onto one bin), and the threshold is the
+// top of the bin where the count reaches r + 1. Any threshold is correct
+// (every key <= it survives); this one keeps ~(r + 1 + bin load) samples'
+// worth of survivors. Whole CTA; every thread gets the 64-bit threshold.
+__device__ uint64_t block_sample_threshold(const uint32_t* keys, int n, int r, int* hist, int* hsum, int* wt) {
+  __shared__ uint32_t s_min, s_max;
+  __shared__ int s_bin;
+  if (threadIdx.x == 0) s_min = 0xffffffffu, s_max = 0u, s_bin = 4095;
+  __syncthreads();
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) lo = min(lo, keys[e]), hi = max(hi, keys[e]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(&s_min, lo), atomicMax(&s_max, hi);
+  for (int d = threadIdx.x; d < 4096; d += blockDim.x) hist[d] = 0;
+  __syncthreads();
+  const uint32_t kmin = s_min, span = s_max - s_min;
+  int shift = 0;
+  while ((span >> shift) >= 4096u) ++shift;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) atomicAdd(&hist[(keys[e] - kmin) >> shift], 1);
+  __syncthreads();
+  block_exclusive_scan(hist, hsum, 4096, wt);
+  for (int d = threadIdx.x; d < 4096; d += blockDim.x)
+    if (hsum[d] <= r && r < hsum[d] + hist[d]) s_bin = d;
+  __syncthreads();
+  const uint64_t top = (uint64_t)kmin + ((uint64_t)(s_bin + 1) << shift) - 1;
+  const uint32_t key32 = top > 0xffffffffull ? 0xffffffffu : (uint32_t)top;
+  return ((uint64_t)key32 << 32) | 0xffffffffull;
+}
+
 template <int NSP, int NRED, bool SEED>
 __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevice D, Src src, int64_t n,
                                                             int toggles, int64_t need, double* __restrict__ cost,
@@ -510,7 +555,8 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
                                                             int* __restrict__ invalid) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* keys = (uint32_t*)smem;  // the last CTA's copy of the sample
-  __shared__ int hist[256];
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[0] = gtimer();
+  __shared__ int hist[4096], hsum[4096], wt[32];
   // n / 256 samples, clamped to [4096, 32768]: each sample stands for <= 512
   // candidates, so the rank-r threshold keeps ~(r + 1) * stride survivors
   const int64_t want = n / 256 > kFastCap ? (n / 256 < kSampleMax ? n / 256 : kSampleMax) : kFastCap;
@@ -530,6 +576,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
     rank_acc[e] = 0, dup[e] = 0;
   if (bad) atomicOr(invalid, 1);
   if (!last_cta(st)) return;
+  if (threadIdx.x == 0) g_sel_ns[1] = gtimer();
   const int ns = (int)((n + stride - 1) / stride);
   for (int e = threadIdx.x; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
   __syncthreads();
@@ -537,8 +584,9 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
   // (then NEED_MORE and a retry with a larger need)
   int64_t r = (3 * need * ns + 2 * n - 1) / (2 * n) + 3;
   const bool all = r >= ns - 1;
-  const uint64_t thr = all ? ~0ull : block_radix_select(keys, ns, (int)r, hist);
+  const uint64_t thr = all ? ~0ull : block_sample_threshold(keys, ns, (int)r, hist, hsum, wt);
   if (threadIdx.x == 0) {
+    g_sel_ns[2] = gtimer();
     st->prefix = thr;
     st->shift = 0;
     st->all = all ? 1 : 0;
@@ -567,6 +615,7 @@ __global__ void __launch_bounds__(256) k_fsel_compact(DevSketch S, Src src, cons
                                                       uint64_t* __restrict__ sfp) {
   const uint64_t thr = st->prefix;
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[3] = gtimer();
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
     uint64_t key = 0;
@@ -613,6 +662,7 @@ __global__ void __launch_bounds__(kRankChunk) k_fsel_rank(DevSketch S, Src src, 
   __shared__ uint64_t ck[kRankChunk], cf[kRankChunk];
   __shared__ int64_t ci[kRankChunk];
   const int m = (int)min(*(volatile const uint32_t*)&st->nsurv, (uint32_t)kFastCap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[4] = gtimer();
   const int chunks = (m + kRankChunk - 1) / kRankChunk;
   for (int blk = blockIdx.x; blk < chunks * chunks; blk += gridDim.x) {
     const int ce = blk / chunks, cj = blk - ce * chunks;  // element chunk, comparison chunk
@@ -661,6 +711,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
   int* pos = flag + kFastCap;
   __shared__ int wt[32];
   const uint32_t nsurv = st->nsurv;
+  if (threadIdx.x == 0) g_sel_ns[5] = gtimer(), g_sel_ns[7] = nsurv;
   if (nsurv > (uint32_t)kFastCap) {
     if (threadIdx.x == 0) st->status |= TT_SEL_OVERFLOW, *out_count = 0;
     return;
@@ -690,6 +741,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
     st->count = cnt;
     const bool everything = st->all || (int64_t)m >= n;
     if (cnt < k && !everything) st->status |= TT_SEL_NEED_MORE;  // duplicates ate the margin
+    g_sel_ns[6] = gtimer();
   }
 }
 
@@ -1015,3 +1067,7 @@ int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, in
 }
 
 }  // namespace tt
+
+extern "C" int ttdbg_select_clocks(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 8 ? n : 8));
+}
