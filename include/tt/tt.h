@@ -148,6 +148,26 @@ int tt_gd_step(tt_ctx* ctx, double* params_dev, const double* grads_dev, int64_t
  * unless 0 <= m < 1. Async. */
 int tt_momentum_update(tt_ctx* ctx, double* phi_dev, const double* target_dev, int64_t n, double m);
 
+/* ------------------------------------------- simulated hardware (§8f #2) -- */
+/* noiseless_latency (oracle.cpp:105-111) of n schedules (SoA): draft cost
+ * under the hidden spec x stride multiplier (oracle.cpp:82-95) x occupancy
+ * multiplier (oracle.cpp:97-103) + launch overhead; bit-exact. Async. */
+int tt_oracle_latency(tt_ctx* ctx, const tt_sketch* sketch, const tt_oracle_spec* oracle, const int32_t* soa_dev,
+                      int64_t ld, int64_t n, double* latency_dev);
+/* measure (oracle.cpp:113-121) as the tuner draws it (tuner.cpp:202-203):
+ * schedule i is trial (trial0 + i) of task `task_hash` (hash_str of the
+ * task name), latency = noiseless x exp(sigma x normal()) from
+ * RngStream(derive_seed(seed, 0x6d656173, task_hash, trial0 + i)). Async. */
+int tt_oracle_measure(tt_ctx* ctx, const tt_sketch* sketch, const tt_oracle_spec* oracle, const int32_t* soa_dev,
+                      int64_t ld, int64_t n, uint64_t task_hash, uint64_t trial0, double* latency_dev,
+                      double* noiseless_dev);
+/* oracle_best (oracle.cpp:123-135): the minimal noiseless latency over the
+ * whole schedule space (enumerated by identity on the device) and the
+ * identity of a schedule attaining it (the lowest such identity).
+ * TT_E_CONFIG when the space exceeds 2^40 schedules. Synchronous. */
+int tt_oracle_best(tt_ctx* ctx, const tt_sketch* sketch, const tt_oracle_spec* oracle, uint64_t* best_identity_host,
+                   double* best_latency_host);
+
 /* ------------------------------------------------------------- round -- */
 typedef struct tt_round_config {
   int64_t n;          /* candidates drafted this round (this rank's shard) */

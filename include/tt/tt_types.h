@@ -85,6 +85,18 @@ typedef struct tt_sketch {
   int64_t unroll[TT_MAX_UNROLL];
 } tt_sketch;
 
+/* The simulated hardware of the reference (tiletune::OracleDevice,
+ * oracle.hpp:40-47): the hidden device spec plus the latency model's
+ * coefficients and the measurement noise. */
+typedef struct tt_oracle_spec {
+  tt_device_spec hidden;
+  double stride_coeff;      /* default 0.35 */
+  double occupancy_coeff;   /* default 1.5 */
+  double launch_overhead_s; /* default 2e-6 */
+  double noise_sigma;       /* default 0.03 */
+  uint64_t seed;
+} tt_oracle_spec;
+
 /* Penalty ablation switches (draft.hpp:83-86). Bit 0 = compute side
  * enabled, bit 1 = memory side enabled; TT_TOGGLES_ALL is the default. */
 #define TT_TOGGLE_COMPUTE 1

@@ -289,6 +289,40 @@ int ref_noiseless_latency(const tt_sketch* sk, const tt_device_spec* hidden, dou
   });
 }
 
+static OracleDevice to_oracle(const tt_oracle_spec& o) {
+  OracleDevice r;
+  r.hidden = to_dev(o.hidden);
+  r.stride_coeff = o.stride_coeff;
+  r.occupancy_coeff = o.occupancy_coeff;
+  r.launch_overhead_s = o.launch_overhead_s;
+  r.noise_sigma = o.noise_sigma;
+  r.seed = o.seed;
+  return r;
+}
+
+int ref_measure(const tt_sketch* sk, const tt_oracle_spec* o, const int32_t* soa, int64_t ld, int64_t n,
+                uint64_t task_hash, uint64_t trial0, double* latency, double* noiseless) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    OracleDevice od = to_oracle(*o);
+    for (int64_t i = 0; i < n; ++i) {
+      RngStream mrng(derive_seed(od.seed, 0x6d656173ULL, task_hash, trial0 + (uint64_t)i));  // tuner.cpp:202
+      Measurement m = measure(s, get_sched(*sk, soa, ld, i), od, mrng);
+      latency[i] = m.latency_s;
+      noiseless[i] = m.noiseless_latency_s;
+    }
+  });
+}
+
+int ref_oracle_best(const tt_sketch* sk, const tt_oracle_spec* o, uint64_t cap, int32_t* argmin_soa,
+                    double* latency) {
+  return guard([&] {
+    OracleBest b = oracle_best(to_sketch(*sk), to_oracle(*o), cap);
+    put_sched(*sk, b.argmin, argmin_soa, 1, 0);
+    *latency = b.latency_s;
+  });
+}
+
 int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t k, int64_t b,
               uint64_t seed, const double* params, int h, int threads, int64_t* sel_idx,
               double* sel_scores, int32_t* drafted_soa, double* drafted_cost,

@@ -45,6 +45,14 @@ int ref_noiseless_latency(const tt_sketch* sk, const tt_device_spec* hidden, dou
                           double occupancy_coeff, double launch_overhead_s, const int32_t* soa,
                           int64_t ld, int64_t n, double* out);
 
+/* measure(sketch, sched, oracle, RngStream(derive_seed(seed, "meas", task,
+ * trial0 + i))) for column i (oracle.cpp:113-121, tuner.cpp:202-203) */
+int ref_measure(const tt_sketch* sk, const tt_oracle_spec* o, const int32_t* soa, int64_t ld, int64_t n,
+                uint64_t task_hash, uint64_t trial0, double* latency, double* noiseless);
+/* oracle_best(sketch, oracle, cap) (oracle.cpp:123-135): argmin schedule (SoA, ld 1) + latency */
+int ref_oracle_best(const tt_sketch* sk, const tt_oracle_spec* o, uint64_t cap, int32_t* argmin_soa,
+                    double* latency);
+
 /* The reference-API draft+verify round of SURVEY.md §3.2, timed inside:
  * explore(n_steps=1) -> extract_features x K -> score_batch -> select_top.
  * Writes the selected b schedules' ranks into sel_idx (positions within the

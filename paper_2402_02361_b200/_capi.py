@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .types import DeviceSpec, OpSpec, Sketch
+from .types import DeviceSpec, OpSpec, OracleSpec, Sketch
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtt_b200.so")
 
@@ -64,6 +64,10 @@ _SIGS = [
     ("tt_forward_calls", C.c_uint64, []),
     ("tt_reset_forward_calls", None, []),
     ("tt_select_top", C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int64, i64p]),
+    ("tt_oracle_latency", C.c_int, [vp, P(Sketch), P(OracleSpec), vp, C.c_int64, C.c_int64, vp]),
+    ("tt_oracle_measure", C.c_int, [vp, P(Sketch), P(OracleSpec), vp, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64,
+                                    vp, vp]),
+    ("tt_oracle_best", C.c_int, [vp, P(Sketch), P(OracleSpec), u64p, f64p]),
     ("tt_gd_step", C.c_int, [vp, vp, vp, C.c_int64, C.c_double]),
     ("tt_momentum_update", C.c_int, [vp, vp, vp, C.c_int64, C.c_double]),
     ("tt_round", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64, i64p, f64p,

@@ -446,7 +446,7 @@ constexpr int kFastThreads = 1024;
 // %globaltimer marks (ns) of the fast selector's phases, read by ttdbg_select_clocks:
 // [0] first CTA start, [1] K1 done (last CTA begins the threshold), [2] threshold done,
 // [3] compact start, [4] rank start, [5] emit start, [6] emit end
-__device__ unsigned long long g_sel_ns[8];
+__device__ unsigned long long g_sel_ns[12];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -693,7 +693,9 @@ __global__ void __launch_bounds__(kRankChunk) k_fsel_rank(DevSketch S, Src src, 
   }
 }
 
-template <int NSP, int NRED, bool SEED>
+// WITH_ID: also write identities of the emitted entries (sharded rounds);
+// a separate instantiation keeps the common kernel's code small.
+template <int NSP, int NRED, bool SEED, bool WITH_ID>
 __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src, int64_t n, int64_t k,
                                                             SelState* __restrict__ st,
                                                             const uint64_t* __restrict__ skey,
@@ -719,6 +721,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
   const int m = (int)nsurv;
   for (int e = threadIdx.x; e < kFastCap; e += blockDim.x) flag[e] = 0;
   __syncthreads();
+  if (threadIdx.x == 0) g_sel_ns[8] = gtimer();
   for (int e = threadIdx.x; e < m; e += blockDim.x) {
     const int r = rank_acc[e];  // a permutation of 0..m-1: (cost, index) keys are distinct
     a[r] = skey[e];
@@ -726,13 +729,15 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
     flag[r] = dup[e] ? 0 : 1;
   }
   __syncthreads();
+  if (threadIdx.x == 0) g_sel_ns[9] = gtimer();
   const int total = block_exclusive_scan(flag, pos, kFastCap, wt);
+  if (threadIdx.x == 0) g_sel_ns[10] = gtimer();
   for (int e = threadIdx.x; e < m; e += blockDim.x) {
     if (flag[e] && pos[e] < k) {
       const int o = pos[e];
       out_idx[o] = bi[e] + src.index_base;
       out_cost[o] = key_cost(a[e]);
-      if (out_id) out_id[o] = identity_at<NSP, NRED, SEED>(S, src, bi[e]);
+      if constexpr (WITH_ID) out_id[o] = identity_at<NSP, NRED, SEED>(S, src, bi[e]);
     }
   }
   if (threadIdx.x == 0) {
@@ -763,9 +768,13 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   k_fsel_rank<NSP, NRED, SEED><<<2 * 148, kRankChunk, 0, st>>>(S, src, w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup);
   constexpr size_t emit_smem = (size_t)kFastCap * (2 * sizeof(uint64_t) + 2 * sizeof(int));
   static bool init = false;
-  if (!init) set_smem(k_fsel_emit<NSP, NRED, SEED>, emit_smem), init = true;
+  if (!init) set_smem(k_fsel_emit<NSP, NRED, SEED, true>, emit_smem), set_smem(k_fsel_emit<NSP, NRED, SEED, false>, emit_smem), init = true;
   tt::note_launch();
-  k_fsel_emit<NSP, NRED, SEED><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
+  if (out_id)
+    k_fsel_emit<NSP, NRED, SEED, true><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
+                                                          out_idx, out_cost, out_id, out_count);
+  else
+    k_fsel_emit<NSP, NRED, SEED, false><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
                                                           out_idx, out_cost, out_id, out_count);
 }
 
@@ -1069,5 +1078,5 @@ int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, in
 }  // namespace tt
 
 extern "C" int ttdbg_select_clocks(unsigned long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 8 ? n : 8));
+  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 12 ? n : 12));
 }

@@ -1076,6 +1076,75 @@ int tt_select_top(tt_ctx* ctx, const double* scores, const double* drafts, const
   return TT_OK;
 }
 
+// ---------------------------------------------------- simulated hardware --
+}  // extern "C"
+
+namespace {
+int compile_oracle(tt_ctx* ctx, const tt_oracle_spec* o, DevOracle& O) {
+  if (!o) return fail(ctx, TT_E_STATE, "null oracle spec");
+  int rc = compile_device(ctx, &o->hidden, O.hidden);
+  if (rc) return rc;
+  // validate_oracle (oracle.cpp:25-36)
+  if (o->stride_coeff < 0.0 || o->occupancy_coeff < 0.0 || o->launch_overhead_s < 0.0 || o->noise_sigma < 0.0)
+    return fail(ctx, TT_E_VALIDATE, "oracle coefficients must be non-negative");
+  O.stride_coeff = o->stride_coeff, O.occupancy_coeff = o->occupancy_coeff;
+  O.launch = o->launch_overhead_s, O.sigma = o->noise_sigma, O.seed = o->seed;
+  return TT_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int tt_oracle_latency(tt_ctx* ctx, const tt_sketch* sk, const tt_oracle_spec* o, const int32_t* soa, int64_t ld,
+                      int64_t n, double* latency) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevOracle O;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_oracle(ctx, o, O))) return rc;
+  if (launch_oracle_latency(S, O, soa, ld, n, 0, 0, 0, nullptr, latency, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_oracle_measure(tt_ctx* ctx, const tt_sketch* sk, const tt_oracle_spec* o, const int32_t* soa, int64_t ld,
+                      int64_t n, uint64_t task_hash, uint64_t trial0, double* latency, double* noiseless) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevOracle O;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_oracle(ctx, o, O))) return rc;
+  if (launch_oracle_latency(S, O, soa, ld, n, 1, task_hash, trial0, latency, noiseless, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  return TT_OK;
+}
+
+int tt_oracle_best(tt_ctx* ctx, const tt_sketch* sk, const tt_oracle_spec* o, uint64_t* best_id, double* best_lat) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevOracle O;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_oracle(ctx, o, O))) return rc;
+  if (!S.id_exact || S.space > (uint64_t{1} << 40))
+    return fail(ctx, TT_E_CONFIG, "oracle_best: schedule space exceeds 2^40");
+  // CTA winners in the selector's survivor scratch (4096 entries), result in its hash table
+  if (launch_oracle_best(S, O, ctx->sel.skey, (uint64_t*)ctx->sel.sidx, 4096, ctx->sel.tkeys, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  uint64_t out[2];
+  TT_CUDA(ctx, cudaMemcpyAsync(out, ctx->sel.tkeys, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.tkeys, 0xff, sizeof(out), ctx->stream));  // hash-table invariant
+  if ((rc = sync_check(ctx))) return rc;
+  if (best_id) *best_id = out[1];
+  if (best_lat) std::memcpy(best_lat, &out[0], sizeof(double));
+  return TT_OK;
+}
+
 int tt_gd_step(tt_ctx* ctx, double* params, const double* grads, int64_t n, double lr) {
   if (!ctx) return TT_E_STATE;
   launch_gd_step(params, grads, n, lr, ctx->stream);

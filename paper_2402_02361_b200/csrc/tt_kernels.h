@@ -106,6 +106,18 @@ int launch_pacm_tc_pack(const double* params, int h, void* packed, cudaStream_t 
 int launch_pacm_tc(const uint8_t* tiles, int n_stmt, int n_block, const int64_t* count_dev, int64_t k_max,
                    const void* packed, int h, double* score_out, cudaStream_t st);
 
+// k_oracle.cu — simulated hardware (oracle.cpp:82-135)
+struct DevOracle {
+  DevDevice hidden;
+  double stride_coeff, occupancy_coeff, launch, sigma;
+  uint64_t seed;
+};
+int launch_oracle_latency(const DevSketch& S, const DevOracle& O, const int32_t* soa, int64_t ld, int64_t n,
+                          int measure, uint64_t task, uint64_t trial0, double* latency, double* noiseless,
+                          cudaStream_t st);
+int launch_oracle_best(const DevSketch& S, const DevOracle& O, uint64_t* scratch_lat, uint64_t* scratch_id,
+                       int max_ctas, uint64_t* out2, cudaStream_t st);
+
 // k_select.cu
 int launch_select_top(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n,
                       const int64_t* n_dev, int64_t b, int64_t* out_pos, int64_t* out_count, int* status,

@@ -26,12 +26,13 @@ import torch
 
 from . import _capi
 from ._capi import TTError, RoundConfig, RoundResult, TT_PREC_BF16, TT_PREC_FP64, lib
-from .types import DeviceSpec, OpSpec, Sketch, TT_TOGGLES_ALL
+from .types import DeviceSpec, OpSpec, OracleSpec, Sketch, TT_TOGGLES_ALL
 
 __all__ = ["Context", "TTError", "TT_PREC_FP64", "TT_PREC_BF16", "random_init", "draft_cost", "draft_topk",
            "explore1", "topk_merge", "schedule_identity", "schedule_from_identity", "extract_features",
            "extract_features_soa", "PaCM", "select_top", "gd_step", "momentum_update", "draft_verify_round",
-           "init_params", "param_count", "generate_sketch", "forward_calls", "reset_forward_calls"]
+           "init_params", "param_count", "generate_sketch", "forward_calls", "reset_forward_calls",
+           "oracle_latency", "oracle_measure", "oracle_best"]
 
 
 def _p(t: torch.Tensor | None):
@@ -268,6 +269,31 @@ def select_top(ctx: Context, scores: torch.Tensor, drafts: torch.Tensor, exclude
     ex = None if excluded is None else excluded.to(torch.uint8).contiguous()
     ctx.check(lib().tt_select_top(ctx.h, _p(scores), _p(drafts), _p(ex), scores.shape[0], b, out))
     return np.frombuffer(out, dtype=np.int64).copy()
+
+
+def oracle_latency(ctx: Context, sketch: Sketch, oracle: OracleSpec, soa: torch.Tensor) -> torch.Tensor:
+    """noiseless_latency (oracle.cpp:105-111) per schedule, bit-exact fp64."""
+    n = soa.shape[1]
+    out = ctx.empty((n,), torch.float64)
+    ctx.check(lib().tt_oracle_latency(ctx.h, C.byref(sketch), C.byref(oracle), _p(soa), soa.stride(0), n, _p(out)))
+    return out
+
+
+def oracle_measure(ctx: Context, sketch: Sketch, oracle: OracleSpec, soa: torch.Tensor, task_hash: int, trial0: int):
+    """measure (oracle.cpp:113-121) with the tuner's per-trial streams
+    (tuner.cpp:202-203): schedule i is trial trial0 + i. Returns (latency, noiseless)."""
+    n = soa.shape[1]
+    lat, nl = ctx.empty((n,), torch.float64), ctx.empty((n,), torch.float64)
+    ctx.check(lib().tt_oracle_measure(ctx.h, C.byref(sketch), C.byref(oracle), _p(soa), soa.stride(0), n,
+                                      task_hash & (2**64 - 1), trial0, _p(lat), _p(nl)))
+    return lat, nl
+
+
+def oracle_best(ctx: Context, sketch: Sketch, oracle: OracleSpec):
+    """oracle_best (oracle.cpp:123-135): (identity of a minimiser, minimal noiseless latency)."""
+    ident, lat = C.c_uint64(0), C.c_double(0)
+    ctx.check(lib().tt_oracle_best(ctx.h, C.byref(sketch), C.byref(oracle), C.byref(ident), C.byref(lat)))
+    return int(ident.value), float(lat.value)
 
 
 def gd_step(ctx: Context, params: torch.Tensor, grads: torch.Tensor, lr: float):

@@ -26,6 +26,13 @@ class DeviceSpec(C.Structure):
                 ("t_p", C.c_double), ("t_m", C.c_double), ("element_bytes", C.c_int64)]
 
 
+class OracleSpec(C.Structure):
+    """tiletune::OracleDevice (oracle.hpp:40-47)."""
+
+    _fields_ = [("hidden", DeviceSpec), ("stride_coeff", C.c_double), ("occupancy_coeff", C.c_double),
+                ("launch_overhead_s", C.c_double), ("noise_sigma", C.c_double), ("seed", C.c_uint64)]
+
+
 class BufferSpec(C.Structure):
     _fields_ = [("io", C.c_int32), ("n_axes", C.c_int32), ("axes", C.c_int32 * TT_MAX_AXES)]
 
@@ -120,6 +127,24 @@ def make_sketch(op: OpSpec, unroll=(1, 4, 16)) -> Sketch:
 def reference_device() -> DeviceSpec:
     """proj/samples/device.txt == test_helpers.hpp:16-28."""
     return DeviceSpec(256, 4096, 4, 32, 8, 32, 1.0e12, 1.0e11, 4)
+
+
+def oracle_a() -> "OracleSpec":
+    """test_helpers.hpp:30-45 == proj/samples/oracle_a.txt."""
+    return OracleSpec(DeviceSpec(192, 3072, 4, 32, 6, 16, 8.0e11, 1.2e11, 4), 0.35, 1.5, 2.0e-6, 0.03, 90001)
+
+
+def oracle_b() -> "OracleSpec":
+    """test_helpers.hpp:47-64 == proj/samples/oracle_b.txt."""
+    return OracleSpec(DeviceSpec(128, 6144, 2, 64, 12, 64, 1.5e12, 0.9e11, 4), 0.5, 2.0, 1.0e-6, 0.03, 90002)
+
+
+def hash_str(s: str) -> int:
+    """FNV-1a (common.hpp:74-82)."""
+    h = 1469598103934665603
+    for ch in s.encode():
+        h = ((h ^ ch) * 1099511628211) & M64
+    return h
 
 
 def oracle_b_hidden() -> DeviceSpec:

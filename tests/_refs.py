@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-from paper_2402_02361_b200.types import DeviceSpec, Sketch
+from paper_2402_02361_b200.types import DeviceSpec, OracleSpec, Sketch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "libtt_oracle.so")
@@ -79,6 +79,9 @@ def ref():
             "ref_momentum_update": (C.c_int, [f64p, f64p, C.c_int, C.c_double]),
             "ref_train": (C.c_int, [f64p, C.c_int, C.c_int, C.c_int, f64p, f64p, f64p, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_uint64, f64p, f64p]),
             "ref_noiseless_latency": (C.c_int, [sk, dv, C.c_double, C.c_double, C.c_double, i32p, C.c_int64, C.c_int64, f64p]),
+            "ref_measure": (C.c_int, [sk, P(OracleSpec), i32p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, f64p,
+                                      f64p]),
+            "ref_oracle_best": (C.c_int, [sk, P(OracleSpec), C.c_uint64, i32p, f64p]),
             "ref_round": (C.c_int, [sk, dv, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, f64p, C.c_int, C.c_int, i64p, f64p, i32p, f64p, i64p, f64p]),
         }
         for name, (res, args) in sig.items():
@@ -218,3 +221,19 @@ def R_select_top(scores, drafts, excluded, b):
     ex = None if excluded is None else np.ascontiguousarray(excluded, np.uint8)
     check(ref().ref_select_top(ptr(scores, f64p), ptr(drafts, f64p), ptr(ex, u8p), len(scores), b, ptr(out, i64p)))
     return out
+
+
+def R_measure(sk, oracle, soa, task_hash, trial0):
+    soa = np.ascontiguousarray(soa)
+    n = soa.shape[1]
+    lat, nl = np.zeros(n), np.zeros(n)
+    check(ref().ref_measure(C.byref(sk), C.byref(oracle), ptr(soa, i32p), n, n, task_hash, trial0, ptr(lat, f64p),
+                            ptr(nl, f64p)))
+    return lat, nl
+
+
+def R_oracle_best(sk, oracle, cap=1 << 30):
+    soa = np.zeros((sk.cols, 1), np.int32)
+    lat = C.c_double(0)
+    check(ref().ref_oracle_best(C.byref(sk), C.byref(oracle), cap, ptr(soa, i32p), C.byref(lat)))
+    return soa, lat.value
