@@ -2,7 +2,9 @@
 // compilation (tt_sketch -> DevSketch) and the round orchestration.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1142,6 +1144,160 @@ int tt_oracle_best(tt_ctx* ctx, const tt_sketch* sk, const tt_oracle_spec* o, ui
   if ((rc = sync_check(ctx))) return rc;
   if (best_id) *best_id = out[1];
   if (best_lat) std::memcpy(best_lat, &out[0], sizeof(double));
+  return TT_OK;
+}
+
+// ------------------------------------------------------------- training --
+}  // extern "C"
+
+namespace {
+
+// RngStream (common.hpp:87-119) on the host: the batch sampling of train()
+struct HostRng {
+  uint64_t s;
+  explicit HostRng(uint64_t seed) : s(seed ? seed : kGolden) {}
+  uint64_t next() {
+    s += kGolden;
+    return scramble64(s);
+  }
+  uint64_t index(uint64_t n) { return (uint64_t)(((unsigned __int128)next() * n) >> 64); }
+};
+
+uint64_t mix64_h(uint64_t x) { return scramble64(x + kGolden); }
+uint64_t derive_seed_h(uint64_t base, uint64_t a) { return mix64_h(base ^ mix64_h(a)); }
+
+double softplus_h(double x) { return x > 30.0 ? x : std::log1p(std::exp(x)); }
+double sigmoid_h(double x) {
+  if (x >= 0) {
+    const double e = std::exp(-x);
+    return 1.0 / (1.0 + e);
+  }
+  const double e = std::exp(x);
+  return e / (1.0 + e);
+}
+double log2_h(double x) { return std::log(x) * 1.4426950408889634074; }
+
+// LambdaRank loss and its score gradient (ranker.cpp:394-441): pairs (i, j)
+// with i strictly faster, weighted by |Δgain| |Δdiscount| / max DCG under
+// the current score ranking (descending, ties by index).
+int lambda_rank_h(tt_ctx* ctx, const std::vector<double>& sc, const std::vector<double>& lat, double* loss,
+                  std::vector<double>* grad) {
+  const size_t n = sc.size();
+  if (n != lat.size()) return fail(ctx, TT_E_STATE, "rank loss: length mismatch");
+  if (n < 2) return fail(ctx, TT_E_STATE, "rank loss: need at least two items");
+  double min_lat = lat[0];
+  for (double l : lat) {
+    if (!(l > 0.0)) return fail(ctx, TT_E_STATE, "rank loss: latencies must be positive");
+    min_lat = l < min_lat ? l : min_lat;
+  }
+  std::vector<double> gain(n), discount(n);
+  for (size_t i = 0; i < n; ++i) gain[i] = std::exp2(min_lat / lat[i]) - 1.0;
+  std::vector<size_t> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return sc[a] != sc[b] ? sc[a] > sc[b] : a < b; });
+  for (size_t pos = 0; pos < n; ++pos) discount[order[pos]] = 1.0 / log2_h((double)pos + 2.0);
+  std::vector<double> ideal = gain;
+  std::sort(ideal.begin(), ideal.end(), [](double a, double b) { return a > b; });
+  double max_dcg = 0.0;
+  for (size_t pos = 0; pos < n; ++pos) max_dcg += ideal[pos] / log2_h((double)pos + 2.0);
+  double L = 0.0;
+  if (grad) grad->assign(n, 0.0);
+  for (size_t i = 0; i < n; ++i)
+    for (size_t j = 0; j < n; ++j) {
+      if (!(lat[i] < lat[j])) continue;
+      const double w = std::fabs(gain[i] - gain[j]) * std::fabs(discount[i] - discount[j]) / max_dcg;
+      if (w == 0.0) continue;
+      const double d = sc[i] - sc[j];
+      L += w * softplus_h(-d);
+      if (grad) {
+        const double slope = w * sigmoid_h(-d);
+        (*grad)[i] -= slope;
+        (*grad)[j] += slope;
+      }
+    }
+  *loss = L;
+  return TT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tt_pacm_train(tt_ctx* ctx, double* params, int h, const double* stmt, const double* block, int n_stmt,
+                  int n_block, const double* latencies, int64_t n, int epochs, double lr, int batch, uint64_t seed,
+                  int attention_identity, double* initial_loss, double* final_loss) {
+  if (!ctx) return TT_E_STATE;
+  if (n < 2) return fail(ctx, TT_E_STATE, "train: dataset needs at least two labeled schedules");
+  if (epochs < 0) return fail(ctx, TT_E_STATE, "train: epochs must be >= 0");
+  if (h < 1 || n_stmt < 1 || n_block < 1 || n_stmt > 14 || n_block > 20)
+    return fail(ctx, TT_E_STATE, "train: unsupported model / feature geometry");
+  const size_t slot = train_slot_doubles(n_stmt, n_block, h);
+  const int64_t np = tt_param_count(h);
+  const int ctas = 8 * 148;
+  const int64_t mmax = n;  // every record is scored for the dataset loss
+  double *slots = nullptr, *work = nullptr, *grads = nullptr, *dscore = nullptr, *scores = nullptr;
+  int32_t* list = nullptr;
+  auto release = [&]() {
+    cudaFree(slots), cudaFree(work), cudaFree(grads), cudaFree(dscore), cudaFree(scores), cudaFree(list);
+  };
+  if (cudaMalloc((void**)&slots, sizeof(double) * slot * mmax) != cudaSuccess ||
+      cudaMalloc((void**)&work, sizeof(double) * train_work_doubles(n_stmt, n_block, h, ctas)) != cudaSuccess ||
+      cudaMalloc((void**)&grads, sizeof(double) * np) != cudaSuccess ||
+      cudaMalloc((void**)&dscore, sizeof(double) * mmax) != cudaSuccess ||
+      cudaMalloc((void**)&scores, sizeof(double) * mmax) != cudaSuccess ||
+      cudaMalloc((void**)&list, sizeof(int32_t) * mmax) != cudaSuccess) {
+    release();
+    return fail(ctx, TT_E_CUDA, "train: allocation failed");
+  }
+  std::vector<double> lat(latencies, latencies + n), sc(n), lt;
+  auto dataset_loss = [&](double* out) -> int {  // ranker.cpp:445-455
+    launch_train_fwd(stmt, block, n_stmt, n_block, nullptr, (int)n, params, h, attention_identity, slots, scores,
+                     ctx->stream);
+    TT_LAUNCHED(ctx);
+    TT_CUDA(ctx, cudaMemcpyAsync(sc.data(), scores, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return lambda_rank_h(ctx, sc, lat, out, nullptr);
+  };
+  int rc = TT_OK;
+  double l0 = 0.0, l1 = 0.0;
+  if ((rc = dataset_loss(&l0))) {
+    release();
+    return rc;
+  }
+  HostRng rng(derive_seed_h(seed, 0x7261696eULL));
+  std::vector<int32_t> idx(n);
+  std::vector<double> bs, bl, g;
+  for (int epoch = 0; epoch < epochs && !rc; ++epoch) {
+    for (int64_t i = 0; i < n; ++i) idx[i] = (int32_t)i;
+    int64_t take = n;
+    if (batch > 0 && batch < n) {  // partial Fisher-Yates (ranker.cpp:478-486)
+      take = batch;
+      for (int64_t i = 0; i < take; ++i) std::swap(idx[i], idx[i + (int64_t)rng.index((uint64_t)(n - i))]);
+    }
+    TT_CUDA(ctx, cudaMemcpyAsync(list, idx.data(), sizeof(int32_t) * take, cudaMemcpyHostToDevice, ctx->stream));
+    launch_train_fwd(stmt, block, n_stmt, n_block, list, (int)take, params, h, attention_identity, slots, scores,
+                     ctx->stream);
+    TT_LAUNCHED(ctx);
+    bs.resize(take), bl.resize(take);
+    TT_CUDA(ctx, cudaMemcpyAsync(bs.data(), scores, sizeof(double) * take, cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < take; ++i) bl[i] = lat[idx[i]];
+    double el = 0.0;
+    if ((rc = lambda_rank_h(ctx, bs, bl, &el, &g))) break;
+    if (lr == 0.0) continue;
+    TT_CUDA(ctx, cudaMemcpyAsync(dscore, g.data(), sizeof(double) * take, cudaMemcpyHostToDevice, ctx->stream));
+    launch_train_bwd(n_stmt, n_block, (int)take, params, h, attention_identity, dscore, slots, work, ctas,
+                     ctx->stream);
+    launch_train_accum(n_stmt, n_block, (int)take, h, attention_identity, slots, grads, ctx->stream);
+    launch_gd_step(params, grads, np, lr, ctx->stream);  // p -= lr * g (ranker.cpp:502-506)
+    TT_LAUNCHED(ctx);
+    TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // g / bs host buffers reused next epoch
+  }
+  if (!rc) rc = dataset_loss(&l1);
+  release();
+  if (rc) return rc;
+  if (initial_loss) *initial_loss = l0;
+  if (final_loss) *final_loss = l1;
   return TT_OK;
 }
 

@@ -118,6 +118,16 @@ int launch_oracle_latency(const DevSketch& S, const DevOracle& O, const int32_t*
 int launch_oracle_best(const DevSketch& S, const DevOracle& O, uint64_t* scratch_lat, uint64_t* scratch_id,
                        int max_ctas, uint64_t* out2, cudaStream_t st);
 
+// k_train.cu — PaCM training (score_backward + ordered gradient sums)
+size_t train_slot_doubles(int S, int B, int h);
+size_t train_work_doubles(int S, int B, int h, int ctas);
+int launch_train_fwd(const double* stmt, const double* block, int S, int B, const int32_t* list, int m,
+                     const double* params, int h, int identity, double* slots, double* scores, cudaStream_t st);
+int launch_train_bwd(int S, int B, int m, const double* params, int h, int identity, const double* dscore,
+                     double* slots, double* work, int ctas, cudaStream_t st);
+int launch_train_accum(int S, int B, int m, int h, int identity, const double* slots, double* grads,
+                       cudaStream_t st);
+
 // k_select.cu
 int launch_select_top(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n,
                       const int64_t* n_dev, int64_t b, int64_t* out_pos, int64_t* out_count, int* status,

@@ -32,7 +32,7 @@ __all__ = ["Context", "TTError", "TT_PREC_FP64", "TT_PREC_BF16", "random_init", 
            "explore1", "topk_merge", "schedule_identity", "schedule_from_identity", "extract_features",
            "extract_features_soa", "PaCM", "select_top", "gd_step", "momentum_update", "draft_verify_round",
            "init_params", "param_count", "generate_sketch", "forward_calls", "reset_forward_calls",
-           "oracle_latency", "oracle_measure", "oracle_best"]
+           "oracle_latency", "oracle_measure", "oracle_best", "train", "momentum_adapt"]
 
 
 def _p(t: torch.Tensor | None):
@@ -294,6 +294,32 @@ def oracle_best(ctx: Context, sketch: Sketch, oracle: OracleSpec):
     ident, lat = C.c_uint64(0), C.c_double(0)
     ctx.check(lib().tt_oracle_best(ctx.h, C.byref(sketch), C.byref(oracle), C.byref(ident), C.byref(lat)))
     return int(ident.value), float(lat.value)
+
+
+def train(ctx: Context, params: torch.Tensor, h: int, stmt: torch.Tensor, block: torch.Tensor, latencies,
+          epochs: int = 8, lr: float = 1e-2, batch: int = 256, seed: int = 0, attention_identity: bool = False):
+    """train(params, {one task}, cfg) (ranker.cpp:459-512) on the device, in
+    place on `params` (flattened RankerParams, fp64 CUDA tensor). Returns
+    (initial_loss, final_loss)."""
+    if params.dtype != torch.float64 or not params.is_cuda or params.numel() != param_count(h):
+        raise TTError("E_STATE", f"params must be {param_count(h)} fp64 values on the GPU")
+    stmt, block = stmt.contiguous(), block.contiguous()
+    lat = np.ascontiguousarray(np.asarray(latencies, np.float64))
+    l0, l1 = C.c_double(0), C.c_double(0)
+    ctx.check(lib().tt_pacm_train(ctx.h, _p(params), h, _p(stmt), _p(block), stmt.shape[1], block.shape[1],
+                                  lat.ctypes.data_as(C.POINTER(C.c_double)), stmt.shape[0], epochs, float(lr), batch,
+                                  seed & (2**64 - 1), int(attention_identity), C.byref(l0), C.byref(l1)))
+    return l0.value, l1.value
+
+
+def momentum_adapt(ctx: Context, phi: torch.Tensor, m: float, h: int, stmt: torch.Tensor, block: torch.Tensor,
+                   latencies, **cfg):
+    """momentum_adapt (momentum.cpp:48-56): target = phi, train(target),
+    phi <- target + m (phi - target). Returns (target, (initial, final) loss)."""
+    target = phi.clone()
+    report = train(ctx, target, h, stmt, block, latencies, **cfg)
+    momentum_update(ctx, phi, target, m)
+    return target, report
 
 
 def gd_step(ctx: Context, params: torch.Tensor, grads: torch.Tensor, lr: float):
