@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <map>
+#include <set>
 #include <vector>
 
 #include "../../include/tt/tt.h"
@@ -75,6 +76,7 @@ struct tt_ctx {
   // cleared whenever scratch is reallocated
   bool graphs = true;
   std::map<std::string, std::pair<cudaGraphExec_t, uint64_t>> graph_cache;  // exec, kernel launches
+  std::set<std::string> graph_seen;  // argument sets run once eagerly: captured on their second use
   // stage profiling with CUDA events on the ctx stream
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -318,6 +320,7 @@ int compile_device(tt_ctx* ctx, const tt_device_spec* d, DevDevice& D) {
 void graphs_clear(tt_ctx* ctx) {
   for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.first);
   ctx->graph_cache.clear();
+  ctx->graph_seen.clear();
 }
 
 template <typename T>
@@ -894,7 +897,13 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
     put(sk, sizeof(*sk)), put(dev, sizeof(*dev)), put(cfg, sizeof(*cfg)), put(&soa, sizeof(soa)), put(&ld, 8);
     put(&seed, 8), put(&need, 8), put(&hash, 1), put(&ctx->h, sizeof(ctx->h));
     auto it = ctx->graph_cache.find(key);
-    if (it == ctx->graph_cache.end()) {
+    // capturing costs ~1 ms: a round whose arguments never repeat (a fresh
+    // seed every tuner round) runs eagerly; repeats are captured and replayed
+    if (ctx->graph_seen.size() > 4096) ctx->graph_seen.clear();  // bounded memory over long tuning runs
+    const bool repeat = it != ctx->graph_cache.end() || !ctx->graph_seen.insert(key).second;
+    if (!repeat) {
+      if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash))) return rc;
+    } else if (it == ctx->graph_cache.end()) {
       cudaStream_t launch = ctx->stream;
       const uint64_t l0 = tt_kernel_launches();
       TT_CUDA(ctx, cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeRelaxed));
@@ -916,7 +925,7 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
     } else {
       for (uint64_t q = 0; q < it->second.second; ++q) tt::note_launch();  // the replay launches them again
     }
-    TT_CUDA(ctx, cudaGraphLaunch(it->second.first, ctx->stream));
+    if (repeat) TT_CUDA(ctx, cudaGraphLaunch(it->second.first, ctx->stream));
   }
   ctx->last_hash = hash;
   ctx->pending = true;
