@@ -58,6 +58,10 @@ class Context:
             # pass cudaStreamLegacy (0x1) explicitly (NULL means "ctx stream")
             self.check(lib().tt_ctx_set_stream(self.h, C.c_void_p(s.cuda_stream or 1)))
 
+    def stream_handle(self) -> int:
+        """The raw cudaStream_t this context enqueues on."""
+        return int(lib().tt_ctx_stream(self.h) or 0)
+
     def check(self, rc: int):
         if rc != 0:
             raise TTError(lib().tt_status_code(rc).decode(), lib().tt_last_error(self.h).decode())
