@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
                                                             uint32_t* __restrict__ sample, SelState* __restrict__ st,
                                                             int* __restrict__ rank_acc, int* __restrict__ dup,
                                                             int* __restrict__ invalid) {
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* keys = (uint32_t*)smem;  // the last CTA's copy of the sample
   if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[0] = gtimer();
@@ -613,6 +614,8 @@ __global__ void __launch_bounds__(256) k_fsel_compact(DevSketch S, Src src, cons
                                                       int64_t n, SelState* __restrict__ st,
                                                       uint64_t* __restrict__ skey, int64_t* __restrict__ sidx,
                                                       uint64_t* __restrict__ sfp) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t thr = st->prefix;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[3] = gtimer();
@@ -659,6 +662,8 @@ __global__ void __launch_bounds__(kRankChunk) k_fsel_rank(DevSketch S, Src src, 
                                                           const int64_t* __restrict__ sidx,
                                                           const uint64_t* __restrict__ sfp,
                                                           int* __restrict__ rank_acc, int* __restrict__ dup) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint64_t ck[kRankChunk], cf[kRankChunk];
   __shared__ int64_t ci[kRankChunk];
   const int m = (int)min(*(volatile const uint32_t*)&st->nsurv, (uint32_t)kFastCap);
@@ -706,6 +711,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
                                                             double* __restrict__ out_cost,
                                                             uint64_t* __restrict__ out_id,
                                                             int64_t* __restrict__ out_count) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* a = (uint64_t*)smem;
   int64_t* bi = (int64_t*)(a + kFastCap);
@@ -762,19 +768,20 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
                                                           w.rank, w.dup, w.invalid);
   if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
   tt::note_launch();
-  k_fsel_compact<NSP, NRED, SEED><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(S, src, w.cost, n, w.state, w.skey,
-                                                                             w.sidx, w.sfp);
+  launch_pdl(k_fsel_compact<NSP, NRED, SEED>, dim3(grid_for(n, 256, 148 * 4)), dim3(256), 0, st, S, src, w.cost, n,
+             w.state, w.skey, w.sidx, w.sfp);
   tt::note_launch();
-  k_fsel_rank<NSP, NRED, SEED><<<2 * 148, kRankChunk, 0, st>>>(S, src, w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup);
+  launch_pdl(k_fsel_rank<NSP, NRED, SEED>, dim3(2 * 148), dim3(kRankChunk), 0, st, S, src, w.state, w.skey, w.sidx,
+             w.sfp, w.rank, w.dup);
   constexpr size_t emit_smem = (size_t)kFastCap * (2 * sizeof(uint64_t) + 2 * sizeof(int));
   static bool init = false;
   if (!init) set_smem(k_fsel_emit<NSP, NRED, SEED, true>, emit_smem), set_smem(k_fsel_emit<NSP, NRED, SEED, false>, emit_smem), init = true;
   tt::note_launch();
   if (out_id)
-    k_fsel_emit<NSP, NRED, SEED, true><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
+    launch_pdl(k_fsel_emit<NSP, NRED, SEED, true>, dim3(1), dim3(kFastThreads), emit_smem, st, S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
                                                           out_idx, out_cost, out_id, out_count);
   else
-    k_fsel_emit<NSP, NRED, SEED, false><<<1, kFastThreads, emit_smem, st>>>(S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
+    launch_pdl(k_fsel_emit<NSP, NRED, SEED, false>, dim3(1), dim3(kFastThreads), emit_smem, st, S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
                                                           out_idx, out_cost, out_id, out_count);
 }
 

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kFeatThreads) k_feat_rows(DevSketch S, DevDevi
                                                             const int* __restrict__ sublist_count,
                                                             double* __restrict__ stmt, double* __restrict__ block,
                                                             uint8_t* __restrict__ tiles) {
+  pdl_trigger();
   __shared__ CandInfo<NSP, NRED> ci[CPP];
   __shared__ int64_t cpos[CPP];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;

@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
                                                      const int* __restrict__ sublist_count,
                                                      const double* __restrict__ params, int h, int identity,
                                                      double* __restrict__ score_out) {
+  pdl_wait();  // feature rows come from the preceding kernel
   extern __shared__ __align__(128) double sm64[];
   __shared__ __align__(8) uint64_t bars[2];
   const int S = n_stmt, B = n_block, t = threadIdx.x;
@@ -355,8 +356,8 @@ int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_blo
   auto go = [&](auto kern, int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     tt::note_launch();
-    kern<<<grid, G * threads, sm, st>>>(stmt, block, n_stmt, n_block, count_dev, k_max, sublist, sublist_count,
-                                        params, h, attention_identity, score_out);
+    launch_pdl(kern, dim3(grid), dim3(G * threads), sm, st, stmt, block, n_stmt, n_block, count_dev, k_max, sublist,
+               sublist_count, params, h, attention_identity, score_out);
   };
   // whole drafted sets: 4 chains per thread, 128 threads per candidate (throughput);
   // certification sublists: 2 chains per thread, 256 threads per candidate (latency)

@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
                                                             int n_block, const int64_t* __restrict__ count_dev,
                                                             int64_t k_max, const uint8_t* __restrict__ pack,
                                                             double* __restrict__ score_out) {
+  pdl_wait();  // the feature tile image comes from the preceding kernel
   extern __shared__ __align__(1024) uint8_t sm[];
   const int t = threadIdx.x, warp = t >> 5;
   const int64_t count = count_dev ? (*count_dev < k_max ? *count_dev : k_max) : k_max;
@@ -388,8 +389,8 @@ int launch_pacm_tc(const uint8_t* tiles, int n_stmt, int n_block, const int64_t*
   const int64_t ntiles = (k_max + kTcCand - 1) / kTcCand;
   const unsigned grid = (unsigned)(ntiles < 148 ? ntiles : 148);
   tt::note_launch();
-  k_pacm_tc<<<grid, kTcThreads, kSmTotal, st>>>(tiles, n_stmt, n_block, count_dev, k_max, (const uint8_t*)packed,
-                                                score_out);
+  launch_pdl(k_pacm_tc, dim3(grid), dim3(kTcThreads), kSmTotal, st, tiles, n_stmt, n_block, count_dev, k_max,
+             (const uint8_t*)packed, score_out);
   return 0;
 }
 

@@ -13,6 +13,27 @@ namespace tt {
 // Kernel launches issued by this library (tt_kernel_launches()).
 void note_launch();
 
+// Programmatic dependent launch. A kernel launched with launch_pdl may be
+// scheduled while its predecessor on the stream is still running; it must
+// call pdl_wait() before touching anything the predecessor reads or writes
+// (griddepcontrol.wait returns once the predecessor grid has completed and
+// its memory is visible). Kernels call pdl_trigger() early so their
+// dependents' launch overlaps their tail. Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = st;
+  cfg.attrs = &attr, cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr int64_t kSmallSelectMax = 1024;
 
 enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2 };
