@@ -746,6 +746,7 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
       if constexpr (WITH_ID) out_id[o] = identity_at<NSP, NRED, SEED>(S, src, bi[e]);
     }
   }
+  if (threadIdx.x == 0) g_sel_ns[11] = gtimer();
   if (threadIdx.x == 0) {
     const int64_t cnt = total < k ? total : k;
     *out_count = cnt;
