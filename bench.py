@@ -6,16 +6,21 @@
 Workload (BASELINE.json configs[1], the metric's 1-GPU configuration): the
 seven ResNet-50 conv2d subgraphs, 65,536 random candidates per subgraph
 round per GPU -> SA draft -> dedup top-512 -> PaCM verify (h = 64,
-random-init weights) -> select b = 10. One step = one round on each of the
-seven subgraphs. For N > 1 every rank drafts its own 65,536 candidates of
+random-init weights) -> select b = 10. PaCM runs on the tcgen05 tensor cores
+(bf16 operands, fp32 TMEM accumulators) with certified selection: the
+boundary band is rescored in fp64, so the selected set equals the
+reference's (`--precision fp64` runs the all-fp64 parity mode; the other
+precision is reported under `other_precision`). One step = one round on each
+of the seven subgraphs. For N > 1 every rank drafts its own 65,536 candidates of
 the same counter-based population (weak scaling); the per-rank top-512
 lists (cost, global index, identity) are merged after one NCCL all-gather
 and verified on every rank.
 
 value: candidates scored / s with the population already resident in HBM.
-e2e:   the same through the public API from host memory: every round copies
-       its population (int32 SoA) and the PaCM weights host->device from
-       pinned memory and reads the selection back.
+e2e:   the same through the public API from host memory: every round
+       uploads its candidates (64-bit schedule identities, decoded on the
+       device) from pinned memory, the PaCM weights once per step, and reads
+       the selection back.
 Only rank 0 prints the JSON line. `--impl reference` times the unmodified
 reference (oracle/_ref, compiled from /root/reference) on the host cores.
 """
@@ -469,7 +474,7 @@ def main():
     ap.add_argument("--k", type=int, default=512)
     ap.add_argument("--b", type=int, default=10)
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "bf16"])
+    ap.add_argument("--precision", default="bf16", choices=["fp64", "bf16"])
     ap.add_argument("--band", type=float, default=0.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rounds-per-step", type=int, default=1)
