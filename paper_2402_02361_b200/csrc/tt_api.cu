@@ -24,6 +24,8 @@ struct tt_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // identities of the drafted set, overlapped with verify
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_done = nullptr;  // recorded after a round's record copy: collect waits on it, not the stream
+  int* h_invalid = nullptr;       // pinned copy of the selector's validate_schedule flag
   std::string err;
   SelScratch sel;
   // drafted set of the current round
@@ -471,6 +473,9 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking))) return TT_E_CUDA;
   if (bad(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming))) return TT_E_CUDA;
   if (bad(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming))) return TT_E_CUDA;
+  if (bad(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming))) return TT_E_CUDA;
+  if (bad(cudaMallocHost((void**)&c->h_invalid, sizeof(int)))) return TT_E_CUDA;
+  *c->h_invalid = 0;
   c->stream = c->own;
   if (const char* g = getenv("TT_GRAPHS")) c->graphs = g[0] != '0';
   if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
@@ -518,6 +523,8 @@ void tt_ctx_destroy(tt_ctx* c) {
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->h_invalid) cudaFreeHost(c->h_invalid);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -839,6 +846,7 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
   TT_LAUNCHED(ctx);
   TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_record, ctx->d_record, sizeof(int64_t) * (4 + 4 * cfg->b),
                                cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   return TT_OK;
 }
 
@@ -927,6 +935,8 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
     }
     if (repeat) TT_CUDA(ctx, cudaGraphLaunch(it->second.first, ctx->stream));
   }
+  // outside any capture: marks the end of this round for round_collect
+  TT_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   ctx->last_hash = hash;
   ctx->pending = true;
   ctx->last_b = cfg->b;
@@ -944,7 +954,14 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
 int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* sel_cost, uint64_t* sel_id,
                   tt_round_result* res, bool allow_retry) {
   if (!ctx->pending) return fail(ctx, TT_E_STATE, "round: nothing enqueued");
-  int rc = sync_check(ctx);
+  // wait for this round only (the stream may already hold the caller's next work)
+  int rc = TT_OK;
+  {
+    const cudaError_t e1 = cudaEventSynchronize(ctx->ev_done);
+    const cudaError_t e2 = cudaGetLastError();
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+      rc = fail(ctx, TT_E_CUDA, std::string("round: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  }
   ctx->pending = false;
   if (rc) return rc;
   const int64_t b = ctx->last_b;
@@ -979,11 +996,8 @@ int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* se
   const int sel_status = status & 0xff;
   if (sel_status & TT_SEL_OVERFLOW)
     return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
-  if (ctx->last_soa) {
-    int invalid = 0;
-    TT_CUDA(ctx, cudaMemcpy(&invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost));
-    if (invalid) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
-  }
+  if (ctx->last_soa && *ctx->h_invalid)
+    return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
   const int64_t selected = rec[0];
   const int64_t* ix = rec + 4;
   const double* sc = (const double*)(ix + b);
@@ -1393,6 +1407,7 @@ int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sk, const tt_devi
   TT_LAUNCHED(ctx);
   CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
   if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  TT_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   ctx->pending = true;
   ctx->last_b = cfg->b;
   ctx->last_k = cfg->k;
