@@ -1052,26 +1052,6 @@ int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, 
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
 }
 
-// Identities of the b selected candidates, written into the round record
-// (positions pos[e] of the drafted index list idx).
-template <int NSP, int NRED, bool SEED>
-__global__ void k_selected_identity(DevSketch S, Src src, const int64_t* __restrict__ pos,
-                                    const int64_t* __restrict__ pos_count, const int64_t* __restrict__ idx, int64_t b,
-                                    uint64_t* __restrict__ out) {
-  const int64_t cnt = *pos_count;
-  for (int64_t e = threadIdx.x; e < b; e += blockDim.x)
-    out[e] = e < cnt ? identity_at<NSP, NRED, SEED>(S, src, idx[pos[e]] - src.index_base) : 0;
-}
-
-int launch_selected_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
-                             bool seeded, const int64_t* pos, const int64_t* pos_count, const int64_t* idx, int64_t b,
-                             uint64_t* out, cudaStream_t st) {
-  Src src{soa, ld, s0, first, first};
-  if (seeded)
-    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_selected_identity<NSP, NRED, true><<<1, 32, 0, st>>>(S, src, pos, pos_count, idx, b, out)));
-  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_selected_identity<NSP, NRED, false><<<1, 32, 0, st>>>(S, src, pos, pos_count, idx, b, out)));
-}
-
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st) {
   if (m > kSurvivorCap) return -1;

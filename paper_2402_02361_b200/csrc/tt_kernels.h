@@ -91,10 +91,6 @@ int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, in
 int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
                             bool seeded, const int64_t* idx, const int64_t* count_dev, int64_t k_max, uint64_t* out,
                             cudaStream_t st);
-int launch_selected_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
-                             bool seeded, const int64_t* pos, const int64_t* pos_count, const int64_t* idx, int64_t b,
-                             uint64_t* out, cudaStream_t st);
-
 // How a kernel finds drafted candidate `pos`. Candidates are addressed by identity (population-independent) or by
 // (soa, ld, local index). `list`/`count` optionally restrict scoring to a
 // device-side sublist of positions (count read on device).
