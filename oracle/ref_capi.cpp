@@ -323,6 +323,47 @@ int ref_oracle_best(const tt_sketch* sk, const tt_oracle_spec* o, uint64_t cap, 
   });
 }
 
+// serialize_params / parse_params (ranker.cpp:534-548) and the Siamese
+// checkpoint (momentum.cpp:58-86): text via a caller buffer
+int ref_serialize_params(const double* params, int h, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    std::string t = serialize_params(unflatten(params, h));
+    *len = (int64_t)t.size();
+    if ((int64_t)t.size() < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+  });
+}
+
+int ref_parse_params(const char* text, double* params, int* h) {
+  return guard([&] {
+    RankerParams p = parse_params(text);
+    *h = p.hidden;
+    if (params) flatten(p, params);
+  });
+}
+
+int ref_serialize_siamese(const double* params, int h, double m, int evolved, char* buf, int64_t cap,
+                          int64_t* len) {
+  return guard([&] {
+    SiameseState s;
+    s.params = unflatten(params, h);
+    s.momentum = m;
+    s.provenance = evolved ? SiameseState::Provenance::kEvolved : SiameseState::Provenance::kPretrained;
+    std::string t = serialize_siamese(s);
+    *len = (int64_t)t.size();
+    if ((int64_t)t.size() < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+  });
+}
+
+int ref_parse_siamese(const char* text, double* params, int* h, double* m, int* evolved) {
+  return guard([&] {
+    SiameseState s = parse_siamese(text);
+    *h = s.params.hidden;
+    if (params) flatten(s.params, params);
+    *m = s.momentum;
+    *evolved = s.provenance == SiameseState::Provenance::kEvolved;
+  });
+}
+
 int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t k, int64_t b,
               uint64_t seed, const double* params, int h, int threads, int64_t* sel_idx,
               double* sel_scores, int32_t* drafted_soa, double* drafted_cost,

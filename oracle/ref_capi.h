@@ -53,6 +53,13 @@ int ref_measure(const tt_sketch* sk, const tt_oracle_spec* o, const int32_t* soa
 int ref_oracle_best(const tt_sketch* sk, const tt_oracle_spec* o, uint64_t cap, int32_t* argmin_soa,
                     double* latency);
 
+/* model / Siamese checkpoints (ranker.cpp:534-548, momentum.cpp:58-86) */
+int ref_serialize_params(const double* params, int h, char* buf, int64_t cap, int64_t* len);
+int ref_parse_params(const char* text, double* params, int* h);
+int ref_serialize_siamese(const double* params, int h, double m, int evolved, char* buf, int64_t cap,
+                          int64_t* len);
+int ref_parse_siamese(const char* text, double* params, int* h, double* m, int* evolved);
+
 /* The reference-API draft+verify round of SURVEY.md §3.2, timed inside:
  * explore(n_steps=1) -> extract_features x K -> score_batch -> select_top.
  * Writes the selected b schedules' ranks into sel_idx (positions within the
