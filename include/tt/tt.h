@@ -106,6 +106,17 @@ int tt_draft_topk(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* de
 int tt_explore1(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, uint64_t seed, int64_t first,
                 int64_t n, int64_t k, int toggles, int64_t* idx_dev, double* cost_dev, uint64_t* identity_dev,
                 int64_t* count_host);
+/* explore(op, dev, n_steps, draft_size = k, pop_size = n, RngStream(seed),
+ * toggles) with any n_steps >= 1 — the reference's genetic draft loop
+ * (draft.cpp:156-221; replaces tiletune::explore, draft.hpp). Each
+ * generation's draft costs + identities run on the device (bit-exact); pool
+ * and mutate() (schedule.cpp:340-396, one sequential RNG stream) on the host.
+ * HOST outputs, sorted by (cost, discovery): soa_host (ld = k, nullable),
+ * cost_host, identity_host (nullable); *count_host = pool size (<= k);
+ * *evaluations = n_steps * n. Synchronous. */
+int tt_explore(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, int n_steps, int64_t k, int64_t n,
+               uint64_t seed, int toggles, int32_t* soa_host, double* cost_host, uint64_t* identity_host,
+               int64_t* count_host, uint64_t* evaluations);
 /* Merge R rank-local top-k lists (C1's consumer): m entries of (cost,
  * global index, identity), global index < 0 = empty slot. Same semantics as
  * one explore over the union. Synchronous. */

@@ -15,6 +15,7 @@ What is dumped, per workload shape (reference call in brackets):
   pop       random_init(sketch, 256, RngStream(42))        schedule.cpp:166-186
   cost_tX   draft_cost(...).total with toggles X            draft.cpp:129-154
   ex_soa/ex_cost  explore(op, dev, 1, 64, 2048, RngStream(43))  draft.cpp:156-221
+  ga_soa/ga_cost  explore(op, dev, 8, 64, 128, RngStream(44))   draft.cpp:156-221 + mutate
   st/bl     extract_features of pop[:, :16]                 features.cpp:98-257
   score     score_batch(init_params(64, RngStream(derive_seed(42,"init"))))  ranker.cpp:375-381
   sel       select_top(score, cost_t3[:16], none, 5)        ranker.cpp:514-532
@@ -76,6 +77,8 @@ def main():
             out[f"{name}/cost_t{t}"] = R.R_draft_cost(sk, dev, pop, t)
         ex_soa, ex_cost = R.R_explore(sk, dev, 2048, 64, 43)
         out[f"{name}/ex_soa"], out[f"{name}/ex_cost"] = ex_soa, ex_cost
+        ga_soa, ga_cost = R.R_explore(sk, dev, 128, 64, 44, n_steps=8)
+        out[f"{name}/ga_soa"], out[f"{name}/ga_cost"] = ga_soa, ga_cost
         idx = np.arange(16, dtype=np.int64)
         st, bl = R.R_features(sk, dev, pop, idx)
         out[f"{name}/st"], out[f"{name}/bl"] = st, bl

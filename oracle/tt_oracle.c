@@ -822,3 +822,113 @@ void tto_momentum_update(double* phi, const double* target, int64_t n, double m)
 void tto_gd_step(double* params, const double* grads, int64_t n, double lr) {
   for (int64_t i = 0; i < n; ++i) params[i] -= lr * grads[i];
 }
+
+/* ---------------- genetic explore, any n_steps: draft.cpp:156-221 + mutate, schedule.cpp:340-396 ---------------- */
+
+typedef struct {
+  double cost;
+  uint64_t disc;
+  int32_t f[4 * TT_MAX_AXES + 1];
+} pool_t;
+
+static int pool_cmp(const void* a, const void* b) {
+  const pool_t* x = (const pool_t*)a;
+  const pool_t* y = (const pool_t*)b;
+  if (x->cost != y->cost) return x->cost < y->cost ? -1 : 1;
+  return (x->disc > y->disc) - (x->disc < y->disc);
+}
+
+/* mutate(population, sketch, costs, rng) (schedule.cpp:340-396) on SoA (ld n) */
+static void mutate(const tt_sketch* sk, const int32_t* pop, const double* costs, int64_t n, rng_t* rng,
+                   int32_t* next) {
+  const double eps = 1e-12;
+  const int cols = tt_schedule_cols(sk), n_sp = sk->op.n_spatial;
+  const int n_axes = n_sp + sk->op.n_reduction;
+  double* cum = (double*)malloc(sizeof(double) * (size_t)n);
+  double total = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    total += 1.0 / (costs[i] + eps);
+    cum[i] = total;
+  }
+  int64_t best = 0;
+  for (int64_t i = 1; i < n; ++i)
+    if (costs[i] < costs[best]) best = i;
+  for (int c = 0; c < cols; ++c) next[(int64_t)c * n] = pop[(int64_t)c * n + best];
+  for (int64_t j = 1; j < n; ++j) {
+    double r = rng_real(rng) * total;
+    int64_t lo = 0, hi = n; /* upper_bound: first cum > r */
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (cum[mid] > r) hi = mid; else lo = mid + 1;
+    }
+    int64_t par = lo < n - 1 ? lo : n - 1;
+    for (int c = 0; c < cols; ++c) next[(int64_t)c * n + j] = pop[(int64_t)c * n + par];
+    int slot = (int)rng_index(rng, (uint64_t)n_axes + 1);
+    if (slot == n_axes) {
+      next[(int64_t)(cols - 1) * n + j] = sk->unroll[rng_index(rng, (uint64_t)sk->n_unroll)];
+      continue;
+    }
+    int c0 = axis_col(sk, slot), arity = slot_arity(sk, slot);
+    int mpos[64];
+    int64_t mp[64];
+    int nm = 0;
+    for (int q = 0; q < arity; ++q) {
+      primes_t pr;
+      prime_factorize(next[(int64_t)(c0 + q) * n + j], &pr);
+      for (int t = 0; t < pr.n; ++t)
+        for (int rep = 0; rep < pr.e[t]; ++rep) mpos[nm] = q, mp[nm++] = pr.p[t];
+    }
+    if (nm > 0 && arity > 1) {
+      int m = (int)rng_index(rng, (uint64_t)nm);
+      int from = mpos[m], to = (int)rng_index(rng, (uint64_t)arity - 1);
+      if (to >= from) ++to;
+      next[(int64_t)(c0 + from) * n + j] /= (int32_t)mp[m];
+      next[(int64_t)(c0 + to) * n + j] *= (int32_t)mp[m];
+    }
+  }
+  free(cum);
+}
+
+int64_t tto_explore(const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t k, int64_t n,
+                    uint64_t seed, int toggles, int32_t* soa_out, double* cost_out) {
+  const int cols = tt_schedule_cols(sk);
+  int32_t* pop = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n * cols));
+  int32_t* next = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n * cols));
+  double* cost = (double*)malloc(sizeof(double) * (size_t)n);
+  pool_t* pool = (pool_t*)malloc(sizeof(pool_t) * (size_t)(k + n));
+  int64_t np = 0;
+  uint64_t disc = 0;
+  rng_t rng;
+  rng_init(&rng, seed);
+  tto_random_init(sk, seed, 0, n, pop, n); /* consumes n * D draws of the stream */
+  rng.state += (uint64_t)n * (uint64_t)tto_draws_per_schedule(sk) * GOLDEN;
+  for (int step = 0; step < n_steps; ++step) {
+    tto_draft_cost(sk, dev, pop, n, n, toggles, cost);
+    for (int64_t i = 0; i < n; ++i) { /* insert if the key is new */
+      int found = 0;
+      for (int64_t q = 0; q < np && !found; ++q) {
+        found = 1;
+        for (int c = 0; c < cols && found; ++c) found = pool[q].f[c] == pop[(int64_t)c * n + i];
+      }
+      if (found) continue;
+      pool[np].cost = cost[i], pool[np].disc = disc++;
+      for (int c = 0; c < cols; ++c) pool[np].f[c] = pop[(int64_t)c * n + i];
+      ++np;
+    }
+    if (np > k) { /* trim: the k smallest by (cost, discovery) */
+      qsort(pool, (size_t)np, sizeof(pool_t), pool_cmp);
+      np = k;
+    }
+    if (step + 1 < n_steps) {
+      mutate(sk, pop, cost, n, &rng, next);
+      memcpy(pop, next, sizeof(int32_t) * (size_t)(n * cols));
+    }
+  }
+  qsort(pool, (size_t)np, sizeof(pool_t), pool_cmp);
+  for (int64_t q = 0; q < np; ++q) {
+    cost_out[q] = pool[q].cost;
+    for (int c = 0; c < cols; ++c) soa_out[(int64_t)c * k + q] = pool[q].f[c];
+  }
+  free(pop), free(next), free(cost), free(pool);
+  return np;
+}

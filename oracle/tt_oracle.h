@@ -67,6 +67,12 @@ uint64_t tto_identity(const tt_sketch* sk, const int32_t* soa, int64_t ld, int64
 int64_t tto_draft_topk(const tt_sketch* sk, const double* cost, const int32_t* soa, int64_t ld,
                        int64_t n, int64_t k, int64_t* idx_out, double* cost_out);
 
+/* explore(op, dev, n_steps, K, N, RngStream(seed), toggles) for any
+ * n_steps (draft.cpp:156-221, mutate schedule.cpp:340-396): the pool sorted
+ * by (cost, discovery), SoA ld = K. Returns the pool size (<= K). */
+int64_t tto_explore(const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t k, int64_t n,
+                    uint64_t seed, int toggles, int32_t* soa_out, double* cost_out);
+
 /* extract_features for columns idx[0..k) (features.cpp:98-257):
  * stmt_out [k][S][24], block_out [k][B][23]. */
 void tto_features(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld,

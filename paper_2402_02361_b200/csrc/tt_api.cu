@@ -11,6 +11,7 @@
 #include <string>
 #include <map>
 #include <set>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/tt/tt.h"
@@ -61,6 +62,12 @@ struct tt_ctx {
   uint8_t* d_tiles = nullptr;
   // merge inputs
   int64_t m_cap = 0;
+  // multi-step explore (GA): one generation on the device, its pinned host mirror
+  int64_t ex_cap = 0;
+  int32_t* d_ex_soa = nullptr;
+  double* d_ex_cost = nullptr;
+  uint64_t* d_ex_id = nullptr;
+  void* h_ex = nullptr;  // pinned: soa | cost | id
   // last async round
   int64_t last_b = 0;
   int64_t last_k = 0;
@@ -515,10 +522,11 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
-                  c->d_tiles};
+                  c->d_tiles, c->d_ex_soa, c->d_ex_cost, c->d_ex_id};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_record) cudaFreeHost(c->h_record);
+  if (c->h_ex) cudaFreeHost(c->h_ex);
   graphs_clear(c);
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -1457,3 +1465,188 @@ int tt_round_drafted(const tt_ctx* ctx, const int64_t** idx, const double** cost
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// explore() with n_steps > 1: the reference's genetic draft loop
+// (draft.cpp:156-221). Each generation's draft costs and identities are
+// computed on the device (K1 + identity kernels, bit-exact); the pool
+// bookkeeping and mutate() (schedule.cpp:340-396) stay on the host because
+// mutate consumes ONE sequential RngStream whose draw count per child depends
+// on the parent it picked — every child's offset in the stream depends on all
+// earlier children. The pool is keyed by the exact 64-bit identity, which is
+// injective, hence equivalent to schedule_key's string (schedule.cpp:280-296).
+namespace {
+
+void prime_factorize_h(int64_t n, std::vector<std::pair<int64_t, int>>& out) {
+  out.clear();
+  for (int64_t p = 2; p * p <= n; ++p)
+    if (n % p == 0) {
+      int e = 0;
+      while (n % p == 0) n /= p, ++e;
+      out.emplace_back(p, e);
+    }
+  if (n > 1) out.emplace_back(n, 1);
+}
+
+int ensure_explore(tt_ctx* ctx, int64_t n, int cols) {
+  const int64_t want = n * cols;
+  if (want <= ctx->ex_cap && ctx->d_ex_soa) return TT_OK;
+  cudaFree(ctx->d_ex_soa), cudaFree(ctx->d_ex_cost), cudaFree(ctx->d_ex_id);
+  if (ctx->h_ex) cudaFreeHost(ctx->h_ex);
+  ctx->d_ex_soa = nullptr, ctx->d_ex_cost = nullptr, ctx->d_ex_id = nullptr, ctx->h_ex = nullptr;
+  ctx->ex_cap = 0;
+  // cost / id sized by `want` too (cols >= 2), so one capacity covers all three
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_ex_soa, sizeof(int32_t) * want));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_ex_cost, sizeof(double) * want));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_ex_id, sizeof(uint64_t) * want));
+  TT_CUDA(ctx, cudaMallocHost(&ctx->h_ex, (sizeof(int32_t) + sizeof(double) + sizeof(uint64_t)) * want + 16));
+  ctx->ex_cap = want;
+  return TT_OK;
+}
+
+// mutate(population, sketch, costs, rng) (schedule.cpp:340-396) on SoA
+// columns: pop (ld n) -> next (ld n), same draw sequence as the reference.
+void mutate_h(const DevSketch& S, const tt_sketch* sk, const int32_t* pop, const double* costs, int64_t n,
+              HostRng& rng, int32_t* next) {
+  constexpr double kEps = 1e-12;
+  std::vector<double> cumulative((size_t)n);
+  double total = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    total += 1.0 / (costs[i] + kEps);
+    cumulative[(size_t)i] = total;
+  }
+  int64_t best = 0;
+  for (int64_t i = 1; i < n; ++i)
+    if (costs[i] < costs[best]) best = i;
+  const int cols = S.cols, n_axes = S.n_axes;
+  const int ucol = 4 * S.n_sp + 3 * S.n_red;
+  for (int c = 0; c < cols; ++c) next[(int64_t)c * n] = pop[(int64_t)c * n + best];  // elite
+  std::vector<std::pair<int64_t, int>> pf;
+  int32_t f[4];
+  int mv_pos[64];
+  int64_t mv_p[64];
+  for (int64_t j = 1; j < n; ++j) {
+    const double r = (double)(rng.next() >> 11) * 0x1.0p-53 * total;
+    int64_t par = std::upper_bound(cumulative.begin(), cumulative.end(), r) - cumulative.begin();
+    if (par > n - 1) par = n - 1;
+    for (int c = 0; c < cols; ++c) next[(int64_t)c * n + j] = pop[(int64_t)c * n + par];
+    const int slot = (int)rng.index((uint64_t)n_axes + 1);
+    if (slot == n_axes) {
+      next[(int64_t)ucol * n + j] = sk->unroll[rng.index((uint64_t)sk->n_unroll)];
+      continue;
+    }
+    const int col0 = slot < S.n_sp ? 4 * slot : 4 * S.n_sp + 3 * (slot - S.n_sp);
+    const int arity = S.arity[slot];
+    for (int q = 0; q < arity; ++q) f[q] = next[(int64_t)(col0 + q) * n + j];
+    int n_moves = 0;
+    for (int q = 0; q < arity; ++q) {
+      prime_factorize_h(f[q], pf);
+      for (auto& [p, e] : pf)
+        for (int rep = 0; rep < e && n_moves < 64; ++rep) mv_pos[n_moves] = q, mv_p[n_moves++] = p;
+    }
+    if (n_moves > 0 && arity > 1) {
+      const int m = (int)rng.index((uint64_t)n_moves);
+      const int from = mv_pos[m];
+      const int64_t prime = mv_p[m];
+      int to = (int)rng.index((uint64_t)arity - 1);
+      if (to >= from) ++to;
+      next[(int64_t)(col0 + from) * n + j] = (int32_t)(f[from] / prime);
+      next[(int64_t)(col0 + to) * n + j] = (int32_t)(f[to] * prime);
+    }
+  }
+}
+
+}  // namespace
+
+int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t k, int64_t n,
+               uint64_t seed, int toggles, int32_t* soa_host, double* cost_host, uint64_t* id_host,
+               int64_t* count_host, uint64_t* evaluations) {
+  if (!ctx) return TT_E_STATE;
+  if (n_steps < 1) return fail(ctx, TT_E_STATE, "explore: n_steps must be >= 1");
+  if (k < 1) return fail(ctx, TT_E_STATE, "explore: draft_size must be >= 1");
+  if (n < 2) return fail(ctx, TT_E_STATE, "explore: pop_size must be >= 2");
+  if (!count_host || !cost_host) return fail(ctx, TT_E_STATE, "explore: null output");
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "explore: schedule space exceeds 2^64 identities");
+  if (n > (int64_t)1 << 31) return fail(ctx, TT_E_STATE, "explore: pop_size too large");
+  const int cols = S.cols;
+  if ((rc = ensure_explore(ctx, n, cols))) return rc;
+  int32_t* h_soa = (int32_t*)ctx->h_ex;
+  double* h_cost = (double*)((char*)h_soa + ((sizeof(int32_t) * (size_t)n * cols + 15) & ~(size_t)15));
+  uint64_t* h_id = (uint64_t*)(h_cost + n);
+  const uint64_t s0 = seed_state(seed);
+  // random_init(sketch, n, rng): the counter-based K0 stream is the
+  // sequential one, so the host RNG resumes after n * draws_per_schedule
+  if (launch_generate(S, s0, 0, n, ctx->d_ex_soa, n, ctx->d_ex_id, ctx->stream))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+  TT_CUDA(ctx, cudaMemcpyAsync(h_soa, ctx->d_ex_soa, sizeof(int32_t) * n * cols, cudaMemcpyDeviceToHost, ctx->stream));
+  HostRng rng(s0);
+  rng.s = s0 + (uint64_t)n * (uint64_t)(S.n_prime + 1) * kGolden;
+
+  struct Entry {
+    uint64_t id;
+    double cost;
+    uint64_t disc;
+    int32_t f[4 * TT_MAX_AXES + 1];
+  };
+  std::vector<Entry> pool;
+  std::unordered_map<uint64_t, size_t> where;
+  pool.reserve((size_t)(k + n));
+  where.reserve((size_t)(k + n) * 2);
+  uint64_t discovery = 0;
+  std::vector<int32_t> next((size_t)n * cols);
+  auto by_cost = [](const Entry& a, const Entry& b) { return a.cost != b.cost ? a.cost < b.cost : a.disc < b.disc; };
+
+  for (int step = 0; step < n_steps; ++step) {
+    if (step > 0) {
+      TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_ex_soa, h_soa, sizeof(int32_t) * n * cols, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+      if (launch_identity(S, ctx->d_ex_soa, n, n, ctx->d_ex_id, ctx->stream))
+        return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+      TT_LAUNCHED(ctx);
+    }
+    TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+    if (launch_draft_cost(S, D, ctx->d_ex_soa, n, 0, 0, false, n, toggles, ctx->d_ex_cost, nullptr,
+                          ctx->sel.invalid, ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    TT_LAUNCHED(ctx);
+    TT_CUDA(ctx, cudaMemcpyAsync(h_cost, ctx->d_ex_cost, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(ctx, cudaMemcpyAsync(h_id, ctx->d_ex_id, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((rc = sync_check(ctx))) return rc;
+    // pool insertion in population order (first discovery wins) + trim
+    for (int64_t i = 0; i < n; ++i) {
+      if (where.count(h_id[i])) continue;
+      Entry e;
+      e.id = h_id[i], e.cost = h_cost[i], e.disc = discovery++;
+      for (int c = 0; c < cols; ++c) e.f[c] = h_soa[(int64_t)c * n + i];
+      where.emplace(e.id, pool.size());
+      pool.push_back(e);
+    }
+    if ((int64_t)pool.size() > k) {
+      std::nth_element(pool.begin(), pool.begin() + k, pool.end(), by_cost);
+      pool.resize((size_t)k);
+      where.clear();
+      for (size_t q = 0; q < pool.size(); ++q) where.emplace(pool[q].id, q);
+    }
+    if (step + 1 < n_steps) {
+      mutate_h(S, sk, h_soa, h_cost, n, rng, next.data());
+      std::memcpy(h_soa, next.data(), sizeof(int32_t) * n * cols);
+    }
+  }
+  std::sort(pool.begin(), pool.end(), by_cost);
+  const int64_t cnt = (int64_t)pool.size();
+  for (int64_t q = 0; q < cnt; ++q) {
+    cost_host[q] = pool[(size_t)q].cost;
+    if (id_host) id_host[q] = pool[(size_t)q].id;
+    if (soa_host)
+      for (int c = 0; c < cols; ++c) soa_host[(int64_t)c * k + q] = pool[(size_t)q].f[c];
+  }
+  *count_host = cnt;
+  if (evaluations) *evaluations = (uint64_t)n_steps * (uint64_t)n;
+  return TT_OK;
+}

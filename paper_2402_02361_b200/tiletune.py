@@ -157,6 +157,24 @@ def explore1(ctx: Context, sketch: Sketch, dev: DeviceSpec, seed: int, n: int, k
     return idx[:m], cost[:m], ids[:m]
 
 
+def explore(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft_size: int, pop_size: int, seed: int,
+            toggles: int = TT_TOGGLES_ALL):
+    """explore(op, dev, n_steps, draft_size, pop_size, RngStream(seed), toggles)
+    (draft.cpp:156-221): the genetic draft loop. Returns host numpy arrays
+    (soa [cols, count] int32, cost [count], identity [count] uint64,
+    evaluations), sorted by (cost, discovery) like ExploreResult.drafted."""
+    cols = sketch.cols
+    soa = np.zeros((cols, draft_size), np.int32)
+    cost = np.zeros(draft_size, np.float64)
+    ids = np.zeros(draft_size, np.uint64)
+    cnt, ev = C.c_int64(0), C.c_uint64(0)
+    ctx.check(lib().tt_explore(ctx.h, C.byref(sketch), C.byref(dev), n_steps, draft_size, pop_size,
+                               seed & (2**64 - 1), toggles, soa.ctypes.data, cost.ctypes.data, ids.ctypes.data,
+                               C.byref(cnt), C.byref(ev)))
+    m = cnt.value
+    return np.ascontiguousarray(soa[:, :m]), cost[:m], ids[:m], ev.value
+
+
 def topk_merge(ctx: Context, cost: torch.Tensor, gidx: torch.Tensor, ids: torch.Tensor, k: int):
     idx, c, i = _topk_out(ctx, k)
     cnt = C.c_int64(0)

@@ -43,6 +43,7 @@ def oracle():
             "tto_trace": (C.c_int, [sk, dv, i32p, C.c_int64, C.c_int64, C.c_int, i64p, f64p, f64p, f64p]),
             "tto_identity": (C.c_uint64, [sk, i32p, C.c_int64, C.c_int64, P(C.c_int)]),
             "tto_draft_topk": (C.c_int64, [sk, f64p, i32p, C.c_int64, C.c_int64, C.c_int64, i64p, f64p]),
+            "tto_explore": (C.c_int64, [sk, dv, C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int, i32p, f64p]),
             "tto_features": (None, [sk, dv, i32p, C.c_int64, i64p, C.c_int64, f64p, f64p]),
             "tto_init_params": (None, [C.c_int, C.c_uint64, f64p]),
             "tto_score": (None, [f64p, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_int64, C.c_int, f64p]),
@@ -150,6 +151,13 @@ def R_explore(sk, dev, n, k, seed, n_steps=1, threads=1):
     ev = C.c_uint64(0)
     check(ref().ref_explore(C.byref(sk), C.byref(dev), n_steps, k, n, seed, threads, ptr(soa, i32p), ptr(cost, f64p), C.byref(cnt), C.byref(ev)))
     m = cnt.value
+    return np.ascontiguousarray(soa[:, :m]), cost[:m]
+
+
+def O_explore(sk, dev, n, k, seed, n_steps, toggles=3):
+    soa = np.zeros((sk.cols, k), np.int32)
+    cost = np.zeros(k)
+    m = oracle().tto_explore(C.byref(sk), C.byref(dev), n_steps, k, n, seed, toggles, ptr(soa, i32p), ptr(cost, f64p))
     return np.ascontiguousarray(soa[:, :m]), cost[:m]
 
 

@@ -247,6 +247,15 @@ def test_oracle_space_and_draws():
     assert R.oracle().tto_draws_per_schedule(C.byref(sk)) == 4
 
 
+@pytest.mark.parametrize("name", SHAPES)
+def test_golden_explore_genetic(G, name):
+    # explore(op, dev, 8, 64, 128, RngStream(44)): 8 generations of mutate()
+    sk = sketch_of(name)
+    soa, c = R.O_explore(sk, DEV, 128, 64, 44, 8)
+    assert (bits(c) == bits(G[f"{name}/ga_cost"])).all()
+    assert (soa == G[f"{name}/ga_soa"]).all()
+
+
 # ------------------------------------------ live reference (when built here) --
 
 live = pytest.mark.skipif(not R.ref_available(), reason="oracle/_ref not built (no /root/reference here)")
@@ -263,6 +272,18 @@ def test_live_population_cost_explore(name):
     idx, c = R.O_draft_topk(sk, cost, pop, 512)
     rs, rc = R.R_explore(sk, DEV, 20000, 512, 7)
     assert (bits(c) == bits(rc)).all() and (pop[:, idx] == rs).all()
+
+
+@live
+@pytest.mark.parametrize("name,n,k,steps", [("gemm1024", 512, 512, 32), ("r50_c3x3_64", 512, 128, 32),
+                                            ("bert_ffn1", 300, 1000, 12), ("elementwise", 64, 16, 40),
+                                            ("gemm4", 256, 64, 20)])
+def test_live_explore_genetic(name, n, k, steps):
+    # the reference's real per-round explore: n_steps generations, pool trim, mutate()
+    sk = make_sketch(make_gemm(4, 4, 4)) if name == "gemm4" else sketch_of(name)
+    soa, c = R.O_explore(sk, DEV, n, k, 11, steps)
+    rs, rc = R.R_explore(sk, DEV, n, k, 11, n_steps=steps)
+    assert len(c) == len(rc) and (bits(c) == bits(rc)).all() and (soa == rs).all()
 
 
 @live
