@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -63,11 +64,10 @@ struct tt_ctx {
   // merge inputs
   int64_t m_cap = 0;
   // multi-step explore (GA): one generation on the device, its pinned host mirror
-  int64_t ex_cap = 0;
-  int32_t* d_ex_soa = nullptr;
-  double* d_ex_cost = nullptr;
-  uint64_t* d_ex_id = nullptr;
-  void* h_ex = nullptr;  // pinned: soa | cost | id
+  size_t ex_dcap = 0, ex_hcap = 0;
+  void* d_ex = nullptr;  // two device generation slots + the RNG state
+  void* h_ex = nullptr;  // pinned generation slots: soa | cost | identity
+  std::vector<cudaEvent_t> ex_ev;  // one per generation in flight
   // last async round
   int64_t last_b = 0;
   int64_t last_k = 0;
@@ -522,11 +522,12 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
-                  c->d_tiles, c->d_ex_soa, c->d_ex_cost, c->d_ex_id};
+                  c->d_tiles, c->d_ex};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_record) cudaFreeHost(c->h_record);
   if (c->h_ex) cudaFreeHost(c->h_ex);
+  for (cudaEvent_t e : c->ex_ev) cudaEventDestroy(e);
   graphs_clear(c);
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -1477,30 +1478,42 @@ int tt_round_drafted(const tt_ctx* ctx, const int64_t** idx, const double** cost
 // injective, hence equivalent to schedule_key's string (schedule.cpp:280-296).
 namespace {
 
-void prime_factorize_h(int64_t n, std::vector<std::pair<int64_t, int>>& out) {
-  out.clear();
-  for (int64_t p = 2; p * p <= n; ++p)
-    if (n % p == 0) {
-      int e = 0;
-      while (n % p == 0) n /= p, ++e;
-      out.emplace_back(p, e);
-    }
-  if (n > 1) out.emplace_back(n, 1);
+// One generation in a flat slot (device or pinned host): soa (ld n) |
+// cost [n] | identity [n]; a whole slot moves in one copy.
+struct GenSlot {
+  int32_t* soa;
+  double* cost;
+  uint64_t* id;
+};
+size_t gen_bytes(int64_t n, int cols) { return (((size_t)n * cols * 4 + 15) & ~(size_t)15) + 16 * (size_t)n; }
+GenSlot gen_slot(void* base, int64_t n, int cols, int which) {
+  char* p = (char*)base + (size_t)which * gen_bytes(n, cols);
+  GenSlot g;
+  g.soa = (int32_t*)p;
+  g.cost = (double*)(p + (((size_t)n * cols * 4 + 15) & ~(size_t)15));
+  g.id = (uint64_t*)(g.cost + n);
+  return g;
 }
 
-int ensure_explore(tt_ctx* ctx, int64_t n, int cols) {
-  const int64_t want = n * cols;
-  if (want <= ctx->ex_cap && ctx->d_ex_soa) return TT_OK;
-  cudaFree(ctx->d_ex_soa), cudaFree(ctx->d_ex_cost), cudaFree(ctx->d_ex_id);
-  if (ctx->h_ex) cudaFreeHost(ctx->h_ex);
-  ctx->d_ex_soa = nullptr, ctx->d_ex_cost = nullptr, ctx->d_ex_id = nullptr, ctx->h_ex = nullptr;
-  ctx->ex_cap = 0;
-  // cost / id sized by `want` too (cols >= 2), so one capacity covers all three
-  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_ex_soa, sizeof(int32_t) * want));
-  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_ex_cost, sizeof(double) * want));
-  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_ex_id, sizeof(uint64_t) * want));
-  TT_CUDA(ctx, cudaMallocHost(&ctx->h_ex, (sizeof(int32_t) + sizeof(double) + sizeof(uint64_t)) * want + 16));
-  ctx->ex_cap = want;
+int ensure_explore(tt_ctx* ctx, int64_t n, int cols, int host_slots) {
+  const size_t dwant = 2 * gen_bytes(n, cols) + 16, hwant = (size_t)host_slots * gen_bytes(n, cols) + 16;
+  if (dwant > ctx->ex_dcap) {
+    cudaFree(ctx->d_ex);
+    ctx->d_ex = nullptr, ctx->ex_dcap = 0;
+    TT_CUDA(ctx, cudaMalloc(&ctx->d_ex, dwant));
+    ctx->ex_dcap = dwant;
+  }
+  if (hwant > ctx->ex_hcap) {
+    if (ctx->h_ex) cudaFreeHost(ctx->h_ex);
+    ctx->h_ex = nullptr, ctx->ex_hcap = 0;
+    TT_CUDA(ctx, cudaMallocHost(&ctx->h_ex, hwant));
+    ctx->ex_hcap = hwant;
+  }
+  while ((int)ctx->ex_ev.size() < host_slots) {
+    cudaEvent_t e;
+    TT_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ex_ev.push_back(e);
+  }
   return TT_OK;
 }
 
@@ -1521,7 +1534,6 @@ void mutate_h(const DevSketch& S, const tt_sketch* sk, const int32_t* pop, const
   const int cols = S.cols, n_axes = S.n_axes;
   const int ucol = 4 * S.n_sp + 3 * S.n_red;
   for (int c = 0; c < cols; ++c) next[(int64_t)c * n] = pop[(int64_t)c * n + best];  // elite
-  std::vector<std::pair<int64_t, int>> pf;
   int32_t f[4];
   int mv_pos[64];
   int64_t mv_p[64];
@@ -1538,11 +1550,24 @@ void mutate_h(const DevSketch& S, const tt_sketch* sk, const int32_t* pop, const
     const int col0 = slot < S.n_sp ? 4 * slot : 4 * S.n_sp + 3 * (slot - S.n_sp);
     const int arity = S.arity[slot];
     for (int q = 0; q < arity; ++q) f[q] = next[(int64_t)(col0 + q) * n + j];
+    // prime_factorize(f[q]) (schedule.cpp:93-108): every factor divides the
+    // axis extent, so only the extent's primes (ascending) occur; exponents
+    // by ctz for 2 and by exact-division inverses for odd primes (no idiv)
     int n_moves = 0;
     for (int q = 0; q < arity; ++q) {
-      prime_factorize_h(f[q], pf);
-      for (auto& [p, e] : pf)
+      uint32_t v = (uint32_t)f[q];
+      for (int t = 0; t < S.n_prime && v > 1; ++t) {
+        if (S.pr_axis[t] != slot) continue;
+        const int32_t p = (int32_t)S.pr_p[t];
+        int e = 0;
+        if (p == 2) {
+          e = __builtin_ctz(v);
+          v >>= e;
+        } else {
+          for (uint32_t qv = v * S.pr_inv[t]; qv <= S.pr_lim[t]; qv = v * S.pr_inv[t]) v = qv, ++e;
+        }
         for (int rep = 0; rep < e && n_moves < 64; ++rep) mv_pos[n_moves] = q, mv_p[n_moves++] = p;
+      }
     }
     if (n_moves > 0 && arity > 1) {
       const int m = (int)rng.index((uint64_t)n_moves);
@@ -1574,77 +1599,147 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   if (!S.id_exact) return fail(ctx, TT_E_STATE, "explore: schedule space exceeds 2^64 identities");
   if (n > (int64_t)1 << 31) return fail(ctx, TT_E_STATE, "explore: pop_size too large");
   const int cols = S.cols;
-  if ((rc = ensure_explore(ctx, n, cols))) return rc;
-  int32_t* h_soa = (int32_t*)ctx->h_ex;
-  double* h_cost = (double*)((char*)h_soa + ((sizeof(int32_t) * (size_t)n * cols + 15) & ~(size_t)15));
-  uint64_t* h_id = (uint64_t*)(h_cost + n);
+  // Device generations (mutate on the GPU, nothing on the host's critical
+  // path) when one CTA holds the roulette wheel and the pinned mirror of all
+  // generations stays modest; otherwise mutate() runs on the host between
+  // device generations.
+  const bool on_device = n <= kMutateMaxN && (size_t)n_steps * gen_bytes(n, cols) <= ((size_t)1 << 30);
+  const int host_slots = on_device ? n_steps : 2;
+  if ((rc = ensure_explore(ctx, n, cols, host_slots))) return rc;
+  GenSlot dgen[2] = {gen_slot(ctx->d_ex, n, cols, 0), gen_slot(ctx->d_ex, n, cols, 1)};
+  uint64_t* d_state = (uint64_t*)((char*)ctx->d_ex + 2 * gen_bytes(n, cols));
+  uint64_t* h_state = (uint64_t*)((char*)ctx->h_ex + (size_t)host_slots * gen_bytes(n, cols));
+  auto hgen = [&](int i) { return gen_slot(ctx->h_ex, n, cols, i); };
   const uint64_t s0 = seed_state(seed);
-  // random_init(sketch, n, rng): the counter-based K0 stream is the
-  // sequential one, so the host RNG resumes after n * draws_per_schedule
-  if (launch_generate(S, s0, 0, n, ctx->d_ex_soa, n, ctx->d_ex_id, ctx->stream))
-    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
-  TT_LAUNCHED(ctx);
-  TT_CUDA(ctx, cudaMemcpyAsync(h_soa, ctx->d_ex_soa, sizeof(int32_t) * n * cols, cudaMemcpyDeviceToHost, ctx->stream));
-  HostRng rng(s0);
-  rng.s = s0 + (uint64_t)n * (uint64_t)(S.n_prime + 1) * kGolden;
-
-  struct Entry {
-    uint64_t id;
-    double cost;
-    uint64_t disc;
-    int32_t f[4 * TT_MAX_AXES + 1];
-  };
-  std::vector<Entry> pool;
-  std::unordered_map<uint64_t, size_t> where;
-  pool.reserve((size_t)(k + n));
-  where.reserve((size_t)(k + n) * 2);
-  uint64_t discovery = 0;
-  std::vector<int32_t> next((size_t)n * cols);
-  auto by_cost = [](const Entry& a, const Entry& b) { return a.cost != b.cost ? a.cost < b.cost : a.disc < b.disc; };
-
-  for (int step = 0; step < n_steps; ++step) {
-    if (step > 0) {
-      TT_CUDA(ctx, cudaMemcpyAsync(ctx->d_ex_soa, h_soa, sizeof(int32_t) * n * cols, cudaMemcpyHostToDevice,
-                                   ctx->stream));
-      if (launch_identity(S, ctx->d_ex_soa, n, n, ctx->d_ex_id, ctx->stream))
-        return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
-      TT_LAUNCHED(ctx);
-    }
-    TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
-    if (launch_draft_cost(S, D, ctx->d_ex_soa, n, 0, 0, false, n, toggles, ctx->d_ex_cost, nullptr,
-                          ctx->sel.invalid, ctx->stream))
+  // random_init(sketch, n, rng) consumes n * draws_per_schedule draws of the
+  // stream; mutate() continues from there
+  const uint64_t s_init = s0 + (uint64_t)n * (uint64_t)(S.n_prime + 1) * kGolden;
+  cudaStream_t st = ctx->stream;
+  auto cost_and_copy = [&](GenSlot& d, GenSlot& h, cudaEvent_t ev) -> int {
+    if (launch_draft_cost(S, D, d.soa, n, 0, 0, false, n, toggles, d.cost, nullptr, ctx->sel.invalid, st))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
-    TT_CUDA(ctx, cudaMemcpyAsync(h_cost, ctx->d_ex_cost, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    TT_CUDA(ctx, cudaMemcpyAsync(h_id, ctx->d_ex_id, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    if ((rc = sync_check(ctx))) return rc;
-    // pool insertion in population order (first discovery wins) + trim
+    TT_CUDA(ctx, cudaMemcpyAsync(h.soa, d.soa, gen_bytes(n, cols), cudaMemcpyDeviceToHost, st));
+    TT_CUDA(ctx, cudaEventRecord(ev, st));
+    return TT_OK;
+  };
+  if (launch_generate(S, s0, 0, n, dgen[0].soa, n, dgen[0].id, st))
+    return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+  TT_LAUNCHED(ctx);
+
+  // the pool (draft.cpp:166-170), flat: identity, cost, discovery, factors;
+  // membership by an open-addressing table over identities, cleared in O(1)
+  // per trim by bumping its epoch
+  const int64_t cap = k + n;
+  std::vector<uint64_t> p_id((size_t)cap), p_disc((size_t)cap);
+  std::vector<double> p_cost((size_t)cap);
+  std::vector<int32_t> p_f((size_t)(cap * cols));
+  std::vector<uint64_t> t_p_id((size_t)cap), t_p_disc((size_t)cap);
+  std::vector<double> t_p_cost((size_t)cap);
+  std::vector<int32_t> t_p_f((size_t)(cap * cols));
+  std::vector<uint32_t> order((size_t)cap);
+  int hbits = 4;
+  while (((int64_t)1 << hbits) < 2 * cap) ++hbits;
+  const uint64_t hmask = ((uint64_t)1 << hbits) - 1;
+  std::vector<uint64_t> h_key((size_t)hmask + 1);
+  std::vector<uint32_t> h_epoch((size_t)hmask + 1, 0);
+  uint32_t epoch = 1;
+  auto h_insert = [&](uint64_t id) -> bool {  // true if id was new
+    for (uint64_t h = scramble64(id) & hmask;; h = (h + 1) & hmask) {
+      if (h_epoch[h] != epoch) {
+        h_epoch[h] = epoch, h_key[h] = id;
+        return true;
+      }
+      if (h_key[h] == id) return false;
+    }
+  };
+  int64_t np = 0;
+  uint64_t discovery = 0;
+  auto by_cost = [&](uint32_t a, uint32_t b) {
+    return p_cost[a] != p_cost[b] ? p_cost[a] < p_cost[b] : p_disc[a] < p_disc[b];
+  };
+  // pool insertion in population order (first discovery wins,
+  // draft.cpp:198-204) + trim to the k smallest (cost, discovery) (:174-191)
+  auto consume = [&](const GenSlot& g) {
     for (int64_t i = 0; i < n; ++i) {
-      if (where.count(h_id[i])) continue;
-      Entry e;
-      e.id = h_id[i], e.cost = h_cost[i], e.disc = discovery++;
-      for (int c = 0; c < cols; ++c) e.f[c] = h_soa[(int64_t)c * n + i];
-      where.emplace(e.id, pool.size());
-      pool.push_back(e);
+      if (!h_insert(g.id[i])) continue;
+      p_id[np] = g.id[i], p_cost[np] = g.cost[i], p_disc[np] = discovery++;
+      for (int c = 0; c < cols; ++c) p_f[np * cols + c] = g.soa[(int64_t)c * n + i];
+      ++np;
     }
-    if ((int64_t)pool.size() > k) {
-      std::nth_element(pool.begin(), pool.begin() + k, pool.end(), by_cost);
-      pool.resize((size_t)k);
-      where.clear();
-      for (size_t q = 0; q < pool.size(); ++q) where.emplace(pool[q].id, q);
+    if (np > k) {
+      for (int64_t q = 0; q < np; ++q) order[q] = (uint32_t)q;
+      std::nth_element(order.begin(), order.begin() + k, order.begin() + np, by_cost);
+      ++epoch;
+      for (int64_t q = 0; q < k; ++q) {
+        const uint32_t o = order[q];
+        t_p_id[q] = p_id[o], t_p_cost[q] = p_cost[o], t_p_disc[q] = p_disc[o];
+        std::memcpy(&t_p_f[q * cols], &p_f[(size_t)o * cols], sizeof(int32_t) * cols);
+        h_insert(p_id[o]);
+      }
+      p_id.swap(t_p_id), p_cost.swap(t_p_cost), p_disc.swap(t_p_disc), p_f.swap(t_p_f);
+      np = k;
     }
-    if (step + 1 < n_steps) {
-      mutate_h(S, sk, h_soa, h_cost, n, rng, next.data());
-      std::memcpy(h_soa, next.data(), sizeof(int32_t) * n * cols);
+  };
+
+  if (on_device) {
+    // every generation enqueued back to back: mutate -> identities -> draft
+    // costs -> one copy of the slot to its pinned mirror; the host folds
+    // generation g into the pool as soon as its event fires
+    *h_state = s_init;
+    TT_CUDA(ctx, cudaMemcpyAsync(d_state, h_state, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    for (int g = 0; g < n_steps; ++g) {
+      GenSlot& d = dgen[g & 1];
+      if (g > 0) {
+        GenSlot& prev = dgen[(g - 1) & 1];
+        if (launch_mutate(S, prev.soa, prev.cost, n, d_state, d.soa, st))
+          return fail(ctx, TT_E_STATE, "explore: mutate launch");
+        TT_LAUNCHED(ctx);
+        if (launch_identity(S, d.soa, n, n, d.id, st)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+        TT_LAUNCHED(ctx);
+      }
+      GenSlot h = hgen(g);
+      if ((rc = cost_and_copy(d, h, ctx->ex_ev[g]))) return rc;
+    }
+    for (int g = 0; g < n_steps; ++g) {
+      TT_CUDA(ctx, cudaEventSynchronize(ctx->ex_ev[g]));
+      consume(hgen(g));
+    }
+    if ((rc = sync_check(ctx))) return rc;
+  } else {
+    GenSlot h0 = hgen(0);
+    if ((rc = cost_and_copy(dgen[0], h0, ctx->ex_ev[0]))) return rc;
+    if ((rc = sync_check(ctx))) return rc;
+    HostRng rng(s0);
+    rng.s = s_init;
+    int cur = 0;
+    for (int step = 0; step < n_steps; ++step) {
+      GenSlot g = hgen(cur), nx = hgen(cur ^ 1);
+      const bool more = step + 1 < n_steps;
+      if (more) {  // critical path: mutate on the host, the next generation's device work
+        mutate_h(S, sk, g.soa, g.cost, n, rng, nx.soa);
+        TT_CUDA(ctx, cudaMemcpyAsync(dgen[0].soa, nx.soa, sizeof(int32_t) * n * cols, cudaMemcpyHostToDevice, st));
+        if (launch_identity(S, dgen[0].soa, n, n, dgen[0].id, st))
+          return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+        TT_LAUNCHED(ctx);
+        if ((rc = cost_and_copy(dgen[0], nx, ctx->ex_ev[cur ^ 1]))) return rc;
+      }
+      consume(g);  // overlaps the device
+      if (more) {
+        if ((rc = sync_check(ctx))) return rc;
+        cur ^= 1;
+      }
     }
   }
-  std::sort(pool.begin(), pool.end(), by_cost);
-  const int64_t cnt = (int64_t)pool.size();
+  for (int64_t q = 0; q < np; ++q) order[q] = (uint32_t)q;
+  std::sort(order.begin(), order.begin() + np, by_cost);
+  const int64_t cnt = np;
   for (int64_t q = 0; q < cnt; ++q) {
-    cost_host[q] = pool[(size_t)q].cost;
-    if (id_host) id_host[q] = pool[(size_t)q].id;
+    const uint32_t o = order[q];
+    cost_host[q] = p_cost[o];
+    if (id_host) id_host[q] = p_id[o];
     if (soa_host)
-      for (int c = 0; c < cols; ++c) soa_host[(int64_t)c * k + q] = pool[(size_t)q].f[c];
+      for (int c = 0; c < cols; ++c) soa_host[(int64_t)c * k + q] = p_f[(size_t)o * cols + c];
   }
   *count_host = cnt;
   if (evaluations) *evaluations = (uint64_t)n_steps * (uint64_t)n;

@@ -85,6 +85,11 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
                   int64_t first, bool seeded, int64_t n, int64_t k, int64_t need, int toggles,
                   int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
                   int64_t* out_count, cudaStream_t st, bool hash = false);
+// k_explore.cu: one GA generation, mutate() bit-exact, one CTA (n <= kMutateMaxN).
+// state: the RngStream state (device), advanced past the generation's draws.
+constexpr int64_t kMutateMaxN = 8192;
+int launch_mutate(const DevSketch& S, const int32_t* pop, const double* cost, int64_t n, uint64_t* state,
+                  int32_t* next, cudaStream_t st);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);
 // identities of the drafted set (side stream)
