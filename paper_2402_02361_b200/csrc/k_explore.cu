@@ -9,8 +9,9 @@
 //      child, the number of draws L(o) in {2, 3, 4} a child starting there
 //      consumes (parent and slot are functions of draws o, o+1 only — the
 //      stream is counter based);
-//   2. one thread walks the chain o_1 = 0, o_{j+1} = o_j + L(o_j) over L in
-//      shared memory (n - 1 dependent shared loads);
+//   2. the chain o_1 = 0, o_{j+1} = o_j + L(o_j) over L in shared memory,
+//      walked per segment from each of the 4 possible entry offsets, stitched
+//      by one thread, then re-walked to write every child's offset;
 //   3. a parallel apply pass: child j re-derives its draws at o_j and writes
 //      its factors.
 // The roulette-wheel prefix sum is one thread's fp64 chain in the reference
@@ -28,12 +29,21 @@ namespace tt {
 
 namespace {
 
-constexpr int kMutThreads = 1024;
+constexpr int kMutThreads = 512;
+constexpr int kSegs = 128;  // offset-chain segments (stitched by one thread)
+constexpr int kMaxCols = 4 * 4 + 3 * 3 + 1;  // 4 spatial x 4 + 3 reduction x 3 + unroll
 
-__device__ __forceinline__ int64_t upper_bound_d(const double* cum, int64_t n, double r) {
-  int64_t lo = 0, hi = n;
+// clock64 marks of thread 0 at the phase boundaries (ttdbg_mutate_clocks)
+__device__ long long g_clk_mut[8];
+#define MUT_MARK(i)                          \
+  do {                                       \
+    if (tid == 0) g_clk_mut[i] = clock64(); \
+  } while (0)
+
+__device__ __forceinline__ int upper_bound_d(const double* cum, int n, double r) {
+  int lo = 0, hi = n;
   while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
+    const int mid = (lo + hi) >> 1;
     if (cum[mid] > r) hi = mid; else lo = mid + 1;
   }
   return lo < n - 1 ? lo : n - 1;
@@ -43,17 +53,19 @@ __device__ __forceinline__ int slot_col0(const DevSketch& S, int slot) {
   return slot < S.n_sp ? 4 * slot : 4 * S.n_sp + 3 * (slot - S.n_sp);
 }
 
-// Moves of factor tuple f (positions 0..arity-1) in the reference's order:
-// position ascending, prime ascending, repeated by multiplicity
-// (schedule.cpp:377-381). Returns the count; if `pick` >= 0 also returns the
-// pick-th move's (position, prime).
-__device__ __forceinline__ int moves_of(const DevSketch& S, int slot, const uint32_t* f, int arity, int pick,
-                                        int* pos, int64_t* prime) {
+// The m-th move of factor tuple f (positions 0..arity-1) in the reference's
+// order: position ascending, prime ascending, repeated by multiplicity
+// (schedule.cpp:377-381). Only the axis' own primes (t0 .. t0+np-1 of the
+// sketch's prime table) can divide its factors. The move count itself is
+// Omega(extent) — the factors multiply to the extent — so it needs no pass.
+__device__ __forceinline__ void pick_move(const DevSketch& S, int t0, int np, const uint32_t (&f)[4], int arity,
+                                          int m, int* pos, int32_t* prime) {
   int cnt = 0;
-  for (int q = 0; q < arity; ++q) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q >= arity) break;
     uint32_t v = f[q];
-    for (int t = 0; t < S.n_prime && v > 1; ++t) {
-      if (S.pr_axis[t] != slot) continue;
+    for (int t = t0; t < t0 + np && v > 1; ++t) {
       int e = 0;
       if (S.pr_p[t] == 2) {
         e = __ffs(v) - 1;
@@ -61,33 +73,126 @@ __device__ __forceinline__ int moves_of(const DevSketch& S, int slot, const uint
       } else {
         for (uint32_t qv = v * S.pr_inv[t]; qv <= S.pr_lim[t]; qv = v * S.pr_inv[t]) v = qv, ++e;
       }
-      if (pick >= cnt && pick < cnt + e) *pos = q, *prime = S.pr_p[t];
+      if (m >= cnt && m < cnt + e) {
+        *pos = q, *prime = (int32_t)S.pr_p[t];
+        return;
+      }
       cnt += e;
     }
   }
-  return cnt;
 }
 
-__global__ void __launch_bounds__(kMutThreads) k_mutate(DevSketch S, const int32_t* __restrict__ pop,
-                                                        const double* __restrict__ cost, int n,
-                                                        uint64_t* __restrict__ state, int32_t* __restrict__ next) {
+__device__ __forceinline__ void named_barrier(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// the arity factors of `slot` of population member `par` (SoA, ld n)
+__device__ __forceinline__ void load_slot(const int32_t* __restrict__ pop, int n, int c0, int arity, int par,
+                                          uint32_t (&f)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) f[q] = q < arity ? (uint32_t)__ldg(pop + (size_t)(c0 + q) * n + par) : 1u;
+}
+
+struct GenDev {
+  int32_t* soa;  // [cols][n]
+  double* cost;
+  uint64_t* id;
+};
+struct GenOut {  // pinned host slots: generation g at base + g * stride
+  char* base;
+  size_t stride, cost_off;
+};
+
+// every thread's host writes, then one system-scope flag per generation
+__device__ __forceinline__ void publish(volatile uint32_t* flags, int g) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) flags[g] = 1u;
+}
+
+// Writes generation g's member j (factors, cost, identity) to the device
+// slot it lives in and to its pinned host mirror.
+template <int NSP, int NRED>
+__device__ __forceinline__ void emit(const GenOut& h, int g, int n, const GenDev& d, int j, const Factors<NSP, NRED>& F,
+                                     double c, uint64_t id, bool write_dev_soa) {
+  constexpr int kN = Factors<NSP, NRED>::kN;
+  char* hb = h.base + (size_t)g * h.stride;
+  int32_t* hs = (int32_t*)hb;
+  double* hc = (double*)(hb + h.cost_off);
+  uint64_t* hi = (uint64_t*)(hc + n);
+#pragma unroll
+  for (int q = 0; q < kN; ++q) {
+    if (write_dev_soa) d.soa[(size_t)q * n + j] = F.f[q];
+    hs[(size_t)q * n + j] = F.f[q];
+  }
+  if (write_dev_soa) d.soa[(size_t)kN * n + j] = F.unroll;
+  hs[(size_t)kN * n + j] = F.unroll;
+  d.cost[j] = c, d.id[j] = id;
+  hc[j] = c, hi[j] = id;
+}
+
+// All generations of one explore in one CTA: generation 0 is the random_init
+// population already in slot 0 (k_generate); generation g >= 1 is
+// mutate(generation g-1) written into slot g & 1. Every member's draft cost
+// and identity are computed by the thread that produced it, and each
+// generation is published to pinned host memory followed by a system-scope
+// flag, so the host folds it into the pool while the device moves on.
+template <int NSP, int NRED>
+__global__ void __launch_bounds__(kMutThreads, 1)
+    k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenDev d0, GenDev d1, uint64_t s_init,
+                   GenOut h, volatile uint32_t* flags) {
+  constexpr int kN = Factors<NSP, NRED>::kN;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* cum = (double*)smem;                 // [n]
-  int32_t* off = (int32_t*)(cum + n);           // [n] stream offset of child j
-  uint8_t* len = (uint8_t*)(off + n);           // [4n] draws a child starting at o consumes
-  __shared__ uint64_t s_state;
+  double* cum = (double*)smem;        // [n] weights, then their running sums
+  int32_t* off = (int32_t*)(cum + n);  // [n] stream offset of child j
+  uint8_t* len = (uint8_t*)(off + n);  // [4n] draws a child starting at offset o consumes
+  int32_t* seg_exit = (int32_t*)(len + 4 * (size_t)n);  // [kSegs][4]
+  int32_t* seg_cnt = seg_exit + 4 * kSegs;              // [kSegs][4]
+  int32_t* seg_entry = seg_cnt + 4 * kSegs;             // [kSegs]
+  int32_t* seg_base = seg_entry + kSegs;                // [kSegs]
   __shared__ double s_total;
-  __shared__ double s_bc[32];
-  __shared__ int s_bi[32];
+  __shared__ uint64_t s_state;
+  __shared__ int s_t0[TT_MAX_AXES], s_np[TT_MAX_AXES], s_omega[TT_MAX_AXES];
+  __shared__ double s_bc[kMutThreads / 32];
+  __shared__ int s_bi[kMutThreads / 32];
   const int tid = threadIdx.x;
-  if (tid == 0) s_state = *state;
-  // weights 1 / (cost + eps) (schedule.cpp:347-351) and the elite: first argmin
+  const int n_axes = S.n_axes;
+  if (tid < n_axes) {  // each axis' slice of the prime table and Omega(extent)
+    int t0 = 0, np = 0, om = 0;
+    for (int t = S.n_prime - 1; t >= 0; --t)
+      if (S.pr_axis[t] == tid) t0 = t, ++np, om += S.pr_e[t];
+    s_t0[tid] = t0, s_np[tid] = np, s_omega[tid] = om;
+  }
+  // generation 0: cost the random_init population
+  for (int j = tid; j < n; j += kMutThreads) {
+    Factors<NSP, NRED> F;
+    load_factors<NSP, NRED>(d0.soa, n, j, F, true);
+    emit<NSP, NRED>(h, 0, n, d0, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), d0.id[j], false);
+  }
+  publish(flags, 0);
+  uint64_t s0 = s_init;
+  const int n_off = 4 * (n - 1);  // child n-1 starts at offset <= 4(n-2)
+  for (int g = 1; g < n_steps; ++g) {
+  const GenDev prev = (g & 1) ? d0 : d1;
+  GenDev cur = (g & 1) ? d1 : d0;
+  const int32_t* __restrict__ pop = prev.soa;
+  const double* __restrict__ cost = prev.cost;
+  if (g == 1) MUT_MARK(0);
+  // A. weights 1 / (cost + eps) (schedule.cpp:347-351), the elite (first
+  // argmin, :360-362) and the draw count of a child starting at every offset.
+  // A child consumes parent + slot draws, then 1 (unroll) or, for an axis
+  // slot, 2 more iff it has a movable prime — and the slot's factors multiply
+  // to the axis extent, so that is "extent > 1", independent of the parent.
   double bc = __longlong_as_double(0x7ff0000000000000LL);
   int bi = n;
   for (int i = tid; i < n; i += kMutThreads) {
     const double c = cost[i];
     cum[i] = 1.0 / __dadd_rn(c, 1e-12);
     if (c < bc) bc = c, bi = i;
+  }
+  for (int o = tid; o < n_off; o += kMutThreads) {
+    const int slot = (int)uniform_index(draw(s0, (uint64_t)o + 1), (uint64_t)n_axes + 1);
+    len[o] = (uint8_t)(slot == n_axes ? 3 : (S.extent[slot] > 1 && S.arity[slot] > 1 ? 4 : 2));
   }
   for (int o = 16; o; o >>= 1) {
     const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
@@ -96,17 +201,28 @@ __global__ void __launch_bounds__(kMutThreads) k_mutate(DevSketch S, const int32
   }
   if ((tid & 31) == 0) s_bc[tid >> 5] = bc, s_bi[tid >> 5] = bi;
   __syncthreads();
+  if (g == 1) MUT_MARK(1);
+  // B. warp 0: the elite, then the running total in the reference's order
+  // (one dependent DADD chain, operands staged through registers).
+  // Meanwhile the other warps build the chain of child start offsets
+  // o_1 = 0, o_{j+1} = o_j + len[o_j]: segment s covers offsets
+  // [s*W, (s+1)*W) and the chain enters it at one of its first 4 offsets
+  // (len <= 4), so each segment is walked from all 4 entries (exit, child
+  // count), one thread stitches the true entries, and every segment is
+  // re-walked from its entry to write the offsets.
+  // segment count balancing the walks (~5W/3 steps) against the stitch (segs steps)
+  const int segs = min(kSegs, max(1, (int)sqrtf(1.67f * (float)n_off)));
+  const int W = (n_off + segs - 1) / segs;
   if (tid < 32) {
-    bc = s_bc[tid], bi = s_bi[tid];
+    bc = tid < kMutThreads / 32 ? s_bc[tid] : __longlong_as_double(0x7ff0000000000000LL);
+    bi = tid < kMutThreads / 32 ? s_bi[tid] : n;
     for (int o = 16; o; o >>= 1) {
       const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
     }
-    if (tid == 0) s_bi[0] = bi;
-    // the running total in the reference's order: one dependent DADD chain,
-    // operands staged through registers 16 at a time
     if (tid == 0) {
+      s_bi[0] = bi;
       double t = 0.0;
       int i = 0;
       for (; i + 16 <= n; i += 16) {
@@ -121,62 +237,70 @@ __global__ void __launch_bounds__(kMutThreads) k_mutate(DevSketch S, const int32
       for (; i < n; ++i) t = __dadd_rn(t, cum[i]), cum[i] = t;
       s_total = t;
     }
-  }
-  __syncthreads();
-  const uint64_t s0 = s_state;
-  const double total = s_total;
-  const int n_axes = S.n_axes;
-  // 1. draw count of a child starting at every offset the chain can reach
-  const int n_off = 4 * (n - 1);
-  for (int o = tid; o < n_off; o += kMutThreads) {
-    const double r = __dmul_rn((double)(draw(s0, (uint64_t)o) >> 11) * 0x1.0p-53, total);
-    const int64_t par = upper_bound_d(cum, n, r);
-    const int slot = (int)uniform_index(draw(s0, (uint64_t)o + 1), (uint64_t)n_axes + 1);
-    int L = 3;
-    if (slot != n_axes) {
-      const int c0 = slot_col0(S, slot), arity = S.arity[slot];
-      uint32_t f[4];
-      for (int q = 0; q < arity; ++q) f[q] = (uint32_t)pop[(int64_t)(c0 + q) * n + par];
-      int pos;
-      int64_t prime;
-      L = moves_of(S, slot, f, arity, -1, &pos, &prime) > 0 && arity > 1 ? 4 : 2;
+  } else {
+    // warps 1..: the offset chain, synchronised among themselves only, so
+    // it runs under warp 0's DADD chain
+    const int sg = tid - 32;
+    if (sg < segs) {
+      const int lo = sg * W, hi = min(lo + W, n_off);
+      for (int e = 0; e < 4; ++e) {
+        int o = lo + e, c = 0;
+        while (o < hi) o += len[o], ++c;
+        seg_exit[sg * 4 + e] = o, seg_cnt[sg * 4 + e] = c;
+      }
     }
-    len[o] = (uint8_t)L;
+    named_barrier(1, kMutThreads - 32);
+    // stitch: the true entry offset and first child of every segment
+    if (sg == 0) {
+      int o = 0, j = 1;
+      for (int g = 0; g < segs; ++g) {
+        seg_entry[g] = o, seg_base[g] = j;
+        const int lo = g * W;
+        if (o < lo + W && lo < n_off) {
+          const int e = o - lo;
+          j += seg_cnt[g * 4 + e];
+          o = seg_exit[g * 4 + e];
+        }
+      }
+    }
+    named_barrier(1, kMutThreads - 32);
+    // every segment re-walked from its entry to place its children's offsets
+    if (sg < segs) {
+      const int hi = min(sg * W + W, n_off);
+      int o = seg_entry[sg], j = seg_base[sg];
+      while (o < hi && j < n) off[j] = o, o += len[o], ++j;
+    }
   }
   __syncthreads();
-  // 2. the chain of child start offsets
+  if (g == 1) MUT_MARK(2);
+  if (g == 1) MUT_MARK(3);
   if (tid == 0) {
-    int o = 0;
-    for (int j = 1; j < n; ++j) {
-      off[j] = o;
-      o += len[o];
-    }
-    *state = s0 + (uint64_t)o * kGolden;  // RngStream state after mutate()
+    const int last = off[n - 1];
+    s_state = s0 + (uint64_t)(last + len[last]) * kGolden;  // RngStream state after mutate()
   }
-  __syncthreads();
-  // 3. children: elite at 0 (schedule.cpp:368), the rest from their draws
-  const int cols = S.cols, ucol = 4 * S.n_sp + 3 * S.n_red;
+  // D. children: elite at 0 (schedule.cpp:368), the rest from their draws
+  const double total = s_total;
   const int best = s_bi[0];
   for (int j = tid; j < n; j += kMutThreads) {
-    int64_t par = best;
+    int par = best;
     int slot = -1, from = 0, to = 0, c0 = 0;
-    int64_t prime = 1, unroll = 0;
+    int32_t prime = 1, unroll = 0;
     if (j > 0) {
       const uint64_t o = (uint64_t)off[j];
       const double r = __dmul_rn((double)(draw(s0, o) >> 11) * 0x1.0p-53, total);
       par = upper_bound_d(cum, n, r);
       slot = (int)uniform_index(draw(s0, o + 1), (uint64_t)n_axes + 1);
       if (slot == n_axes) {
-        unroll = S.unroll[uniform_index(draw(s0, o + 2), (uint64_t)S.n_unroll)];
+        unroll = (int32_t)S.unroll[uniform_index(draw(s0, o + 2), (uint64_t)S.n_unroll)];
       } else {
         c0 = slot_col0(S, slot);
         const int arity = S.arity[slot];
-        uint32_t f[4];
-        for (int q = 0; q < arity; ++q) f[q] = (uint32_t)pop[(int64_t)(c0 + q) * n + par];
-        const int nm = moves_of(S, slot, f, arity, -1, &from, &prime);
+        const int nm = s_omega[slot];
         if (nm > 0 && arity > 1) {
+          uint32_t f[4];
+          load_slot(pop, n, c0, arity, par, f);
           const int m = (int)uniform_index(draw(s0, o + 2), (uint64_t)nm);
-          moves_of(S, slot, f, arity, m, &from, &prime);
+          pick_move(S, s_t0[slot], s_np[slot], f, arity, m, &from, &prime);
           to = (int)uniform_index(draw(s0, o + 3), (uint64_t)arity - 1);
           if (to >= from) ++to;
         } else {
@@ -184,33 +308,52 @@ __global__ void __launch_bounds__(kMutThreads) k_mutate(DevSketch S, const int32
         }
       }
     }
-    for (int c = 0; c < cols; ++c) {
-      int64_t v = pop[(int64_t)c * n + par];
-      if (slot == n_axes && c == ucol) v = unroll;
-      if (slot >= 0 && slot < n_axes) {
-        if (c == c0 + from) v /= prime;
-        if (c == c0 + to) v *= prime;
-      }
-      next[(int64_t)c * n + j] = (int32_t)v;
+    const bool mv = slot >= 0 && slot < n_axes;
+    const int c_from = mv ? c0 + from : -1, c_to = mv ? c0 + to : -1, c_un = slot == n_axes ? kN : -1;
+    // all columns loaded before any store: one L2 round trip per child
+    Factors<NSP, NRED> F;
+    load_factors<NSP, NRED>(pop, n, par, F, true);
+    if (c_un == kN) F.unroll = unroll;
+#pragma unroll
+    for (int q = 0; q < kN; ++q) {
+      if (q == c_from) F.f[q] /= prime;
+      if (q == c_to) F.f[q] *= prime;
     }
+    emit<NSP, NRED>(h, g, n, cur, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), identity_of<NSP, NRED>(S, F),
+                    true);
+  }
+  if (g == 1) MUT_MARK(4);
+  publish(flags, g);
+  s0 = s_state;
   }
 }
 
 }  // namespace
 
-size_t mutate_smem_bytes(int64_t n) { return (size_t)n * 8 + (size_t)n * 4 + (size_t)n * 4 + 16; }
+size_t mutate_smem_bytes(int64_t n) { return (size_t)n * 16 + (size_t)kSegs * 10 * 4 + 16; }
 
-int launch_mutate(const DevSketch& S, const int32_t* pop, const double* cost, int64_t n, uint64_t* state,
-                  int32_t* next, cudaStream_t st) {
+int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int64_t n, int n_steps,
+                        int32_t* soa0, double* cost0, uint64_t* id0, int32_t* soa1, double* cost1, uint64_t* id1,
+                        uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
+                        volatile uint32_t* flags, cudaStream_t st) {
   if (n < 2 || n > kMutateMaxN) return 1;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_mutate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mutate_smem_bytes(kMutateMaxN));
-    init = true;
-  }
-  tt::note_launch();
-  k_mutate<<<1, kMutThreads, mutate_smem_bytes(n), st>>>(S, pop, cost, (int)n, state, next);
-  return 0;
+  GenDev d0{soa0, cost0, id0}, d1{soa1, cost1, id1};
+  GenOut h{(char*)host_base, host_stride, host_cost_off};
+  const size_t sm = mutate_smem_bytes(n);
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_explore_gens<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)mutate_smem_bytes(kMutateMaxN));
+      init = true;
+    }
+    tt::note_launch();
+    k_explore_gens<NSP, NRED><<<1, kMutThreads, sm, st>>>(S, D, toggles, (int)n, n_steps, d0, d1, s_init, h, flags);
+  }));
 }
 
 }  // namespace tt
+
+extern "C" int ttdbg_mutate_clocks(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_clk_mut, sizeof(long long) * (n < 8 ? n : 8));
+}

@@ -1496,7 +1496,8 @@ GenSlot gen_slot(void* base, int64_t n, int cols, int which) {
 }
 
 int ensure_explore(tt_ctx* ctx, int64_t n, int cols, int host_slots) {
-  const size_t dwant = 2 * gen_bytes(n, cols) + 16, hwant = (size_t)host_slots * gen_bytes(n, cols) + 16;
+  const size_t dwant = 2 * gen_bytes(n, cols) + 16;
+  const size_t hwant = (size_t)host_slots * gen_bytes(n, cols) + 4 * (size_t)host_slots + 16;  // + flags
   if (dwant > ctx->ex_dcap) {
     cudaFree(ctx->d_ex);
     ctx->d_ex = nullptr, ctx->ex_dcap = 0;
@@ -1607,8 +1608,7 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   const int host_slots = on_device ? n_steps : 2;
   if ((rc = ensure_explore(ctx, n, cols, host_slots))) return rc;
   GenSlot dgen[2] = {gen_slot(ctx->d_ex, n, cols, 0), gen_slot(ctx->d_ex, n, cols, 1)};
-  uint64_t* d_state = (uint64_t*)((char*)ctx->d_ex + 2 * gen_bytes(n, cols));
-  uint64_t* h_state = (uint64_t*)((char*)ctx->h_ex + (size_t)host_slots * gen_bytes(n, cols));
+  volatile uint32_t* h_flags = (volatile uint32_t*)((char*)ctx->h_ex + (size_t)host_slots * gen_bytes(n, cols));
   auto hgen = [&](int i) { return gen_slot(ctx->h_ex, n, cols, i); };
   const uint64_t s0 = seed_state(seed);
   // random_init(sketch, n, rng) consumes n * draws_per_schedule draws of the
@@ -1683,26 +1683,26 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   };
 
   if (on_device) {
-    // every generation enqueued back to back: mutate -> identities -> draft
-    // costs -> one copy of the slot to its pinned mirror; the host folds
-    // generation g into the pool as soon as its event fires
-    *h_state = s_init;
-    TT_CUDA(ctx, cudaMemcpyAsync(d_state, h_state, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    // one persistent CTA runs every generation (mutate -> identity -> draft
+    // cost) and publishes each to its pinned slot + flag; the host folds
+    // generation g into the pool as soon as its flag is up
+    for (int g = 0; g < n_steps; ++g) h_flags[g] = 0u;
+    if (launch_explore_gens(S, D, toggles, n, n_steps, dgen[0].soa, dgen[0].cost, dgen[0].id, dgen[1].soa,
+                            dgen[1].cost, dgen[1].id, s_init, ctx->h_ex, gen_bytes(n, cols),
+                            (size_t)((char*)hgen(0).cost - (char*)ctx->h_ex), h_flags, st))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    TT_LAUNCHED(ctx);
     for (int g = 0; g < n_steps; ++g) {
-      GenSlot& d = dgen[g & 1];
-      if (g > 0) {
-        GenSlot& prev = dgen[(g - 1) & 1];
-        if (launch_mutate(S, prev.soa, prev.cost, n, d_state, d.soa, st))
-          return fail(ctx, TT_E_STATE, "explore: mutate launch");
-        TT_LAUNCHED(ctx);
-        if (launch_identity(S, d.soa, n, n, d.id, st)) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
-        TT_LAUNCHED(ctx);
+      for (uint64_t spin = 0; h_flags[g] == 0u; ++spin) {
+        if ((spin & 1023) == 1023) {  // a faulted or finished kernel never raises the flag
+          const cudaError_t q = cudaStreamQuery(st);
+          if (q != cudaErrorNotReady && h_flags[g] == 0u) {
+            if (q != cudaSuccess) return fail(ctx, TT_E_CUDA, cudaGetErrorString(q));
+            return fail(ctx, TT_E_STATE, "explore: generation kernel ended without publishing");
+          }
+        }
       }
-      GenSlot h = hgen(g);
-      if ((rc = cost_and_copy(d, h, ctx->ex_ev[g]))) return rc;
-    }
-    for (int g = 0; g < n_steps; ++g) {
-      TT_CUDA(ctx, cudaEventSynchronize(ctx->ex_ev[g]));
+      std::atomic_thread_fence(std::memory_order_acquire);
       consume(hgen(g));
     }
     if ((rc = sync_check(ctx))) return rc;

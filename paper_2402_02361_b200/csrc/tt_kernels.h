@@ -85,11 +85,16 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
                   int64_t first, bool seeded, int64_t n, int64_t k, int64_t need, int toggles,
                   int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
                   int64_t* out_count, cudaStream_t st, bool hash = false);
-// k_explore.cu: one GA generation, mutate() bit-exact, one CTA (n <= kMutateMaxN).
-// state: the RngStream state (device), advanced past the generation's draws.
+// k_explore.cu: all GA generations of one explore in one persistent CTA
+// (n <= kMutateMaxN): generation 0 = slot 0 as generated (soa + identity),
+// then mutate() bit-exact from RNG state s_init; generation g is written to
+// device slot g & 1 and to pinned host memory at host_base + g * host_stride
+// (soa | cost at host_cost_off | identity), then flags[g] = 1.
 constexpr int64_t kMutateMaxN = 8192;
-int launch_mutate(const DevSketch& S, const int32_t* pop, const double* cost, int64_t n, uint64_t* state,
-                  int32_t* next, cudaStream_t st);
+int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int64_t n, int n_steps,
+                        int32_t* soa0, double* cost0, uint64_t* id0, int32_t* soa1, double* cost1, uint64_t* id1,
+                        uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
+                        volatile uint32_t* flags, cudaStream_t st);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);
 // identities of the drafted set (side stream)
