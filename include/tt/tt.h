@@ -117,6 +117,16 @@ int tt_explore1(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
 int tt_explore(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, int n_steps, int64_t k, int64_t n,
                uint64_t seed, int toggles, int32_t* soa_host, double* cost_host, uint64_t* identity_host,
                int64_t* count_host, uint64_t* evaluations);
+/* The tuner's per-round draft set (Tuner::build_draft_set, tuner.cpp:294-323):
+ * explore(n_steps, n_spec = max(1, llround((1 - random_mix) * draft_size)),
+ * pop_size, RngStream(explore_seed)) followed by the draft_size - n_spec
+ * schedules of random_init(., RngStream(mix_seed)) not already in the set,
+ * in that order. HOST outputs (capacity draft_size): identities and draft
+ * costs; *count_host = set size. Score it with tt_pacm_score and pick with
+ * tt_select_top (tuner.cpp:361-396). Synchronous. */
+int tt_draft_set(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, int n_steps, int64_t draft_size,
+                 int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int toggles,
+                 uint64_t* identity_host, double* cost_host, int64_t* count_host, uint64_t* evaluations);
 /* Merge R rank-local top-k lists (C1's consumer): m entries of (cost,
  * global index, identity), global index < 0 = empty slot. Same semantics as
  * one explore over the union. Synchronous. */

@@ -68,6 +68,8 @@ struct tt_ctx {
   void* d_ex = nullptr;  // two device generation slots + the RNG state
   void* h_ex = nullptr;  // pinned generation slots: soa | cost | identity
   std::vector<cudaEvent_t> ex_ev;  // one per generation in flight
+  void* d_mix = nullptr;           // random-mix schedules of a draft set: soa | cost | identity
+  size_t mix_cap = 0;
   // last async round
   int64_t last_b = 0;
   int64_t last_k = 0;
@@ -522,7 +524,7 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
-                  c->d_tiles, c->d_ex};
+                  c->d_tiles, c->d_ex, c->d_mix};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_record) cudaFreeHost(c->h_record);
@@ -1743,5 +1745,57 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   }
   *count_host = cnt;
   if (evaluations) *evaluations = (uint64_t)n_steps * (uint64_t)n;
+  return TT_OK;
+}
+
+// The tuner's draft set (Tuner::build_draft_set, tuner.cpp:294-323): the
+// explore() pool of n_spec = max(1, llround((1 - random_mix) * draft_size))
+// schedules, then draft_size - n_spec fresh random_init schedules of the mix
+// stream, each appended (with its draft cost) unless its key was seen.
+int tt_draft_set(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t draft_size,
+                 int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int toggles,
+                 uint64_t* id_host, double* cost_host, int64_t* count_host, uint64_t* evaluations) {
+  if (!ctx) return TT_E_STATE;
+  if (!(random_mix >= 0.0 && random_mix < 1.0)) return fail(ctx, TT_E_CONFIG, "random_mix must be in [0, 1)");
+  if (draft_size < 1) return fail(ctx, TT_E_CONFIG, "draft_size must be >= 1");
+  if (!id_host || !cost_host || !count_host) return fail(ctx, TT_E_STATE, "draft_set: null output");
+  const int64_t n_spec = std::max<int64_t>(1, std::llround((1.0 - random_mix) * (double)draft_size));
+  const int64_t n_random = draft_size - n_spec;
+  int64_t cnt = 0;
+  int rc = tt_explore(ctx, sk, dev, n_steps, n_spec, pop_size, explore_seed, toggles, nullptr, cost_host, id_host,
+                      &cnt, evaluations);
+  if (rc) return rc;
+  if (n_random > 0) {
+    DevSketch S;
+    DevDevice D;
+    if ((rc = compile_sketch(ctx, sk, S))) return rc;
+    if ((rc = compile_device(ctx, dev, D))) return rc;
+    const size_t want = gen_bytes(n_random, S.cols);
+    if (want > ctx->mix_cap) {
+      cudaFree(ctx->d_mix);
+      ctx->d_mix = nullptr, ctx->mix_cap = 0;
+      TT_CUDA(ctx, cudaMalloc(&ctx->d_mix, want));
+      ctx->mix_cap = want;
+    }
+    GenSlot m = gen_slot(ctx->d_mix, n_random, S.cols, 0);
+    if (launch_generate(S, seed_state(mix_seed), 0, n_random, m.soa, n_random, m.id, ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    TT_LAUNCHED(ctx);
+    if (launch_draft_cost(S, D, m.soa, n_random, 0, 0, false, n_random, toggles, m.cost, nullptr, ctx->sel.invalid,
+                          ctx->stream))
+      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    TT_LAUNCHED(ctx);
+    std::vector<double> mc((size_t)n_random);
+    std::vector<uint64_t> mi((size_t)n_random);
+    TT_CUDA(ctx, cudaMemcpyAsync(mc.data(), m.cost, sizeof(double) * n_random, cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(ctx, cudaMemcpyAsync(mi.data(), m.id, sizeof(uint64_t) * n_random, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((rc = sync_check(ctx))) return rc;
+    std::unordered_map<uint64_t, int> seen;
+    seen.reserve((size_t)(cnt + n_random) * 2);
+    for (int64_t i = 0; i < cnt; ++i) seen.emplace(id_host[i], 0);
+    for (int64_t i = 0; i < n_random; ++i)
+      if (seen.emplace(mi[(size_t)i], 0).second) id_host[cnt] = mi[(size_t)i], cost_host[cnt++] = mc[(size_t)i];
+  }
+  *count_host = cnt;
   return TT_OK;
 }

@@ -175,6 +175,21 @@ def explore(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft_s
     return np.ascontiguousarray(soa[:, :m]), cost[:m], ids[:m], ev.value
 
 
+def draft_set(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft_size: int, pop_size: int,
+              random_mix: float, explore_seed: int, mix_seed: int, toggles: int = TT_TOGGLES_ALL):
+    """Tuner::build_draft_set (tuner.cpp:294-323): the GA explore pool of
+    n_spec schedules then the unseen random-mix schedules. Returns host numpy
+    (identity uint64 [count], draft cost [count], evaluations)."""
+    ids = np.zeros(draft_size, np.uint64)
+    cost = np.zeros(draft_size, np.float64)
+    cnt, ev = C.c_int64(0), C.c_uint64(0)
+    ctx.check(lib().tt_draft_set(ctx.h, C.byref(sketch), C.byref(dev), n_steps, draft_size, pop_size, random_mix,
+                                 explore_seed & (2**64 - 1), mix_seed & (2**64 - 1), toggles, ids.ctypes.data,
+                                 cost.ctypes.data, C.byref(cnt), C.byref(ev)))
+    m = cnt.value
+    return ids[:m], cost[:m], ev.value
+
+
 def topk_merge(ctx: Context, cost: torch.Tensor, gidx: torch.Tensor, ids: torch.Tensor, k: int):
     idx, c, i = _topk_out(ctx, k)
     cnt = C.c_int64(0)
