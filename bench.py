@@ -294,6 +294,7 @@ def run_ours(args, rank, world, local_rank):
         stage_ms = {s: v[0] / max(v[1], 1) for s, v in (prof or {}).items()}
         roof = roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec)
         cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+        ga = explore_ga(args, ctx, dev, sketches, names) if world == 1 else None
         result = {
             "metric": METRIC, "value": cands / tot, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
@@ -322,6 +323,7 @@ def run_ours(args, rank, world, local_rank):
                 "value": cands / conc, "unit": UNIT,
                 "note": "the step's 7 subgraph rounds on 7 contexts/streams at once (independent tasks, "
                         "fixed weights); the headline `value` runs them one after another"},
+            "explore_ga": ga,
             "gpu_launches": launches,
             "stage_ms_per_round": stage_ms,
             "roofline": roof,
@@ -384,6 +386,33 @@ def roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec):
     res = dict(out[dom])
     res["others"] = {k: v for k, v in out.items() if k != dom}
     return res
+
+
+def explore_ga(args, ctx, dev, sketches, names, reps=5):
+    """the tuner's real explore — the LSE genetic loop at
+    TunerConfig defaults (n_steps 32, pop_size 512, draft_size 512) — through
+    tt_explore (host call, results on the host), beside the reference's own
+    explore() (oracle/_ref, all host threads) on the same seeds."""
+    R = None if args.no_cpu else _ref_setup(args)
+    threads = os.cpu_count() or 1
+    rows = {}
+    for name, sk in list(zip(names, sketches))[:2]:
+        tt.explore(ctx, sk, dev, 32, 512, 512, 1)
+        t0 = time.perf_counter()
+        for r in range(reps):
+            _, cost, _, ev = tt.explore(ctx, sk, dev, 32, 512, 512, 1000 + r)
+        g = (time.perf_counter() - t0) / reps
+        row = {"ms_per_explore": 1e3 * g, "evaluations_per_s": ev / g}
+        if R is not None and R.ref_available():
+            t0 = time.perf_counter()
+            for r in range(3):
+                _, rc = R.R_explore(sk, dev, 512, 512, 1000 + r, n_steps=32, threads=threads)
+            c = (time.perf_counter() - t0) / 3
+            row.update({"reference_ms_per_explore": 1e3 * c, "reference_threads": threads,
+                        "identical_last_seed": bool(len(rc) == len(cost) and (rc == cost).all())})
+        rows[name] = row
+    return {"config": "explore(op, dev, n_steps=32, draft_size=512, pop_size=512): TunerConfig defaults "
+                      "(tuner.hpp:38-40); wall clock of the host call", "subgraphs": rows}
 
 
 # ------------------------------------------------------------------------------------ reference --
