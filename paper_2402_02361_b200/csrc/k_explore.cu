@@ -103,11 +103,15 @@ struct GenOut {  // pinned host slots: generation g at base + g * stride
   size_t stride, cost_off;
 };
 
-// every thread's host writes, then one system-scope flag per generation
+// every thread's host writes, then one system-scope flag per generation:
+// the CTA barrier orders the block's writes before thread 0's fence, and the
+// (cumulative) fence orders them before the flag, as in a grid barrier
 __device__ __forceinline__ void publish(volatile uint32_t* flags, int g) {
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) flags[g] = 1u;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    flags[g] = 1u;
+  }
 }
 
 // Writes generation g's member j (factors, cost, identity) to the device
