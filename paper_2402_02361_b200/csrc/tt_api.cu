@@ -1629,17 +1629,21 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
     return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
   TT_LAUNCHED(ctx);
 
-  // the pool (draft.cpp:166-170), flat: identity, cost, discovery, factors;
-  // membership by an open-addressing table over identities, cleared in O(1)
-  // per trim by bumping its epoch
+  // the pool (draft.cpp:166-170): (cost, discovery, identity, where its
+  // factors are) entries, trimmed in place with nth_element; membership by an
+  // open-addressing table over identities, cleared in O(1) per trim by
+  // bumping its epoch. On the device path every generation's pinned slot
+  // stays alive, so an entry just points at its column (generation * n +
+  // index); the host path copies factor rows into an arena.
+  struct PE {
+    double cost;
+    uint64_t disc, id, ref;
+  };
   const int64_t cap = k + n;
-  std::vector<uint64_t> p_id((size_t)cap), p_disc((size_t)cap);
-  std::vector<double> p_cost((size_t)cap);
-  std::vector<int32_t> p_f((size_t)(cap * cols));
-  std::vector<uint64_t> t_p_id((size_t)cap), t_p_disc((size_t)cap);
-  std::vector<double> t_p_cost((size_t)cap);
-  std::vector<int32_t> t_p_f((size_t)(cap * cols));
-  std::vector<uint32_t> order((size_t)cap);
+  std::vector<PE> pool;
+  pool.reserve((size_t)cap);
+  std::vector<int32_t> rows, rows_t;  // host path only
+  if (!on_device) rows.resize((size_t)(cap * cols)), rows_t.resize((size_t)(k * cols));
   int hbits = 4;
   while (((int64_t)1 << hbits) < 2 * cap) ++hbits;
   const uint64_t hmask = ((uint64_t)1 << hbits) - 1;
@@ -1655,32 +1659,34 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
       if (h_key[h] == id) return false;
     }
   };
-  int64_t np = 0;
   uint64_t discovery = 0;
-  auto by_cost = [&](uint32_t a, uint32_t b) {
-    return p_cost[a] != p_cost[b] ? p_cost[a] < p_cost[b] : p_disc[a] < p_disc[b];
-  };
+  auto by_cost = [](const PE& a, const PE& b) { return a.cost != b.cost ? a.cost < b.cost : a.disc < b.disc; };
   // pool insertion in population order (first discovery wins,
   // draft.cpp:198-204) + trim to the k smallest (cost, discovery) (:174-191)
-  auto consume = [&](const GenSlot& g) {
+  auto consume = [&](const GenSlot& g, int gen) {
     for (int64_t i = 0; i < n; ++i) {
       if (!h_insert(g.id[i])) continue;
-      p_id[np] = g.id[i], p_cost[np] = g.cost[i], p_disc[np] = discovery++;
-      for (int c = 0; c < cols; ++c) p_f[np * cols + c] = g.soa[(int64_t)c * n + i];
-      ++np;
-    }
-    if (np > k) {
-      for (int64_t q = 0; q < np; ++q) order[q] = (uint32_t)q;
-      std::nth_element(order.begin(), order.begin() + k, order.begin() + np, by_cost);
-      ++epoch;
-      for (int64_t q = 0; q < k; ++q) {
-        const uint32_t o = order[q];
-        t_p_id[q] = p_id[o], t_p_cost[q] = p_cost[o], t_p_disc[q] = p_disc[o];
-        std::memcpy(&t_p_f[q * cols], &p_f[(size_t)o * cols], sizeof(int32_t) * cols);
-        h_insert(p_id[o]);
+      PE e{g.cost[i], discovery++, g.id[i], 0};
+      if (on_device) {
+        e.ref = (uint64_t)gen * (uint64_t)n + (uint64_t)i;
+      } else {
+        e.ref = pool.size();
+        for (int c = 0; c < cols; ++c) rows[e.ref * cols + c] = g.soa[(int64_t)c * n + i];
       }
-      p_id.swap(t_p_id), p_cost.swap(t_p_cost), p_disc.swap(t_p_disc), p_f.swap(t_p_f);
-      np = k;
+      pool.push_back(e);
+    }
+    if ((int64_t)pool.size() > k) {
+      std::nth_element(pool.begin(), pool.begin() + k, pool.end(), by_cost);
+      pool.resize((size_t)k);
+      ++epoch;
+      for (size_t q = 0; q < pool.size(); ++q) {
+        h_insert(pool[q].id);
+        if (!on_device) {
+          std::memcpy(&rows_t[q * cols], &rows[pool[q].ref * cols], sizeof(int32_t) * cols);
+          pool[q].ref = q;
+        }
+      }
+      if (!on_device) std::copy(rows_t.begin(), rows_t.begin() + (size_t)k * cols, rows.begin());
     }
   };
 
@@ -1705,7 +1711,7 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
         }
       }
       std::atomic_thread_fence(std::memory_order_acquire);
-      consume(hgen(g));
+      consume(hgen(g), g);
     }
     if ((rc = sync_check(ctx))) return rc;
   } else {
@@ -1726,22 +1732,28 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
         TT_LAUNCHED(ctx);
         if ((rc = cost_and_copy(dgen[0], nx, ctx->ex_ev[cur ^ 1]))) return rc;
       }
-      consume(g);  // overlaps the device
+      consume(g, step);  // overlaps the device
       if (more) {
         if ((rc = sync_check(ctx))) return rc;
         cur ^= 1;
       }
     }
   }
-  for (int64_t q = 0; q < np; ++q) order[q] = (uint32_t)q;
-  std::sort(order.begin(), order.begin() + np, by_cost);
-  const int64_t cnt = np;
+  std::sort(pool.begin(), pool.end(), by_cost);
+  const int64_t cnt = (int64_t)pool.size();
   for (int64_t q = 0; q < cnt; ++q) {
-    const uint32_t o = order[q];
-    cost_host[q] = p_cost[o];
-    if (id_host) id_host[q] = p_id[o];
-    if (soa_host)
-      for (int c = 0; c < cols; ++c) soa_host[(int64_t)c * k + q] = p_f[(size_t)o * cols + c];
+    const PE& e = pool[(size_t)q];
+    cost_host[q] = e.cost;
+    if (id_host) id_host[q] = e.id;
+    if (soa_host) {
+      if (on_device) {
+        const GenSlot g = hgen((int)(e.ref / (uint64_t)n));
+        const int64_t i = (int64_t)(e.ref % (uint64_t)n);
+        for (int c = 0; c < cols; ++c) soa_host[(int64_t)c * k + q] = g.soa[(int64_t)c * n + i];
+      } else {
+        for (int c = 0; c < cols; ++c) soa_host[(int64_t)c * k + q] = rows[e.ref * cols + c];
+      }
+    }
   }
   *count_host = cnt;
   if (evaluations) *evaluations = (uint64_t)n_steps * (uint64_t)n;
