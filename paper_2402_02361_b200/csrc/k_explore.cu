@@ -18,9 +18,13 @@
 // order (the weights are computed in parallel first), so `total` and every
 // cumulative bound are the reference's bits. Built with --fmad=false.
 //
-// One CTA per generation (n <= kMutateMaxN); the population is tiny (512 at
-// the TunerConfig defaults) and the generation chain is latency bound, so
-// the kernel's job is to remove the host round trip from the GA loop.
+// One persistent thread-block cluster runs every generation (n <=
+// kMutateMaxN): each CTA derives the wheel and the offset chain itself and
+// produces a slice of the children with their draft costs; a child's identity
+// is its parent's with one mixed-radix digit updated. The population is tiny
+// (512 at the TunerConfig defaults) and the generation chain is latency
+// bound, so the kernel's job is to remove every host round trip from the loop.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "tt_kernels.h"
@@ -37,7 +41,7 @@ constexpr int kMaxCols = 4 * 4 + 3 * 3 + 1;  // 4 spatial x 4 + 3 reduction x 3 
 __device__ long long g_clk_mut[8];
 #define MUT_MARK(i)                          \
   do {                                       \
-    if (tid == 0) g_clk_mut[i] = clock64(); \
+    if (tid == 0 && blockIdx.x == 0) g_clk_mut[i] = clock64(); \
   } while (0)
 
 __device__ __forceinline__ int upper_bound_d(const double* cum, int n, double r) {
@@ -58,8 +62,18 @@ __device__ __forceinline__ int slot_col0(const DevSketch& S, int slot) {
 // (schedule.cpp:377-381). Only the axis' own primes (t0 .. t0+np-1 of the
 // sketch's prime table) can divide its factors. The move count itself is
 // Omega(extent) — the factors multiply to the extent — so it needs no pass.
-__device__ __forceinline__ void pick_move(const DevSketch& S, int t0, int np, const uint32_t (&f)[4], int arity,
-                                          int m, int* pos, int32_t* prime) {
+// The sketch's prime table, copied to shared memory once: the apply pass
+// indexes it with per-lane (divergent) indices, which the kernel-parameter
+// bank would serialise.
+struct PrimeTab {
+  int32_t p[TT_MAX_PRIMES], e[TT_MAX_PRIMES];
+  uint32_t inv[TT_MAX_PRIMES], lim[TT_MAX_PRIMES];
+  int32_t arity[TT_MAX_AXES], unroll[TT_MAX_UNROLL];
+  int32_t len[TT_MAX_AXES + 1];  // draws a child consumes by slot
+};
+
+__device__ __forceinline__ void pick_move(const PrimeTab& S, int t0, int np, const uint32_t (&f)[4], int arity,
+                                          int m, int* pos, int32_t* prime, int* tsel) {
   int cnt = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -67,14 +81,14 @@ __device__ __forceinline__ void pick_move(const DevSketch& S, int t0, int np, co
     uint32_t v = f[q];
     for (int t = t0; t < t0 + np && v > 1; ++t) {
       int e = 0;
-      if (S.pr_p[t] == 2) {
+      if (S.p[t] == 2) {
         e = __ffs(v) - 1;
         v >>= e;
       } else {
-        for (uint32_t qv = v * S.pr_inv[t]; qv <= S.pr_lim[t]; qv = v * S.pr_inv[t]) v = qv, ++e;
+        for (uint32_t qv = v * S.inv[t]; qv <= S.lim[t]; qv = v * S.inv[t]) v = qv, ++e;
       }
       if (m >= cnt && m < cnt + e) {
-        *pos = q, *prime = (int32_t)S.pr_p[t];
+        *pos = q, *prime = (int32_t)S.p[t], *tsel = t;
         return;
       }
       cnt += e;
@@ -87,10 +101,39 @@ __device__ __forceinline__ void named_barrier(int id, int threads) {
 }
 
 // the arity factors of `slot` of population member `par` (SoA, ld n)
-__device__ __forceinline__ void load_slot(const int32_t* __restrict__ pop, int n, int c0, int arity, int par,
+__device__ __forceinline__ void load_slot(const int32_t* pop, int n, int c0, int arity, int par,
                                           uint32_t (&f)[4]) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) f[q] = q < arity ? (uint32_t)__ldg(pop + (size_t)(c0 + q) * n + par) : 1u;
+  for (int q = 0; q < 4; ++q) f[q] = q < arity ? (uint32_t)pop[(size_t)(c0 + q) * n + par] : 1u;
+}
+
+// Factors of member i (SoA, ld n). The generation slots are rewritten while
+// the kernel runs (and by other CTAs of the cluster), so reads are ordinary
+// coherent loads (ordered by the cluster barrier's acquire), never the
+// non-coherent read-only path: the pointers are deliberately not
+// const __restrict__.
+template <int NSP, int NRED>
+__device__ __forceinline__ void load_factors_cg(const int32_t* soa, int n, int i, Factors<NSP, NRED>& F) {
+#pragma unroll
+  for (int q = 0; q < Factors<NSP, NRED>::kN; ++q) F.f[q] = soa[(size_t)q * n + i];
+  F.unroll = soa[(size_t)Factors<NSP, NRED>::kN * n + i];
+}
+
+// exponents of prime table entry t in the arity factors f
+__device__ __forceinline__ void exps_of(const PrimeTab& S, int t, const uint32_t (&f)[4], int arity, int (&e)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t v = f[q];
+    int x = 0;
+    if (q < arity) {
+      if (S.p[t] == 2) {
+        x = __ffs(v) - 1;
+      } else {
+        for (uint32_t qv = v * S.inv[t]; qv <= S.lim[t]; qv = v * S.inv[t]) v = qv, ++x;
+      }
+    }
+    e[q] = x;
+  }
 }
 
 struct GenDev {
@@ -135,16 +178,18 @@ __device__ __forceinline__ void emit(const GenOut& h, int g, int n, const GenDev
   hc[j] = c, hi[j] = id;
 }
 
-// All generations of one explore in one CTA: generation 0 is the random_init
+// All generations of one explore in one thread-block cluster (<= 8 CTAs):
+// generation 0 is the random_init
 // population already in slot 0 (k_generate); generation g >= 1 is
 // mutate(generation g-1) written into slot g & 1. Every member's draft cost
-// and identity are computed by the thread that produced it, and each
-// generation is published to pinned host memory followed by a system-scope
-// flag, so the host folds it into the pool while the device moves on.
+// and identity are computed by the thread that produced it, and each CTA's
+// slice of a generation is published to pinned host memory followed by a
+// system-scope flag (flags[g * clusters + rank]), so the host folds the
+// generation into the pool while the device moves on.
 template <int NSP, int NRED>
 __global__ void __launch_bounds__(kMutThreads, 1)
     k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenDev d0, GenDev d1, uint64_t s_init,
-                   GenOut h, volatile uint32_t* flags) {
+                   GenOut h, volatile uint32_t* flags, int staged) {
   constexpr int kN = Factors<NSP, NRED>::kN;
   extern __shared__ __align__(16) unsigned char smem[];
   double* cum = (double*)smem;        // [n] weights, then their running sums
@@ -154,34 +199,64 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   int32_t* seg_cnt = seg_exit + 4 * kSegs;              // [kSegs][4]
   int32_t* seg_entry = seg_cnt + 4 * kSegs;             // [kSegs]
   int32_t* seg_base = seg_entry + kSegs;                // [kSegs]
+  // staged copy of the previous generation (when it fits): parents are read
+  // at random by the apply pass, so they come from shared memory
+  uint64_t* id_s = (uint64_t*)(seg_base + kSegs);  // [n]
+  int32_t* pop_s = (int32_t*)(id_s + n);            // [cols][n]
   __shared__ double s_total;
   __shared__ uint64_t s_state;
   __shared__ int s_t0[TT_MAX_AXES], s_np[TT_MAX_AXES], s_omega[TT_MAX_AXES];
+  __shared__ uint64_t s_w[TT_MAX_PRIMES];  // identity weight of each (axis, prime) digit
+  __shared__ PrimeTab tab;
   __shared__ double s_bc[kMutThreads / 32];
   __shared__ int s_bi[kMutThreads / 32];
   const int tid = threadIdx.x;
   const int n_axes = S.n_axes;
+  // the grid is one thread-block cluster: every CTA derives the generation's
+  // wheel and offset chain itself (identical, deterministic) and produces its
+  // own slice of the children; generations are separated by cluster barriers
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+  const int nc = (int)gridDim.x, cr = (int)blockIdx.x;
+  const int per = (n + nc - 1) / nc, jlo = min(n, cr * per), jhi = min(n, jlo + per);
   if (tid < n_axes) {  // each axis' slice of the prime table and Omega(extent)
     int t0 = 0, np = 0, om = 0;
     for (int t = S.n_prime - 1; t >= 0; --t)
       if (S.pr_axis[t] == tid) t0 = t, ++np, om += S.pr_e[t];
     s_t0[tid] = t0, s_np[tid] = np, s_omega[tid] = om;
   }
+  if (tid < S.n_prime) {
+    tab.p[tid] = (int32_t)S.pr_p[tid], tab.e[tid] = S.pr_e[tid];
+    tab.inv[tid] = S.pr_inv[tid], tab.lim[tid] = S.pr_lim[tid];
+  }
+  if (tid < TT_MAX_AXES) tab.arity[tid] = S.arity[tid];
+  if (tid < TT_MAX_UNROLL) tab.unroll[tid] = (int32_t)S.unroll[tid];
+  if (tid <= n_axes)
+    tab.len[tid] = tid == n_axes ? 3 : (S.extent[tid] > 1 && S.arity[tid] > 1 ? 4 : 2);
+  if (tid == 32) {  // identity = mixed radix (digit per (axis, prime), then the unroll index)
+    uint64_t w = (uint64_t)S.n_unroll;
+    for (int t = S.n_prime - 1; t >= 0; --t) s_w[t] = w, w *= S.pr_count[t];
+  }
   // generation 0: cost the random_init population
-  for (int j = tid; j < n; j += kMutThreads) {
+  for (int j = jlo + tid; j < jhi; j += kMutThreads) {
     Factors<NSP, NRED> F;
-    load_factors<NSP, NRED>(d0.soa, n, j, F, true);
+    load_factors_cg<NSP, NRED>(d0.soa, n, j, F);
     emit<NSP, NRED>(h, 0, n, d0, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), d0.id[j], false);
   }
-  publish(flags, 0);
+  publish(flags, cr);
+  cluster.sync();
   uint64_t s0 = s_init;
   const int n_off = 4 * (n - 1);  // child n-1 starts at offset <= 4(n-2)
   for (int g = 1; g < n_steps; ++g) {
   const GenDev prev = (g & 1) ? d0 : d1;
   GenDev cur = (g & 1) ? d1 : d0;
-  const int32_t* __restrict__ pop = prev.soa;
-  const double* __restrict__ cost = prev.cost;
+  const double* cost = prev.cost;
   if (g == 1) MUT_MARK(0);
+  if (staged) {
+    for (int i = tid; i < (kN + 1) * n; i += kMutThreads) pop_s[i] = prev.soa[i];
+    for (int i = tid; i < n; i += kMutThreads) id_s[i] = prev.id[i];
+  }
+  const int32_t* pop = staged ? pop_s : prev.soa;
+  const uint64_t* pid = staged ? id_s : prev.id;
   // A. weights 1 / (cost + eps) (schedule.cpp:347-351), the elite (first
   // argmin, :360-362) and the draw count of a child starting at every offset.
   // A child consumes parent + slot draws, then 1 (unroll) or, for an axis
@@ -196,7 +271,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   }
   for (int o = tid; o < n_off; o += kMutThreads) {
     const int slot = (int)uniform_index(draw(s0, (uint64_t)o + 1), (uint64_t)n_axes + 1);
-    len[o] = (uint8_t)(slot == n_axes ? 3 : (S.extent[slot] > 1 && S.arity[slot] > 1 ? 4 : 2));
+    len[o] = (uint8_t)tab.len[slot];
   }
   for (int o = 16; o; o >>= 1) {
     const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
@@ -285,26 +360,27 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   // D. children: elite at 0 (schedule.cpp:368), the rest from their draws
   const double total = s_total;
   const int best = s_bi[0];
-  for (int j = tid; j < n; j += kMutThreads) {
+  for (int j = jlo + tid; j < jhi; j += kMutThreads) {
     int par = best;
-    int slot = -1, from = 0, to = 0, c0 = 0;
+    int slot = -1, from = 0, to = 0, c0 = 0, tsel = 0, uidx = 0;
     int32_t prime = 1, unroll = 0;
+    uint32_t f[4] = {1u, 1u, 1u, 1u};
     if (j > 0) {
       const uint64_t o = (uint64_t)off[j];
       const double r = __dmul_rn((double)(draw(s0, o) >> 11) * 0x1.0p-53, total);
       par = upper_bound_d(cum, n, r);
       slot = (int)uniform_index(draw(s0, o + 1), (uint64_t)n_axes + 1);
       if (slot == n_axes) {
-        unroll = (int32_t)S.unroll[uniform_index(draw(s0, o + 2), (uint64_t)S.n_unroll)];
+        uidx = (int)uniform_index(draw(s0, o + 2), (uint64_t)S.n_unroll);
+        unroll = tab.unroll[uidx];
       } else {
         c0 = slot_col0(S, slot);
-        const int arity = S.arity[slot];
+        const int arity = tab.arity[slot];
         const int nm = s_omega[slot];
         if (nm > 0 && arity > 1) {
-          uint32_t f[4];
           load_slot(pop, n, c0, arity, par, f);
           const int m = (int)uniform_index(draw(s0, o + 2), (uint64_t)nm);
-          pick_move(S, s_t0[slot], s_np[slot], f, arity, m, &from, &prime);
+          pick_move(tab, s_t0[slot], s_np[slot], f, arity, m, &from, &prime, &tsel);
           to = (int)uniform_index(draw(s0, o + 3), (uint64_t)arity - 1);
           if (to >= from) ++to;
         } else {
@@ -316,25 +392,49 @@ __global__ void __launch_bounds__(kMutThreads, 1)
     const int c_from = mv ? c0 + from : -1, c_to = mv ? c0 + to : -1, c_un = slot == n_axes ? kN : -1;
     // all columns loaded before any store: one L2 round trip per child
     Factors<NSP, NRED> F;
-    load_factors<NSP, NRED>(pop, n, par, F, true);
+    load_factors_cg<NSP, NRED>(pop, n, par, F);
+    // the child's identity from its parent's: one digit changes (the moved
+    // prime's exponent composition, or the unroll index)
+    uint64_t id_j = pid[par];
+    if (c_un == kN) {
+      int uold = 0;
+      for (int u = 0; u < S.n_unroll; ++u)
+        if (tab.unroll[u] == F.unroll) uold = u;
+      id_j += (uint64_t)uidx - (uint64_t)uold;
+    } else if (mv) {
+      const int arity = tab.arity[slot];
+      int e[4];
+      exps_of(tab, tsel, f, arity, e);
+      const uint64_t d_old = rank_composition(tab.e[tsel], arity, e);
+      e[from] -= 1, e[to] += 1;
+      const uint64_t d_new = rank_composition(tab.e[tsel], arity, e);
+      id_j += (d_new - d_old) * s_w[tsel];
+    }
     if (c_un == kN) F.unroll = unroll;
 #pragma unroll
     for (int q = 0; q < kN; ++q) {
       if (q == c_from) F.f[q] /= prime;
       if (q == c_to) F.f[q] *= prime;
     }
-    emit<NSP, NRED>(h, g, n, cur, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), identity_of<NSP, NRED>(S, F),
-                    true);
+    if (g == 1) MUT_MARK(5);
+    const double c_j = draft_cost_of<NSP, NRED>(S, D, F, toggles);
+    if (g == 1 && c_j > 0) MUT_MARK(6);
+    if (g == 1 && id_j != 1) MUT_MARK(7);
+    emit<NSP, NRED>(h, g, n, cur, j, F, c_j, id_j, true);
   }
   if (g == 1) MUT_MARK(4);
-  publish(flags, g);
+  publish(flags, g * nc + cr);
+  cluster.sync();  // generation g complete in every CTA before anyone reads it
   s0 = s_state;
   }
 }
 
 }  // namespace
 
-size_t mutate_smem_bytes(int64_t n) { return (size_t)n * 16 + (size_t)kSegs * 10 * 4 + 16; }
+size_t mutate_smem_bytes(int64_t n, int cols, bool staged) {
+  return (size_t)n * 16 + (size_t)kSegs * 10 * 4 + (staged ? (size_t)n * (8 + 4 * (size_t)cols) : 0) + 16;
+}
+constexpr size_t kSmemCap = 220 * 1024;
 
 int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int64_t n, int n_steps,
                         int32_t* soa0, double* cost0, uint64_t* id0, int32_t* soa1, double* cost1, uint64_t* id1,
@@ -343,18 +443,30 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
   if (n < 2 || n > kMutateMaxN) return 1;
   GenDev d0{soa0, cost0, id0}, d1{soa1, cost1, id1};
   GenOut h{(char*)host_base, host_stride, host_cost_off};
-  const size_t sm = mutate_smem_bytes(n);
+  const bool staged = mutate_smem_bytes(n, S.cols, true) <= kSmemCap;
+  const size_t sm = mutate_smem_bytes(n, S.cols, staged);
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
     static bool init = false;
     if (!init) {
-      cudaFuncSetAttribute(k_explore_gens<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)mutate_smem_bytes(kMutateMaxN));
+      cudaFuncSetAttribute(k_explore_gens<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
       init = true;
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(explore_cluster_size(n));
+    cfg.blockDim = dim3(kMutThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = explore_cluster_size(n), at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    cfg.attrs = at, cfg.numAttrs = 1;
     tt::note_launch();
-    k_explore_gens<NSP, NRED><<<1, kMutThreads, sm, st>>>(S, D, toggles, (int)n, n_steps, d0, d1, s_init, h, flags);
+    cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, d0, d1, s_init, h, flags,
+                       (int)staged);
   }));
 }
+
+int explore_cluster_size(int64_t n) { return (int)std::min<int64_t>(8, std::max<int64_t>(1, (n + 63) / 64)); }
 
 }  // namespace tt
 

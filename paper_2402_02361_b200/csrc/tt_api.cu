@@ -1497,9 +1497,9 @@ GenSlot gen_slot(void* base, int64_t n, int cols, int which) {
   return g;
 }
 
-int ensure_explore(tt_ctx* ctx, int64_t n, int cols, int host_slots) {
+int ensure_explore(tt_ctx* ctx, int64_t n, int cols, int host_slots, int nflag) {
   const size_t dwant = 2 * gen_bytes(n, cols) + 16;
-  const size_t hwant = (size_t)host_slots * gen_bytes(n, cols) + 4 * (size_t)host_slots + 16;  // + flags
+  const size_t hwant = (size_t)host_slots * gen_bytes(n, cols) + 4 * (size_t)host_slots * nflag + 16;  // + flags
   if (dwant > ctx->ex_dcap) {
     cudaFree(ctx->d_ex);
     ctx->d_ex = nullptr, ctx->ex_dcap = 0;
@@ -1608,7 +1608,8 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   // device generations.
   const bool on_device = n <= kMutateMaxN && (size_t)n_steps * gen_bytes(n, cols) <= ((size_t)1 << 30);
   const int host_slots = on_device ? n_steps : 2;
-  if ((rc = ensure_explore(ctx, n, cols, host_slots))) return rc;
+  const int nflag = on_device ? explore_cluster_size(n) : 1;  // flags per generation
+  if ((rc = ensure_explore(ctx, n, cols, host_slots, nflag))) return rc;
   GenSlot dgen[2] = {gen_slot(ctx->d_ex, n, cols, 0), gen_slot(ctx->d_ex, n, cols, 1)};
   volatile uint32_t* h_flags = (volatile uint32_t*)((char*)ctx->h_ex + (size_t)host_slots * gen_bytes(n, cols));
   auto hgen = [&](int i) { return gen_slot(ctx->h_ex, n, cols, i); };
@@ -1694,17 +1695,18 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
     // one persistent CTA runs every generation (mutate -> identity -> draft
     // cost) and publishes each to its pinned slot + flag; the host folds
     // generation g into the pool as soon as its flag is up
-    for (int g = 0; g < n_steps; ++g) h_flags[g] = 0u;
+    for (int g = 0; g < n_steps * nflag; ++g) h_flags[g] = 0u;
     if (launch_explore_gens(S, D, toggles, n, n_steps, dgen[0].soa, dgen[0].cost, dgen[0].id, dgen[1].soa,
                             dgen[1].cost, dgen[1].id, s_init, ctx->h_ex, gen_bytes(n, cols),
                             (size_t)((char*)hgen(0).cost - (char*)ctx->h_ex), h_flags, st))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
     for (int g = 0; g < n_steps; ++g) {
-      for (uint64_t spin = 0; h_flags[g] == 0u; ++spin) {
+      for (int f = g * nflag; f < (g + 1) * nflag; ++f)
+      for (uint64_t spin = 0; h_flags[f] == 0u; ++spin) {
         if ((spin & 1023) == 1023) {  // a faulted or finished kernel never raises the flag
           const cudaError_t q = cudaStreamQuery(st);
-          if (q != cudaErrorNotReady && h_flags[g] == 0u) {
+          if (q != cudaErrorNotReady && h_flags[f] == 0u) {
             if (q != cudaSuccess) return fail(ctx, TT_E_CUDA, cudaGetErrorString(q));
             return fail(ctx, TT_E_STATE, "explore: generation kernel ended without publishing");
           }
