@@ -157,23 +157,31 @@ __device__ __forceinline__ void publish(volatile uint32_t* flags, int g) {
   }
 }
 
-// Writes generation g's member j (factors, cost, identity) to the device
-// slot it lives in and to its pinned host mirror.
+// generation g's device slot
+__device__ __forceinline__ GenDev gen_dev(const GenOut& d, int g, int n) {
+  char* b = d.base + (size_t)g * d.stride;
+  GenDev r;
+  r.soa = (int32_t*)b;
+  r.cost = (double*)(b + d.cost_off);
+  r.id = (uint64_t*)(r.cost + n);
+  return r;
+}
+
+// Writes generation g's member j: factors, cost and identity to its device
+// slot (every generation keeps its own), cost and identity to the pinned
+// host mirror the pool is built from.
 template <int NSP, int NRED>
 __device__ __forceinline__ void emit(const GenOut& h, int g, int n, const GenDev& d, int j, const Factors<NSP, NRED>& F,
                                      double c, uint64_t id, bool write_dev_soa) {
   constexpr int kN = Factors<NSP, NRED>::kN;
   char* hb = h.base + (size_t)g * h.stride;
-  int32_t* hs = (int32_t*)hb;
   double* hc = (double*)(hb + h.cost_off);
   uint64_t* hi = (uint64_t*)(hc + n);
+  if (write_dev_soa) {
 #pragma unroll
-  for (int q = 0; q < kN; ++q) {
-    if (write_dev_soa) d.soa[(size_t)q * n + j] = F.f[q];
-    hs[(size_t)q * n + j] = F.f[q];
+    for (int q = 0; q < kN; ++q) d.soa[(size_t)q * n + j] = F.f[q];
+    d.soa[(size_t)kN * n + j] = F.unroll;
   }
-  if (write_dev_soa) d.soa[(size_t)kN * n + j] = F.unroll;
-  hs[(size_t)kN * n + j] = F.unroll;
   d.cost[j] = c, d.id[j] = id;
   hc[j] = c, hi[j] = id;
 }
@@ -188,7 +196,7 @@ __device__ __forceinline__ void emit(const GenOut& h, int g, int n, const GenDev
 // generation into the pool while the device moves on.
 template <int NSP, int NRED>
 __global__ void __launch_bounds__(kMutThreads, 1)
-    k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenDev d0, GenDev d1, uint64_t s_init,
+    k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenOut dv, uint64_t s_init,
                    GenOut h, volatile uint32_t* flags, int staged) {
   constexpr int kN = Factors<NSP, NRED>::kN;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -239,6 +247,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   // generation 0: cost the random_init population
   for (int j = jlo + tid; j < jhi; j += kMutThreads) {
     Factors<NSP, NRED> F;
+    const GenDev d0 = gen_dev(dv, 0, n);
     load_factors_cg<NSP, NRED>(d0.soa, n, j, F);
     emit<NSP, NRED>(h, 0, n, d0, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), d0.id[j], false);
   }
@@ -247,8 +256,8 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   uint64_t s0 = s_init;
   const int n_off = 4 * (n - 1);  // child n-1 starts at offset <= 4(n-2)
   for (int g = 1; g < n_steps; ++g) {
-  const GenDev prev = (g & 1) ? d0 : d1;
-  GenDev cur = (g & 1) ? d1 : d0;
+  const GenDev prev = gen_dev(dv, g - 1, n);
+  const GenDev cur = gen_dev(dv, g, n);
   const double* cost = prev.cost;
   if (g == 1) MUT_MARK(0);
   if (staged) {
@@ -437,11 +446,10 @@ size_t mutate_smem_bytes(int64_t n, int cols, bool staged) {
 constexpr size_t kSmemCap = 220 * 1024;
 
 int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int64_t n, int n_steps,
-                        int32_t* soa0, double* cost0, uint64_t* id0, int32_t* soa1, double* cost1, uint64_t* id1,
-                        uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
+                        void* dev_base, size_t dev_stride, size_t dev_cost_off, uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
                         volatile uint32_t* flags, cudaStream_t st) {
   if (n < 2 || n > kMutateMaxN) return 1;
-  GenDev d0{soa0, cost0, id0}, d1{soa1, cost1, id1};
+  GenOut dv{(char*)dev_base, dev_stride, dev_cost_off};
   GenOut h{(char*)host_base, host_stride, host_cost_off};
   const bool staged = mutate_smem_bytes(n, S.cols, true) <= kSmemCap;
   const size_t sm = mutate_smem_bytes(n, S.cols, staged);
@@ -461,7 +469,7 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
     at[0].val.clusterDim.x = explore_cluster_size(n), at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
     cfg.attrs = at, cfg.numAttrs = 1;
     tt::note_launch();
-    cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, d0, d1, s_init, h, flags,
+    cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, dv, s_init, h, flags,
                        (int)staged);
   }));
 }

@@ -1498,7 +1498,7 @@ GenSlot gen_slot(void* base, int64_t n, int cols, int which) {
 }
 
 int ensure_explore(tt_ctx* ctx, int64_t n, int cols, int host_slots, int nflag) {
-  const size_t dwant = 2 * gen_bytes(n, cols) + 16;
+  const size_t dwant = (size_t)std::max(2, host_slots) * gen_bytes(n, cols) + 16;  // device path: one slot per generation
   const size_t hwant = (size_t)host_slots * gen_bytes(n, cols) + 4 * (size_t)host_slots * nflag + 16;  // + flags
   if (dwant > ctx->ex_dcap) {
     cudaFree(ctx->d_ex);
@@ -1696,9 +1696,9 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
     // cost) and publishes each to its pinned slot + flag; the host folds
     // generation g into the pool as soon as its flag is up
     for (int g = 0; g < n_steps * nflag; ++g) h_flags[g] = 0u;
-    if (launch_explore_gens(S, D, toggles, n, n_steps, dgen[0].soa, dgen[0].cost, dgen[0].id, dgen[1].soa,
-                            dgen[1].cost, dgen[1].id, s_init, ctx->h_ex, gen_bytes(n, cols),
-                            (size_t)((char*)hgen(0).cost - (char*)ctx->h_ex), h_flags, st))
+    const size_t cost_off = (size_t)((char*)hgen(0).cost - (char*)ctx->h_ex);
+    if (launch_explore_gens(S, D, toggles, n, n_steps, ctx->d_ex, gen_bytes(n, cols), cost_off, s_init, ctx->h_ex,
+                            gen_bytes(n, cols), cost_off, h_flags, st))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
     for (int g = 0; g < n_steps; ++g) {
@@ -1716,6 +1716,12 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
       consume(hgen(g), g);
     }
     if ((rc = sync_check(ctx))) return rc;
+    // factor columns stay in the device slots; fetched only when asked for
+    if (soa_host) {
+      TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_ex, ctx->d_ex, (size_t)n_steps * gen_bytes(n, cols), cudaMemcpyDeviceToHost,
+                                   st));
+      if ((rc = sync_check(ctx))) return rc;
+    }
   } else {
     GenSlot h0 = hgen(0);
     if ((rc = cost_and_copy(dgen[0], h0, ctx->ex_ev[0]))) return rc;

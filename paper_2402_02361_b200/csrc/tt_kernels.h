@@ -86,16 +86,16 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
                   int64_t index_base, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
                   int64_t* out_count, cudaStream_t st, bool hash = false);
 // k_explore.cu: all GA generations of one explore in one persistent cluster
-// (n <= kMutateMaxN): generation 0 = slot 0 as generated (soa + identity),
-// then mutate() bit-exact from RNG state s_init; generation g is written to
-// device slot g & 1 and to pinned host memory at host_base + g * host_stride
-// (soa | cost at host_cost_off | identity), then flags[g * C + rank] = 1 per
+// (n <= kMutateMaxN): generation 0 = device slot 0 as generated (soa +
+// identity), then mutate() bit-exact from RNG state s_init; generation g is
+// written to device slot g (dev_base + g * dev_stride: soa | cost at
+// dev_cost_off | identity) and its costs + identities to pinned host memory
+// at host_base + g * host_stride (same layout), then flags[g * C + rank] = 1 per
 // CTA of the C = explore_cluster_size(n) CTA cluster.
 constexpr int64_t kMutateMaxN = 8192;
 int explore_cluster_size(int64_t n);  // CTAs of the explore cluster (flags per generation)
 int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int64_t n, int n_steps,
-                        int32_t* soa0, double* cost0, uint64_t* id0, int32_t* soa1, double* cost1, uint64_t* id1,
-                        uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
+                        void* dev_base, size_t dev_stride, size_t dev_cost_off, uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
                         volatile uint32_t* flags, cudaStream_t st);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);

