@@ -6,11 +6,12 @@
 Workload (BASELINE.json configs[1], the metric's 1-GPU configuration): the
 seven ResNet-50 conv2d subgraphs, 65,536 random candidates per subgraph
 round per GPU -> SA draft -> dedup top-512 -> PaCM verify (h = 64,
-random-init weights) -> select b = 10. PaCM runs on the tcgen05 tensor cores
-(bf16 operands, fp32 TMEM accumulators) with certified selection: the
-boundary band is rescored in fp64, so the selected set equals the
-reference's (`--precision fp64` runs the all-fp64 parity mode; the other
-precision is reported under `other_precision`). One step = one round on each
+random-init weights) -> select b = 10. PaCM runs in fp64 on the CUDA cores
+(scores within 1e-12 of the reference; the default, as fast as the tensor
+path at K = 512 and exact); `--precision bf16` runs it on the tcgen05 tensor
+cores (bf16 operands, fp32 TMEM accumulators) with certified selection (the
+boundary band rescored in fp64, so the selected set equals the reference's).
+The other precision is reported under `other_precision`. One step = one round on each
 of the seven subgraphs. For N > 1 every rank drafts its own 65,536 candidates of
 the same counter-based population (weak scaling); the per-rank top-512
 lists (cost, global index, identity) are merged after one NCCL all-gather
@@ -507,7 +508,7 @@ def main():
     ap.add_argument("--k", type=int, default=512)
     ap.add_argument("--b", type=int, default=10)
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--precision", default="bf16", choices=["fp64", "bf16"])
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "bf16"])
     ap.add_argument("--band", type=float, default=0.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-explore", action="store_true", help="skip the explore_ga entry (e.g. under ncu)")
