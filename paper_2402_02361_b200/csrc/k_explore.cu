@@ -453,7 +453,8 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
   GenOut h{(char*)host_base, host_stride, host_cost_off};
   const bool staged = mutate_smem_bytes(n, S.cols, true) <= kSmemCap;
   const size_t sm = mutate_smem_bytes(n, S.cols, staged);
-  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
+  cudaError_t err = cudaSuccess;
+  const int rc = TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
     static bool init = false;
     if (!init) {
       cudaFuncSetAttribute(k_explore_gens<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
@@ -469,9 +470,10 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
     at[0].val.clusterDim.x = explore_cluster_size(n), at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
     cfg.attrs = at, cfg.numAttrs = 1;
     tt::note_launch();
-    cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, dv, s_init, h, flags,
-                       (int)staged);
+    err = cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, dv, s_init, h, flags,
+                             (int)staged);
   }));
+  return rc ? rc : (err != cudaSuccess ? 2 : 0);
 }
 
 int explore_cluster_size(int64_t n) { return (int)std::min<int64_t>(8, std::max<int64_t>(1, (n + 63) / 64)); }

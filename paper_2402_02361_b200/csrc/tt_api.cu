@@ -4,7 +4,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1697,9 +1696,11 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
     // generation g into the pool as soon as its flag is up
     for (int g = 0; g < n_steps * nflag; ++g) h_flags[g] = 0u;
     const size_t cost_off = (size_t)((char*)hgen(0).cost - (char*)ctx->h_ex);
-    if (launch_explore_gens(S, D, toggles, n, n_steps, ctx->d_ex, gen_bytes(n, cols), cost_off, s_init, ctx->h_ex,
-                            gen_bytes(n, cols), cost_off, h_flags, st))
-      return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+    const int lrc = launch_explore_gens(S, D, toggles, n, n_steps, ctx->d_ex, gen_bytes(n, cols), cost_off, s_init,
+                                        ctx->h_ex, gen_bytes(n, cols), cost_off, h_flags, st);
+    if (lrc == 2) return fail(ctx, TT_E_CUDA, std::string("explore: cluster launch: ") +
+                                                  cudaGetErrorString(cudaGetLastError()));
+    if (lrc) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
     for (int g = 0; g < n_steps; ++g) {
       for (int f = g * nflag; f < (g + 1) * nflag; ++f)
