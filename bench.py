@@ -133,11 +133,11 @@ def run_ours(args, rank, world, local_rank):
     gather_out = torch.empty((3, k), dtype=torch.int64, device="cuda")
     gathered = torch.empty((world * 3 * k,), dtype=torch.int64, device="cuda")
 
-    def one_round(sk, soa):
+    def one_round(sk, soa, seed_=0):
         if world == 1:
-            tt.round_async(ctx, sk, dev, n, k, b, soa=soa, precision=prec, band=args.band, first=first)
+            tt.round_async(ctx, sk, dev, n, k, b, seed=seed_, soa=soa, precision=prec, band=args.band, first=first)
         else:
-            tt.round_local_async(ctx, sk, dev, n, k, b, first, gather_out, soa=soa)
+            tt.round_local_async(ctx, sk, dev, n, k, b, first, gather_out, seed=seed_, soa=soa)
             dist.all_gather_into_tensor(gathered, gather_out.reshape(-1))
             tt.round_finish_merged_async(ctx, sk, dev, gathered, n * world, k, b, precision=prec, band=args.band)
 
@@ -202,6 +202,8 @@ def run_ours(args, rank, world, local_rank):
             ev_copy[r].record(copy_stream)
 
     def step_e2e():
+        # rounds pipelined through the context's ring: round r is enqueued, then round r-1's
+        # selection is read back while r runs; the step ends with every selection on the host
         upload(0)
         model.load(params_host)                     # H2D PaCM weights (pinned, async), once per step
         for r, sk in enumerate(sketches):
@@ -209,12 +211,12 @@ def run_ours(args, rank, world, local_rank):
                 upload(r + 1)
             stream.wait_event(ev_copy[r])
             tt.schedule_from_identity(ctx, sk, ids[r], out=pops[r])  # decode to factor columns on device
-            if world == 1:
-                tt.draft_verify_round(ctx, sk, dev, n, k, b, soa=pops[r], precision=prec, band=args.band,
-                                      first=first)
-            else:
-                one_round(sk, pops[r])
-                tt.round_collect(ctx, b)
+            one_round(sk, pops[r])
+            if r > 0:
+                out_e = tt.round_collect(ctx, b)
+                assert out_e.selected == b
+        out_e = tt.round_collect(ctx, b)
+        assert out_e.selected == b
     etimes, elaunch, _ = timed(step_e2e)
     h2d = sum(x.numel() * 8 for x in ids_host) + params_host.numel() * 8
     d2h = len(sketches) * 8 * (4 + 4 * b)
@@ -222,12 +224,11 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e, seeded API (explore(seed) semantics: population drawn inside the call)
     def step_seeded():
         model.load(params_host)
-        for sk in sketches:
-            if world == 1:
-                tt.draft_verify_round(ctx, sk, dev, n, k, b, seed=seed, precision=prec, band=args.band, first=first)
-            else:
-                one_round(sk, None)
+        for r, sk in enumerate(sketches):
+            one_round(sk, None, seed)
+            if r > 0:
                 tt.round_collect(ctx, b)
+        tt.round_collect(ctx, b)
     stimes, _, _ = timed(step_seeded)
 
     def agg(ts):
@@ -307,10 +308,10 @@ def run_ours(args, rank, world, local_rank):
                        "l2": "flushed (256 MiB write) between timed steps",
                        "parallelism": f"dp{world} (population sharded, NCCL all-gather top-K merge)"},
             "e2e": {"value": cands / etot, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "tt_schedule_from_identity + tt_round (tiletune.draft_verify_round): candidates as "
+                    "api": "tt_schedule_from_identity + tt_round_async / tt_round_collect: candidates as "
                            "exact 64-bit schedule identities (every round) and PaCM weights (once per step) "
                            "from pinned host memory, the next subgraph's upload overlapped on a copy stream, "
-                           "selection read back every round"},
+                           "every round's selection read back (round r-1's while round r runs)"},
             "e2e_seeded": {"value": cands / stot, "unit": UNIT,
                            "h2d_bytes_per_step": params_host.numel() * 8, "d2h_bytes_per_step": d2h,
                            "api": "explore(seed) semantics: population drawn on device inside the call"},

@@ -228,8 +228,10 @@ typedef struct tt_round_result {
 int tt_round(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
              const int32_t* soa_dev, int64_t ld, uint64_t seed, int64_t* sel_index_host, double* sel_score_host,
              double* sel_cost_host, uint64_t* sel_identity_host, tt_round_result* result_host);
-/* Async variant: enqueue only; results land in the context and are read
- * with tt_round_collect (which synchronises). */
+/* Async variant: enqueue only. Up to 16 rounds may be in flight on one
+ * context (each copies its record into its own pinned slot); tt_round_collect
+ * returns the OLDEST uncollected round, waiting for that round only. When a
+ * 17th round is enqueued the oldest uncollected one is dropped. */
 int tt_round_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
                    const int32_t* soa_dev, int64_t ld, uint64_t seed);
 int tt_round_collect(tt_ctx* ctx, int64_t* sel_index_host, double* sel_score_host, double* sel_cost_host,

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <deque>
 #include <map>
 #include <set>
 #include <unordered_map>
@@ -25,8 +26,6 @@ struct tt_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // identities of the drafted set, overlapped with verify
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev_done = nullptr;  // recorded after a round's record copy: collect waits on it, not the stream
-  int* h_invalid = nullptr;       // pinned copy of the selector's validate_schedule flag
   std::string err;
   SelScratch sel;
   // drafted set of the current round
@@ -48,7 +47,6 @@ struct tt_ctx {
   int64_t* d_pos_fast_count = nullptr;
   int* d_status = nullptr;
   int64_t* d_record = nullptr;
-  int64_t* h_record = nullptr;  // pinned
   // PaCM params
   double* d_params = nullptr;
   int h = 0;
@@ -69,18 +67,26 @@ struct tt_ctx {
   std::vector<cudaEvent_t> ex_ev;  // one per generation in flight
   void* d_mix = nullptr;           // random-mix schedules of a draft set: soa | cost | identity
   size_t mix_cap = 0;
-  // last async round
-  int64_t last_b = 0;
-  int64_t last_k = 0;
-  bool pending = false;
-  tt_round_config last_cfg{};
-  tt_sketch last_sketch{};
-  tt_device_spec last_dev{};
-  const int32_t* last_soa = nullptr;
-  int64_t last_ld = 0;
-  uint64_t last_seed = 0;
-  int64_t last_need = 0;
-  bool last_hash = false;
+  // rounds in flight: each enqueued round copies its record into its own
+  // pinned ring slot and records its own event, so a caller can keep up to
+  // kRing rounds in flight and collect them in order (the oldest uncollected
+  // round is dropped when the ring wraps)
+  static constexpr int kRing = 16;
+  struct Pending {
+    int slot;
+    int64_t b, k, need, ld;
+    bool hash, merged;
+    tt_round_config cfg;
+    tt_sketch sketch;
+    tt_device_spec dev;
+    const int32_t* soa;
+    uint64_t seed;
+  };
+  std::deque<Pending> pend;
+  int ring_next = 0;
+  int64_t* h_rec[kRing] = {};
+  int* h_inv[kRing] = {};
+  cudaEvent_t ev_rec[kRing] = {};
   // CUDA graphs of whole rounds, keyed by every argument that shapes the
   // enqueued work (sketch, device, config, population pointer, seed, need);
   // cleared whenever scratch is reallocated
@@ -362,15 +368,37 @@ int ensure_k(tt_ctx* ctx, int64_t k) {
 
 int ensure_b(tt_ctx* ctx, int64_t b) {
   if (b <= ctx->b_cap) return TT_OK;
+  // rounds in flight still copy into the old record buffers: finish them first
+  if (!ctx->pend.empty()) TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->pend.clear();
   graphs_clear(ctx);
   cudaFree(ctx->d_pos), cudaFree(ctx->d_pos_fast), cudaFree(ctx->d_record);
-  if (ctx->h_record) cudaFreeHost(ctx->h_record);
+  for (int r = 0; r < tt_ctx::kRing; ++r)
+    if (ctx->h_rec[r]) cudaFreeHost(ctx->h_rec[r]), ctx->h_rec[r] = nullptr;
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos, sizeof(int64_t) * b));
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos_fast, sizeof(int64_t) * b));
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_record, sizeof(int64_t) * (4 + 4 * b)));
-  TT_CUDA(ctx, cudaMallocHost((void**)&ctx->h_record, sizeof(int64_t) * (4 + 4 * b)));
+  for (int r = 0; r < tt_ctx::kRing; ++r)
+    TT_CUDA(ctx, cudaMallocHost((void**)&ctx->h_rec[r], sizeof(int64_t) * (4 + 4 * b)));
   ctx->b_cap = b;
   return TT_OK;
+}
+
+// Claims the next ring slot for a round about to be enqueued (record_copy
+// lands its record and validity flag there).
+int ring_claim(tt_ctx* ctx) {
+  const int slot = ctx->ring_next;
+  for (auto it = ctx->pend.begin(); it != ctx->pend.end(); ++it)
+    if (it->slot == slot) {  // the ring wrapped: drop the oldest uncollected round
+      ctx->pend.erase(ctx->pend.begin(), it + 1);
+      break;
+    }
+  return slot;
+}
+
+void ring_push(tt_ctx* ctx, tt_ctx::Pending p) {
+  ctx->pend.push_back(p);
+  ctx->ring_next = (p.slot + 1) % tt_ctx::kRing;
 }
 
 int ensure_cost(tt_ctx* ctx, int64_t n) { return grow(ctx, ctx->sel.cost, ctx->sel.cost_cap, n); }
@@ -481,9 +509,11 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking))) return TT_E_CUDA;
   if (bad(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming))) return TT_E_CUDA;
   if (bad(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming))) return TT_E_CUDA;
-  if (bad(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming))) return TT_E_CUDA;
-  if (bad(cudaMallocHost((void**)&c->h_invalid, sizeof(int)))) return TT_E_CUDA;
-  *c->h_invalid = 0;
+  for (int r = 0; r < tt_ctx::kRing; ++r) {
+    if (bad(cudaEventCreateWithFlags(&c->ev_rec[r], cudaEventDisableTiming))) return TT_E_CUDA;
+    if (bad(cudaMallocHost((void**)&c->h_inv[r], sizeof(int)))) return TT_E_CUDA;
+    *c->h_inv[r] = 0;
+  }
   c->stream = c->own;
   if (const char* g = getenv("TT_GRAPHS")) c->graphs = g[0] != '0';
   if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
@@ -526,15 +556,17 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_tiles, c->d_ex, c->d_mix};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (c->h_record) cudaFreeHost(c->h_record);
+  for (int r = 0; r < tt_ctx::kRing; ++r) {
+    if (c->h_rec[r]) cudaFreeHost(c->h_rec[r]);
+    if (c->h_inv[r]) cudaFreeHost(c->h_inv[r]);
+    if (c->ev_rec[r]) cudaEventDestroy(c->ev_rec[r]);
+  }
   if (c->h_ex) cudaFreeHost(c->h_ex);
   for (cudaEvent_t e : c->ex_ev) cudaEventDestroy(e);
   graphs_clear(c);
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->ev_done) cudaEventDestroy(c->ev_done);
-  if (c->h_invalid) cudaFreeHost(c->h_invalid);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -854,9 +886,16 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
   }
   prof_end(ctx, 3);
   TT_LAUNCHED(ctx);
-  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_record, ctx->d_record, sizeof(int64_t) * (4 + 4 * cfg->b),
-                               cudaMemcpyDeviceToHost, ctx->stream));
-  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  return TT_OK;
+}
+
+// The round's record and validity flag into its ring slot, then its event.
+// Outside any graph (the slot changes every round; the graphs do not).
+int record_copy(tt_ctx* ctx, int slot, int64_t b) {
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_rec[slot], ctx->d_record, sizeof(int64_t) * (4 + 4 * b), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_inv[slot], ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(ctx, cudaEventRecord(ctx->ev_rec[slot], ctx->stream));
   return TT_OK;
 }
 
@@ -906,6 +945,7 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   if ((rc = ensure_feat(ctx, cfg->k))) return rc;
   if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
   if (cfg->precision == TT_PREC_BF16 && (rc = ensure_packed(ctx))) return rc;
+  const int slot = ring_claim(ctx);
   if (!ctx->graphs || ctx->prof) {
     if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash))) return rc;
   } else {
@@ -945,68 +985,61 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
     }
     if (repeat) TT_CUDA(ctx, cudaGraphLaunch(it->second.first, ctx->stream));
   }
-  // outside any capture: marks the end of this round for round_collect
-  TT_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
-  ctx->last_hash = hash;
-  ctx->pending = true;
-  ctx->last_b = cfg->b;
-  ctx->last_k = cfg->k;
-  ctx->last_cfg = *cfg;
-  ctx->last_sketch = *sk;
-  ctx->last_dev = *dev;
-  ctx->last_soa = soa;
-  ctx->last_ld = ld;
-  ctx->last_seed = seed;
-  ctx->last_need = need;
+  // outside any capture: the record into this round's ring slot, then its event
+  if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
+  ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, need, ld, hash, false, *cfg, *sk, *dev, soa, seed});
   return TT_OK;
 }
 
 int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* sel_cost, uint64_t* sel_id,
                   tt_round_result* res, bool allow_retry) {
-  if (!ctx->pending) return fail(ctx, TT_E_STATE, "round: nothing enqueued");
-  // wait for this round only (the stream may already hold the caller's next work)
+  if (ctx->pend.empty()) return fail(ctx, TT_E_STATE, "round: nothing enqueued");
+  // the oldest round in flight; wait for it only (the stream may already hold later rounds)
+  const tt_ctx::Pending p = ctx->pend.front();
+  ctx->pend.pop_front();
   int rc = TT_OK;
   {
-    const cudaError_t e1 = cudaEventSynchronize(ctx->ev_done);
+    const cudaError_t e1 = cudaEventSynchronize(ctx->ev_rec[p.slot]);
     const cudaError_t e2 = cudaGetLastError();
     if (e1 != cudaSuccess || e2 != cudaSuccess)
       rc = fail(ctx, TT_E_CUDA, std::string("round: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
   }
-  ctx->pending = false;
   if (rc) return rc;
-  const int64_t b = ctx->last_b;
+  const int64_t b = p.b;
+  const int64_t* rec = ctx->h_rec[p.slot];
+  const int* inv = ctx->h_inv[p.slot];
   const int retry_mask = TT_SEL_NEED_MORE | TT_SEL_OVERFLOW;
-  if (((int)ctx->h_record[2] & retry_mask) && allow_retry) {
+  if (((int)rec[2] & retry_mask) && allow_retry && !p.merged) {
     // NEED_MORE: duplicates consumed the selector's margin → raise the
-    // target; OVERFLOW: > 4096 keys tie at the threshold → hash path
-    int64_t need = ctx->last_need;
-    bool hash = ctx->last_hash;
+    // target; OVERFLOW: > 4096 keys tie at the threshold → hash path.
+    // Re-run synchronously (behind any rounds still in flight).
+    int64_t need = p.need;
+    bool hash = p.hash;
     bool ok = false;
     for (int attempt = 0; attempt < 62 && !ok; ++attempt) {
-      const int st = (int)ctx->h_record[2];
+      const int st = (int)rec[2];
       if (st & TT_SEL_OVERFLOW) {
         if (hash) break;
         hash = true;
       } else {
         need *= 2;
       }
-      tt_round_config cfg = ctx->last_cfg;
-      if ((rc = round_enqueue(ctx, &ctx->last_sketch, &ctx->last_dev, &cfg, ctx->last_soa, ctx->last_ld,
-                              ctx->last_seed, need, hash)))
-        return rc;
+      tt_round_config cfg = p.cfg;
+      if ((rc = round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, need, hash))) return rc;
+      const tt_ctx::Pending q = ctx->pend.back();
+      ctx->pend.pop_back();
       if ((rc = sync_check(ctx))) return rc;
-      ctx->pending = false;
-      ok = !((int)ctx->h_record[2] & retry_mask);
+      rec = ctx->h_rec[q.slot], inv = ctx->h_inv[q.slot];
+      ok = !((int)rec[2] & retry_mask);
     }
-    if (!ok && ((int)ctx->h_record[2] & TT_SEL_NEED_MORE))
+    if (!ok && ((int)rec[2] & TT_SEL_NEED_MORE))
       return fail(ctx, TT_E_STATE, "draft selector did not converge");
   }
-  const int64_t* rec = ctx->h_record;
   const int status = (int)rec[2];
   const int sel_status = status & 0xff;
   if (sel_status & TT_SEL_OVERFLOW)
     return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
-  if (ctx->last_soa && *ctx->h_invalid)
+  if (p.soa && *inv)
     return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
   const int64_t selected = rec[0];
   const int64_t* ix = rec + 4;
@@ -1410,6 +1443,7 @@ int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sk, const tt_devi
   if (m < 0 || m > 4096) return fail(ctx, TT_E_STATE, "merge: at most 4096 gathered entries per call");
   if ((rc = ensure_k(ctx, cfg->k))) return rc;
   if ((rc = ensure_b(ctx, cfg->b))) return rc;
+  const int slot = ring_claim(ctx);
   prof_begin(ctx, 4);
   if (launch_merge(cost, gidx, id, (int)m, cfg->k, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->stream))
     return fail(ctx, TT_E_STATE, "merge launch");
@@ -1417,12 +1451,9 @@ int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sk, const tt_devi
   TT_LAUNCHED(ctx);
   CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
   if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
-  TT_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
-  ctx->pending = true;
-  ctx->last_b = cfg->b;
-  ctx->last_k = cfg->k;
-  ctx->last_soa = nullptr;
-  ctx->last_need = -1;  // no retry: the local selections are the caller's
+  if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
+  // no retry: the local selections are the caller's
+  ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, -1, 0, false, true, *cfg, *sk, *dev, nullptr, 0});
   return TT_OK;
 }
 
