@@ -318,6 +318,8 @@ int compile_sketch(tt_ctx* ctx, const tt_sketch* sk, DevSketch& S) {
     }
   }
   S.space = sat_mul(space, (uint64_t)sk->n_unroll);
+  for (int q = 0; q < S.n_prime; ++q) S.pr_cinv[q] = UINT64_MAX / (S.pr_count[q] ? S.pr_count[q] : 1);
+  S.unroll_cinv = UINT64_MAX / (uint64_t)S.n_unroll;
   S.id_exact = S.space != UINT64_MAX;
   return TT_OK;
 }
