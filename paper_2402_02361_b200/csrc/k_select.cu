@@ -305,15 +305,27 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
                                                  int64_t* __restrict__ out) {
   __shared__ Key3 lists[32][33];
   __shared__ int avail;
-  __shared__ uint32_t win[32];
+  __shared__ int16_t rank_of[1024];  // output position of each selected candidate, -1 otherwise
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
-  const int64_t n = n_dev ? (*n_dev < n_max ? *n_dev : n_max) : n_max;
+  // every global read issued up front, independent of each other (one
+  // memory round trip): the count, this thread's candidate, and the record
+  // fields it writes if it is selected
+  const int64_t nd = n_dev ? *n_dev : n_max;
+  const bool in = t < n_max;
+  const double s_t = in ? scores[t] : 0.0, d_t = in ? drafts[t] : 0.0;
+  const bool ex_t = in && excluded && excluded[t];
+  const int64_t ix_t = in ? idx[t] : -1;
+  const uint64_t id_t = in && id ? id[t] : 0;
+  const int64_t st = t == 0 && sel ? (int64_t)sel->status : 0;
+  const int64_t rs = t == 0 && rescored ? (int64_t)*rescored : 0;
   if (t == 0) avail = 0;
+  rank_of[t] = -1;
   __syncthreads();
-  const bool ok = t < n && !(excluded && excluded[t]);
+  const int64_t n = nd < n_max ? nd : n_max;
+  const bool ok = t < n && !ex_t;
   Key3 k;
-  k.a = ok ? ~ordered(scores[t]) : kAll;
-  k.b = ok ? ordered(drafts[t]) : kAll;
+  k.a = ok ? ~ordered(s_t) : kAll;
+  k.b = ok ? ordered(d_t) : kAll;
   k.c = ok ? (uint32_t)t : 0xffffffffu;
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   if (lane == 0 && bal) atomicAdd(&avail, __popc(bal));
@@ -336,7 +348,7 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
         const int ow = __shfl_xor_sync(0xffffffffu, who, off);
         if (o.lt(m)) m = o, who = ow;
       }
-      if (lane == 0) win[it] = m.c;
+      if (lane == 0) rank_of[m.c] = (int16_t)it;
       if (lane == who) ++head;
     }
   }
@@ -345,22 +357,14 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
   double* sc = (double*)(ix + b);
   double* co = sc + b;
   uint64_t* ids = (uint64_t*)(co + b);
-  if (t < b) {
-    if (t < keep) {
-      const uint32_t q = win[t];
-      ix[t] = idx[q];
-      sc[t] = scores[q];
-      co[t] = drafts[q];
-      ids[t] = id ? id[q] : 0;
-    } else {
-      ix[t] = -1, sc[t] = 0.0, co[t] = 0.0, ids[t] = 0;
-    }
-  }
+  const int r = rank_of[t];
+  if (r >= 0) ix[r] = ix_t, sc[r] = s_t, co[r] = d_t, ids[r] = id_t;  // the selected candidate writes its own entry
+  if (t >= keep && t < b) ix[t] = -1, sc[t] = 0.0, co[t] = 0.0, ids[t] = 0;
   if (t == 0) {
     out[0] = keep;
     out[1] = n;
-    out[2] = (int64_t)(sel ? sel->status : 0);
-    out[3] = rescored ? *rescored : 0;
+    out[2] = st;
+    out[3] = rs;
   }
 }
 
