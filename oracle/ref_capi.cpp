@@ -5,6 +5,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,7 @@
 #include "tiletune/oracle.hpp"
 #include "tiletune/ranker.hpp"
 #include "tiletune/schedule.hpp"
+#include "tiletune/tuner.hpp"
 #include "tiletune/workload.hpp"
 
 using namespace tiletune;
@@ -402,3 +404,36 @@ int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t
 }
 
 }  // extern "C"
+
+/* ---- measurement records JSONL (tuner.cpp:577-645), one task named `task` ---- */
+int ref_records_to_jsonl(const tt_sketch* sk, const char* task, const int32_t* soa, int64_t ld, int64_t n,
+                         const int32_t* rounds, const double* lat, const double* draft, const double* score,
+                         char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    std::map<std::string, Sketch> sketches{{task, to_sketch(*sk)}};
+    std::vector<TuningRecord> recs;
+    for (int64_t i = 0; i < n; ++i) {
+      TuningRecord r;
+      r.task = task, r.round = rounds[i], r.schedule = get_sched(*sk, soa, ld, i);
+      r.latency_s = lat[i], r.draft_cost = draft[i], r.model_score = score[i];
+      recs.push_back(std::move(r));
+    }
+    std::string t = records_to_jsonl(recs, sketches);
+    *len = (int64_t)t.size();
+    if ((int64_t)t.size() < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+  });
+}
+
+int ref_records_from_jsonl(const tt_sketch* sk, const char* task, const char* text, int32_t* soa, int64_t ld,
+                           int32_t* rounds, double* lat, double* draft, double* score, int64_t cap, int64_t* n) {
+  return guard([&] {
+    std::map<std::string, Sketch> sketches{{task, to_sketch(*sk)}};
+    std::vector<TuningRecord> recs = records_from_jsonl(text, sketches);
+    *n = (int64_t)recs.size();
+    for (int64_t i = 0; i < (int64_t)recs.size() && i < cap; ++i) {
+      put_sched(*sk, recs[i].schedule, soa, ld, i);
+      rounds[i] = recs[i].round, lat[i] = recs[i].latency_s, draft[i] = recs[i].draft_cost;
+      score[i] = recs[i].model_score;
+    }
+  });
+}

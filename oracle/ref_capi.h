@@ -60,6 +60,14 @@ int ref_serialize_siamese(const double* params, int h, double m, int evolved, ch
                           int64_t* len);
 int ref_parse_siamese(const char* text, double* params, int* h, double* m, int* evolved);
 
+/* measurement records JSONL (tuner.cpp:577-645) for one task named `task`,
+ * axes named s0.., r0.. (the names this wrapper gives the op's axes) */
+int ref_records_to_jsonl(const tt_sketch* sk, const char* task, const int32_t* soa, int64_t ld, int64_t n,
+                         const int32_t* rounds, const double* lat, const double* draft, const double* score,
+                         char* buf, int64_t cap, int64_t* len);
+int ref_records_from_jsonl(const tt_sketch* sk, const char* task, const char* text, int32_t* soa, int64_t ld,
+                           int32_t* rounds, double* lat, double* draft, double* score, int64_t cap, int64_t* n);
+
 /* The reference-API draft+verify round of SURVEY.md §3.2, timed inside:
  * explore(n_steps=1) -> extract_features x K -> score_batch -> select_top.
  * Writes the selected b schedules' ranks into sel_idx (positions within the

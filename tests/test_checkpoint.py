@@ -98,3 +98,110 @@ def test_checkpoint_errors():
     with pytest.raises(TTError) as e:
         ck.parse_siamese(ck.serialize_siamese(init_params(4, 1), 4, 0.5).replace('"momentum":0.5', '"momentum":1.5'))
     assert e.value.code == "E_VALIDATE"
+
+
+@live
+@pytest.mark.parametrize("h", [8, 64])
+def test_params_text_layout_matches_reference(h):
+    # nlohmann::json's number layout (plain notation for decimal-point
+    # positions in (-4, 15], else d.ddde+XX): byte-identical text on values
+    # whose shortest digits are unique. (For arbitrary doubles the reference's
+    # Grisu2 may pick a different last digit of equal length; both texts parse
+    # to the same bits — test_params_interchange_with_reference.)
+    nice = np.array([1.0, 1e-5, 1234567890123456.0, 1e15, 123.25, -0.0, 5e-324, 1e300, 0.1, 2.5e-7, 100.0, -3.0e16,
+                     0.001, 123456789012345.0])
+    n = init_params(h, 5).size
+    p = nice[np.arange(n) % nice.size] * np.where(np.arange(n) % 3 == 0, -1.0, 1.0)
+    assert ck.serialize_params(p, h) == ref_serialize(p, h)
+    assert ck.serialize_siamese(p, h, 0.5, "evolved") == ref_serialize(p, h, (0.5, True))
+
+
+# ------------------------------------------------------- records JSONL --
+
+def _records(sk, n, seed):
+    rng = np.random.default_rng(seed)
+    soa = R.O_random_init(sk, seed, n)
+    cols = [soa[:, i].tolist() for i in range(n)]
+    nice = [0.00025, 1.5e-6, 3.0, 1234567890123456.0, 1e16, 0.125, 7e-5, 42.0]
+    recs = [{"task": "op", "round": int(i // 3), "schedule": cols[i],
+             "latency_s": float(rng.lognormal(-8, 2)), "draft_cost": float(rng.random() * 10.0 ** int(rng.integers(-6, 18))),
+             "model_score": float(rng.normal())} for i in range(n)]
+    seen, out = set(), []
+    for r in recs:  # the reference rejects duplicate (task, schedule) pairs
+        if tuple(r["schedule"]) not in seen:
+            seen.add(tuple(r["schedule"]))
+            out.append(r)
+    for i in range(0, len(out), 2):  # values with unique shortest digits: byte-identical text expected
+        out[i].update(latency_s=nice[i % 8], draft_cost=nice[(i + 3) % 8], model_score=-nice[(i + 5) % 8])
+    return out
+
+
+def _names(sk):
+    # the axis names the reference wrapper (oracle/ref_capi.cpp) gives the op
+    return [f"s{a}" for a in range(sk.op.n_spatial)] + [f"r{r}" for r in range(sk.op.n_reduction)]
+
+
+def ref_records_to_jsonl(sk, recs):
+    n = len(recs)
+    soa = np.ascontiguousarray(np.array([r["schedule"] for r in recs], np.int32).T)
+    rounds = np.array([r["round"] for r in recs], np.int32)
+    lat, dc, ms = (np.array([r[k] for r in recs]) for k in ("latency_s", "draft_cost", "model_score"))
+    buf = C.create_string_buffer(1 << 22)
+    ln = C.c_int64(0)
+    f = _ref_fn("ref_records_to_jsonl", C.c_int, [C.c_void_p, C.c_char_p, R.i32p, C.c_int64, C.c_int64, R.i32p,
+                                                   R.f64p, R.f64p, R.f64p, C.c_char_p, C.c_int64, R.i64p])
+    R.check(f(C.byref(sk), b"op", R.ptr(soa, R.i32p), n, n, R.ptr(rounds, R.i32p), R.ptr(lat, R.f64p),
+              R.ptr(dc, R.f64p), R.ptr(ms, R.f64p), buf, len(buf), C.byref(ln)))
+    return buf.value.decode()
+
+
+def ref_records_from_jsonl(sk, text, cap):
+    soa = np.zeros((sk.cols, cap), np.int32)
+    rounds = np.zeros(cap, np.int32)
+    lat, dc, ms = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    n = C.c_int64(0)
+    f = _ref_fn("ref_records_from_jsonl", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, R.i32p, C.c_int64, R.i32p,
+                                                     R.f64p, R.f64p, R.f64p, C.c_int64, R.i64p])
+    rc = f(C.byref(sk), b"op", text.encode(), R.ptr(soa, R.i32p), cap, R.ptr(rounds, R.i32p), R.ptr(lat, R.f64p),
+           R.ptr(dc, R.f64p), R.ptr(ms, R.f64p), cap, C.byref(n))
+    if rc:
+        return None
+    m = n.value
+    return [{"task": "op", "round": int(rounds[i]), "schedule": soa[:, i].tolist(), "latency_s": float(lat[i]),
+             "draft_cost": float(dc[i]), "model_score": float(ms[i])} for i in range(m)]
+
+
+@live
+@pytest.mark.parametrize("name", ["gemm1024", "r50_c3x3_64", "elementwise"])
+def test_records_jsonl_interchange_with_reference(name):
+    from paper_2402_02361_b200.types import WORKLOADS, make_elementwise, make_sketch
+    sk = make_sketch(make_elementwise(64, 48) if name == "elementwise" else WORKLOADS[name]())
+    recs = _records(sk, 40, 9)
+    tasks = {"op": (sk, _names(sk))}
+    ours = ck.records_to_jsonl(recs, tasks)
+    theirs = ref_records_to_jsonl(sk, recs)
+    # byte-identical lines where every double has unique shortest digits (even
+    # records); elsewhere the reference's Grisu2 may pick another last digit
+    for i, (lo, lt) in enumerate(zip(ours.splitlines(), theirs.splitlines())):
+        if i % 2 == 0:
+            assert lo == lt
+    assert ck.records_from_jsonl(ours, tasks) == recs  # our text, our parser: exact
+    assert ck.records_from_jsonl(theirs, tasks) == recs  # their text, our parser: exact
+    assert ref_records_from_jsonl(sk, ours, len(recs) + 1) == recs  # our text, their parser: exact
+
+
+@live
+def test_records_jsonl_errors_match_reference():
+    from paper_2402_02361_b200.types import make_gemm, make_sketch
+    sk = make_sketch(make_gemm(64, 64, 64))
+    tasks = {"op": (sk, _names(sk))}
+    recs = _records(sk, 4, 2)
+    good = ck.records_to_jsonl(recs, tasks)
+    dup = good + good.splitlines()[0] + "\n"
+    bad_sched = good.replace('"unroll":', '"unroll":3', 1)  # 1 -> 31 / 4 -> 34 / 16 -> 316: not a choice
+    unknown = good.replace('"task":"op"', '"task":"zz"', 1)
+    for text, code in [(dup, "E_VALIDATE"), (bad_sched, "E_VALIDATE"), (unknown, "E_PARSE"), ("{oops\n", "E_PARSE")]:
+        with pytest.raises(TTError) as e:
+            ck.records_from_jsonl(text, tasks)
+        assert e.value.code == code
+        assert ref_records_from_jsonl(sk, text, 16) is None  # the reference rejects it too
