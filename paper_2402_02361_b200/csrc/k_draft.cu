@@ -564,7 +564,11 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevi
   int64_t stride = 1;  // a power of two: the per-candidate sample test is a mask, not a 64-bit modulo
   while (stride * want < n) stride <<= 1;
   bool bad = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  // a contiguous chunk per CTA, so small populations still spread over every
+  // SM (the per-candidate fp64 division chains share each SM's fp64 pipe)
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t i_end = (blockIdx.x + 1) * chunk < n ? (blockIdx.x + 1) * chunk : n;
+  for (int64_t i = blockIdx.x * chunk + threadIdx.x; i < i_end; i += blockDim.x) {
     Factors<NSP, NRED> F;
     load_cand<NSP, NRED, SEED>(S, src, i, F, false);
     if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
@@ -765,7 +769,7 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   tt::note_launch();
   static bool init_cost = false;
   if (!init_cost) set_smem(k_fsel_cost<NSP, NRED, SEED>, kSampleMax * sizeof(uint32_t)), init_cost = true;
-  k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, kFastThreads, 148), kFastThreads, kSampleMax * sizeof(uint32_t), st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
+  k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, 128, 148), kFastThreads, kSampleMax * sizeof(uint32_t), st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
                                                           w.rank, w.dup, w.invalid);
   if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
   tt::note_launch();
