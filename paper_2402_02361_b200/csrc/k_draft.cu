@@ -722,7 +722,17 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
   int* flag = (int*)(bi + kFastCap);
   int* pos = flag + kFastCap;
   __shared__ int wt[32];
+  // the survivor count and every survivor slot are read together (one memory
+  // round trip): the slot arrays hold kFastCap entries, those >= nsurv unused
   const uint32_t nsurv = st->nsurv;
+  int r_[kFastE], d_[kFastE];
+  uint64_t k_[kFastE];
+  int64_t b_[kFastE];
+#pragma unroll
+  for (int q = 0; q < kFastE; ++q) {
+    const int e = threadIdx.x + q * kFastThreads;
+    r_[q] = rank_acc[e], k_[q] = skey[e], b_[q] = sidx[e], d_[q] = dup[e];
+  }
   if (threadIdx.x == 0) g_sel_ns[5] = gtimer(), g_sel_ns[7] = nsurv;
   if (nsurv > (uint32_t)kFastCap) {
     if (threadIdx.x == 0) st->status |= TT_SEL_OVERFLOW, *out_count = 0;
@@ -732,11 +742,15 @@ __global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src
   for (int e = threadIdx.x; e < kFastCap; e += blockDim.x) flag[e] = 0;
   __syncthreads();
   if (threadIdx.x == 0) g_sel_ns[8] = gtimer();
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    const int r = rank_acc[e];  // a permutation of 0..m-1: (cost, index) keys are distinct
-    a[r] = skey[e];
-    bi[r] = sidx[e];
-    flag[r] = dup[e] ? 0 : 1;
+#pragma unroll
+  for (int q = 0; q < kFastE; ++q) {
+    const int e = threadIdx.x + q * kFastThreads;
+    if (e < m) {
+      const int r = r_[q];  // a permutation of 0..m-1: (cost, index) keys are distinct
+      a[r] = k_[q];
+      bi[r] = b_[q];
+      flag[r] = d_[q] ? 0 : 1;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) g_sel_ns[9] = gtimer();
