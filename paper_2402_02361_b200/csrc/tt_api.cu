@@ -1642,7 +1642,7 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   const int host_slots = on_device ? n_steps : 2;
   const int nflag = on_device ? explore_cluster_size(n) : 1;  // flags per generation
   if ((rc = ensure_explore(ctx, n, cols, host_slots, nflag))) return rc;
-  GenSlot dgen[2] = {gen_slot(ctx->d_ex, n, cols, 0), gen_slot(ctx->d_ex, n, cols, 1)};
+  GenSlot dgen[1] = {gen_slot(ctx->d_ex, n, cols, 0)};  // generation 0 (device path: slot g holds generation g)
   volatile uint32_t* h_flags = (volatile uint32_t*)((char*)ctx->h_ex + (size_t)host_slots * gen_bytes(n, cols));
   auto hgen = [&](int i) { return gen_slot(ctx->h_ex, n, cols, i); };
   const uint64_t s0 = seed_state(seed);
