@@ -108,9 +108,12 @@ int tt_explore1(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
                 int64_t* count_host);
 /* explore(op, dev, n_steps, draft_size = k, pop_size = n, RngStream(seed),
  * toggles) with any n_steps >= 1 — the reference's genetic draft loop
- * (draft.cpp:156-221; replaces tiletune::explore, draft.hpp). Each
- * generation's draft costs + identities run on the device (bit-exact); pool
- * and mutate() (schedule.cpp:340-396, one sequential RNG stream) on the host.
+ * (draft.cpp:156-221; replaces tiletune::explore, draft.hpp). For
+ * n <= 8192 every generation — mutate() (schedule.cpp:340-396) on the
+ * reference's RNG stream, identities, draft costs — runs in one persistent
+ * device kernel and the host folds each generation into the pool as it
+ * lands; larger populations run mutate() on the host between device
+ * generations. Bit-identical to the reference either way.
  * HOST outputs, sorted by (cost, discovery): soa_host (ld = k, nullable),
  * cost_host, identity_host (nullable); *count_host = pool size (<= k);
  * *evaluations = n_steps * n. Synchronous. */
