@@ -428,10 +428,53 @@ def explore_ga(args, ctx, dev, sketches, names, reps=5):
             c = (time.perf_counter() - t0) / 3
             row.update({"reference_ms_per_explore": 1e3 * c, "reference_threads": threads,
                         "identical_to_reference_seed_1000": bool(len(rc) == len(cost) and (rc == cost).all())})
+        row["tuner_round"] = tuner_round(R, ctx, sk, dev, threads, reps)
         rows[name] = row
     return {"config": "explore(op, dev, n_steps=32, draft_size=512, pop_size=512): TunerConfig defaults "
                       "(tuner.hpp:38-40); wall clock of the host call, drafted schedules returned as exact "
                       "64-bit identities + draft costs", "subgraphs": rows}
+
+
+def tuner_round(R, ctx, sk, dev, threads, reps):
+    """The tuner's whole real round at TunerConfig defaults (tuner.cpp:294-384: GA draft set with
+    random_mix 0.2 -> features -> PaCM fp64 -> select_top(10)) through the public API (tt_draft_set,
+    tt_pacm_score, tt_select_top; host in, host out), beside the reference's own functions composed
+    the same way (oracle/_ref ref_tuner_round)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, derive_seed
+    params = tt.init_params(64, derive_seed(5, TAG_INIT))
+    model = tt.PaCM(ctx, params, 64)
+
+    def ours(seed):
+        ids, dc, _ = tt.draft_set(ctx, sk, dev, 32, 512, 512, 0.2, seed, seed + 1)
+        ids_d = torch.from_numpy(ids.view(np.int64)).cuda()
+        sc = model.score(sk, dev, ids_d, tt.TT_PREC_FP64)
+        return tt.select_top(ctx, sc, torch.from_numpy(dc).cuda(), None, 10)
+    ours(7)
+    t0 = time.perf_counter()
+    for r in range(reps):
+        sel = ours(2000 + r)
+        first = sel if r == 0 else first
+    g = (time.perf_counter() - t0) / reps
+    row = {"ms_per_round": 1e3 * g}
+    if R is not None and R.ref_available():
+        f = R.ref().ref_tuner_round
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_uint64,
+                      C.c_int64, R.f64p, C.c_int, C.c_int, R.i64p, R.f64p, R.i64p, R.f64p]
+        t0 = time.perf_counter()
+        for r in range(3):
+            sel_r, ncand, secs = np.zeros(10, np.int64), C.c_int64(0), np.zeros(2)
+            R.check(f(C.byref(sk), C.byref(dev), 32, 512, 512, 0.2, 2000 + r, 2001 + r, 10, R.ptr(params, R.f64p), 64,
+                      threads, R.ptr(sel_r, R.i64p), None, C.byref(ncand), R.ptr(secs, R.f64p)))
+            first_r = sel_r.copy() if r == 0 else first_r
+        c = (time.perf_counter() - t0) / 3
+        row.update({"reference_ms_per_round": 1e3 * c, "identical_selection_seed_2000": bool((first_r == first).all())})
+    return row
 
 
 # ------------------------------------------------------------------------------------ reference --

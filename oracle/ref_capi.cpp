@@ -4,8 +4,10 @@
 #include "ref_capi.h"
 
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -400,6 +402,52 @@ int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t
       for (std::size_t i = 0; i < ex.drafted.size(); ++i) put_sched(*sk, ex.drafted[i], drafted_soa, k, (int64_t)i);
     if (drafted_cost)
       for (std::size_t i = 0; i < ex.drafted.size(); ++i) drafted_cost[i] = ex.draft_costs[i];
+  });
+}
+
+/* The tuner's real round (build_draft_set tuner.cpp:294-323 restated over the
+ * reference's own functions, then tuner.cpp:366-384): GA explore + random
+ * mix -> features -> score_batch -> select_top. seconds[0] draft set,
+ * [1] features + scores + select. */
+int ref_tuner_round(const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t draft_size,
+                    int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int64_t b,
+                    const double* params, int h, int threads, int64_t* sel_idx, double* sel_scores,
+                    int64_t* n_candidates, double* seconds) {
+  return guard([&] {
+    TensorOpSpec op = to_op(sk->op);
+    DeviceSpec d = to_dev(*dev);
+    RankerParams p = unflatten(params, h);
+    auto t0 = std::chrono::steady_clock::now();
+    int64_t n_spec = std::llround((1.0 - random_mix) * (double)draft_size);
+    if (n_spec < 1) n_spec = 1;
+    const int64_t n_random = draft_size - n_spec;
+    RngStream erng(explore_seed);
+    ExploreResult ex = explore(op, d, n_steps, (int)n_spec, (int)pop_size, erng, {}, threads);
+    std::vector<Schedule> cands;
+    std::vector<double> drafts;
+    std::set<std::string> seen;
+    for (std::size_t i = 0; i < ex.drafted.size(); ++i)
+      if (seen.insert(schedule_key(ex.sketch, ex.drafted[i])).second)
+        cands.push_back(ex.drafted[i]), drafts.push_back(ex.draft_costs[i]);
+    if (n_random > 0) {
+      RngStream mrng(mix_seed);
+      for (auto& s : random_init(ex.sketch, n_random, mrng))
+        if (seen.insert(schedule_key(ex.sketch, s)).second)
+          cands.push_back(s), drafts.push_back(draft_cost(ex.sketch, s, d).total);
+    }
+    seconds[0] = secs_since(t0);
+    auto t1 = std::chrono::steady_clock::now();
+    std::vector<HybridFeature> feats(cands.size());
+    parallel_for(feats.size(), threads, [&](std::size_t i) { feats[i] = extract_features(ex.sketch, cands[i], d); });
+    std::vector<double> scores = score_batch(p, feats, {}, threads);
+    std::vector<char> excluded(scores.size(), 0);
+    auto sel = select_top(scores, drafts, excluded, (std::size_t)b);
+    seconds[1] = secs_since(t1);
+    for (int64_t i = 0; i < b && i < (int64_t)sel.size(); ++i) {
+      sel_idx[i] = (int64_t)sel[i];
+      if (sel_scores) sel_scores[i] = scores[sel[i]];
+    }
+    *n_candidates = (int64_t)cands.size();
   });
 }
 

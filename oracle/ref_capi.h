@@ -60,6 +60,15 @@ int ref_serialize_siamese(const double* params, int h, double m, int evolved, ch
                           int64_t* len);
 int ref_parse_siamese(const char* text, double* params, int* h, double* m, int* evolved);
 
+/* The tuner's real round: build_draft_set (tuner.cpp:294-323: GA explore of
+ * n_spec + unseen random mix) -> extract_features -> score_batch ->
+ * select_top(b). sel_idx = positions in the candidate list; seconds[0] the
+ * draft set, seconds[1] features + scores + select. */
+int ref_tuner_round(const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t draft_size,
+                    int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int64_t b,
+                    const double* params, int h, int threads, int64_t* sel_idx, double* sel_scores,
+                    int64_t* n_candidates, double* seconds);
+
 /* measurement records JSONL (tuner.cpp:577-645) for one task named `task`,
  * axes named s0.., r0.. (the names this wrapper gives the op's axes) */
 int ref_records_to_jsonl(const tt_sketch* sk, const char* task, const int32_t* soa, int64_t ld, int64_t n,
