@@ -185,6 +185,14 @@ __device__ __forceinline__ WStages weight_stages(const Params64& P, int h, bool 
   return w;
 }
 
+// clock64 marks of CTA 0, thread 0, first pass (phase probe, ttdbg_pacm64_clocks,
+// tools/probe_pacm64.py)
+__device__ long long g_clk_p64[24];
+#define P64_MARK(i)                                                   \
+  do {                                                                \
+    if (blockIdx.x == 0 && t == 0 && e0 == 0) g_clk_p64[i] = clock64(); \
+  } while (0)
+
 // G candidate groups of kT64 threads per CTA share each staged weight block
 // (G = 4 for whole drafted sets, 1 for the short certification sublists).
 template <int RG, int kT64>
@@ -243,6 +251,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
     const int64_t ent = e0 + grp;
     const bool live = ent < count;
     const int64_t pos = live ? (sublist ? sublist[ent] : ent) : 0;
+    P64_MARK(0);
     base = gs;
     issue(0);
     issue(1);
@@ -258,14 +267,17 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
       for (int u = lt; u < h; u += kT64) hw2s[u] = __ldg(P.hw2 + u);
     }
     __syncthreads();
+    P64_MARK(1);
     int s = 0;
     // one weight stage: wait for its buffer, compute, release, prefetch s + 2
 #define TT_STAGE(CALL)                                 \
   do {                                                 \
     tc::mbar_wait(&bars[gs & 1u], (gs >> 1) & 1u);     \
     const double* Wm = sm64 + (gs & 1u) * wd;          \
+    P64_MARK(2 + 2 * s);                               \
     if (live) CALL;                                    \
     __syncthreads();                                   \
+    P64_MARK(3 + 2 * s);                               \
     ++gs;                                              \
     issue(s + 2);                                      \
     ++s;                                               \
@@ -288,6 +300,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
           pr[u] = __dmul_rn(acc, scale);
         }
       __syncthreads();
+      P64_MARK(19);
       if (live && lt < B) {  // softmax rows (ranker.cpp:181-191)
         double* row = pr + lt * B;
         double mx = row[0];
@@ -301,6 +314,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
         for (int j = 0; j < B; ++j) row[j] = __ddiv_rn(row[j], sum);
       }
       __syncthreads();
+      P64_MARK(20);
       if (live)
         for (int u = lt; u < B * h; u += kT64) {  // matmul (ranker.cpp:113-122)
           const int j = u / B, i = u - j * B;
@@ -309,6 +323,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
           ao[j * bp + i] = acc;
         }
       __syncthreads();
+      P64_MARK(21);
       pooled = ao;
     }
     const double inv_n = __ddiv_rn(1.0, (double)B);
@@ -324,6 +339,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
         if (j < h) gp[j] = 0.0;
       }
     __syncthreads();
+    P64_MARK(22);
     // head layer 1 over k = 0..2h-1 (1 row), split in two weight stages
     TT_STAGE((dense_row64<kT64>(lt, cat, h, Wm, h, gp, nullptr, false, gp)));
     TT_STAGE((dense_row64<kT64>(lt, cat + h, h, Wm, h, gp, P.hb1, true, g)));
@@ -335,6 +351,7 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
       score_out[pos] = __dadd_rn(acc, __ldg(P.hb2));
     }
     __syncthreads();
+    P64_MARK(18);
   }
 }
 
@@ -367,3 +384,7 @@ int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_blo
 }
 
 }  // namespace tt
+
+extern "C" int ttdbg_pacm64_clocks(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_clk_p64, sizeof(long long) * (n < 24 ? n : 24));
+}
