@@ -295,8 +295,15 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
         for (int u = lt; u < B * B; u += kT64) {  // matmul_nt (ranker.cpp:102-111), then scale
           const int i = u / B, j = u - (u / B) * B;
           double acc = 0.0;
-#pragma unroll 8
-          for (int c = 0; c < h; ++c) acc = __dadd_rn(acc, __dmul_rn(qm[c * bp + i], km[c * bp + j]));
+          int c = 0;
+          for (; c + 16 <= h; c += 16) {  // 16 products staged in registers, then the chain in c order
+            double pq[16];
+#pragma unroll
+            for (int v = 0; v < 16; ++v) pq[v] = __dmul_rn(qm[(c + v) * bp + i], km[(c + v) * bp + j]);
+#pragma unroll
+            for (int v = 0; v < 16; ++v) acc = __dadd_rn(acc, pq[v]);
+          }
+          for (; c < h; ++c) acc = __dadd_rn(acc, __dmul_rn(qm[c * bp + i], km[c * bp + j]));
           pr[u] = __dmul_rn(acc, scale);
         }
       __syncthreads();
@@ -316,11 +323,22 @@ __global__ void __launch_bounds__(4 * kT64) k_pacm64(const double* __restrict__ 
       __syncthreads();
       P64_MARK(20);
       if (live)
-        for (int u = lt; u < B * h; u += kT64) {  // matmul (ranker.cpp:113-122)
-          const int j = u / B, i = u - j * B;
-          double acc = 0.0;
-          for (int r = 0; r < B; ++r) acc = __dadd_rn(acc, __dmul_rn(pr[i * B + r], vm[j * bp + r]));
-          ao[j * bp + i] = acc;
+        for (int u0 = lt; u0 < B * h; u0 += 4 * kT64) {  // matmul (ranker.cpp:113-122), 4 outputs interleaved
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          int jj[4], ii[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int u = u0 + x * kT64 < B * h ? u0 + x * kT64 : u0;
+            jj[x] = u / B, ii[x] = u - jj[x] * B;
+          }
+          for (int r = 0; r < B; ++r) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              acc[x] = __dadd_rn(acc[x], __dmul_rn(pr[ii[x] * B + r], vm[jj[x] * bp + r]));
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            if (u0 + x * kT64 < B * h) ao[jj[x] * bp + ii[x]] = acc[x];
         }
       __syncthreads();
       P64_MARK(21);
