@@ -18,6 +18,6 @@ from paper_2402_02361_b200 import _capi  # noqa: E402
 clk = (C.c_longlong * 8)()
 C.CDLL(_capi.LIB_PATH).ttdbg_mutate_clocks(clk, 8)
 c = np.array(clk[:8], dtype=np.int64)
-print("k_mutate cycles: weights+sum", c[1] - c[0], "lengths", c[2] - c[1], "chain", c[3] - c[2], "apply", c[4] - c[3],
+print("k_explore_gens generation-1 cycles: weights+lengths", c[1] - c[0], "sum || offset chain", c[2] - c[1], "stitch", c[3] - c[2], "apply", c[4] - c[3],
       "| thread 0 of CTA 0: child built", c[5] - c[3], "draft cost", c[6] - c[5], "identity", c[7] - c[6],
       "writes", c[4] - c[7])
