@@ -141,9 +141,22 @@ def run_ours(args, rank, world, local_rank):
             dist.all_gather_into_tensor(gathered, gather_out.reshape(-1))
             tt.round_finish_merged_async(ctx, sk, dev, gathered, n * world, k, b, precision=prec, band=args.band)
 
+    # rounds pipelined through the context's record ring: round r is enqueued, then
+    # round r-1's selection is read back while r runs (at most two in flight)
+    inflight = {"n": 0}
+
+    def collect_lagged(c=None, keep=1):
+        c = c or ctx
+        while inflight["n"] > keep:
+            out_ = tt.round_collect(c, b)
+            assert out_.selected == b and (out_.status & 0xff) == 0, out_
+            inflight["n"] -= 1
+
     def step_value():
         for sk, soa in zip(sketches, pops):
             one_round(sk, soa)
+            inflight["n"] += 1
+            collect_lagged()
 
     # warm-up + correctness gate: every subgraph's round must collect cleanly
     for _ in range(args.warmup):
@@ -155,6 +168,8 @@ def run_ours(args, rank, world, local_rank):
 
     def drain():
         # collect every round still in flight on the context (oldest first)
+        collect_lagged(keep=0)
+        inflight["n"] = 0
         while True:
             try:
                 tt.round_collect(ctx, b)
@@ -195,8 +210,6 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         times, launches, _ = timed(step_value)
     clocks = clk.summary()
-    out = tt.round_collect(ctx, b)  # oldest round still in flight
-    assert out.selected == b and out.status == 0
     drain()
 
     # ---- stage breakdown (separate pass, events per stage on the ctx stream)
@@ -275,9 +288,11 @@ def run_ours(args, rank, world, local_rank):
                 tt.round_local_async(ctx, sk, dev, n, k, b, first, gather_out, soa=soa)
                 dist.all_gather_into_tensor(gathered, gather_out.reshape(-1))
                 tt.round_finish_merged_async(ctx, sk, dev, gathered, n * world, k, b, precision=alt, band=args.band)
+            inflight["n"] += 1
+            collect_lagged()
     for _ in range(2):
         step_alt()
-        tt.round_collect(ctx, b)
+    drain()
     atimes, _, aprof = timed(step_alt, profile=True)
     drain()
 
@@ -292,6 +307,9 @@ def run_ours(args, rank, world, local_rank):
         cstreams = [torch.cuda.ExternalStream(c_.stream_handle()) for c_ in cctx]
 
         def step_conc():
+            for c_ in cctx:  # the previous step's rounds (complete: the step ended with a sync)
+                if c_._inflight:
+                    tt.round_collect(c_, b)
             e_start = torch.cuda.Event()
             e_start.record(stream)
             for c_, cs, sk, soa in zip(cctx, cstreams, sketches, pops):
@@ -303,8 +321,7 @@ def run_ours(args, rank, world, local_rank):
                 stream.wait_event(e_done)
         for _ in range(2):
             step_conc()
-            for c_ in cctx:
-                tt.round_collect(c_, b)
+            torch.cuda.synchronize()
         ctimes, _, _ = timed(step_conc)
         for c_ in cctx:
             out_c = tt.round_collect(c_, b)
@@ -580,7 +597,7 @@ def main():
     ap.add_argument("--b", type=int, default=10)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--precision", default="fp64", choices=["fp64", "bf16"])
-    ap.add_argument("--band", type=float, default=0.0)
+    ap.add_argument("--band", type=float, default=None, help="bf16 certification band (default TT_BF16_BAND)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-explore", action="store_true", help="skip the explore_ga entry (e.g. under ncu)")
     ap.add_argument("--ref-rounds-per-step", type=int, default=1)

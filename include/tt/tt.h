@@ -35,7 +35,12 @@ enum tt_status {
   TT_E_STATE = 4,    /* tiletune::err::kState */
   TT_E_IO = 5,       /* tiletune::err::kIo */
   TT_E_CUDA = 6,     /* device / launch failure */
-  TT_E_NCCL = 7      /* collective failure (reserved; collectives run in the host orchestrator) */
+  TT_E_NCCL = 7      /* collective failure (tt_comm_*) */
+};
+
+/* tt_round_result.status bits above the selector's own (low byte) */
+enum tt_round_flags {
+  TT_ROUND_BAND_RERUN = 1 << 16 /* bf16 error on the rescored set exceeded the band: re-run in fp64 */
 };
 
 /* PaCM arithmetic for tt_pacm_score / tt_round */
@@ -210,7 +215,7 @@ typedef struct tt_round_config {
   int64_t b;          /* measurement batch (tuner.hpp:37, 10) */
   int32_t toggles;    /* TT_TOGGLES_ALL */
   int32_t precision;  /* tt_precision */
-  double band;        /* TT_PREC_BF16: certified |score error| bound */
+  double band;        /* TT_PREC_BF16: certified |score error| bound, > 0 (TT_E_CONFIG otherwise) */
   int64_t first;      /* seeded source: first schedule index of the shard */
 } tt_round_config;
 
@@ -218,8 +223,9 @@ typedef struct tt_round_result {
   int64_t selected; /* min(b, drafted) */
   int64_t drafted;  /* unique drafted candidates (<= k) */
   int64_t rescored; /* fp64-rescored candidates (certification band) */
-  int32_t status;   /* internal selector flags, 0 when clean */
-  int32_t _pad;
+  int32_t status;   /* selector flags (low byte, 0 when clean) | tt_round_flags */
+  int32_t retries;  /* selector re-runs (device threshold retries + host re-runs) */
+  double band_err;  /* TT_PREC_BF16: max |bf16 - fp64| score over the rescored set */
 } tt_round_result;
 
 /* One draft+verify round (tuner.cpp:361-396 minus the measurement):
@@ -232,22 +238,32 @@ int tt_round(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, co
              const int32_t* soa_dev, int64_t ld, uint64_t seed, int64_t* sel_index_host, double* sel_score_host,
              double* sel_cost_host, uint64_t* sel_identity_host, tt_round_result* result_host);
 /* Async variant: enqueue only. Up to 16 rounds may be in flight on one
- * context (each copies its record into its own pinned slot); tt_round_collect
- * returns the OLDEST uncollected round, waiting for that round only. When a
- * 17th round is enqueued the oldest uncollected one is dropped. */
+ * context (each copies its record into its own pinned slot); a 17th enqueue
+ * fails with TT_E_STATE until the oldest is collected. tt_round_collect
+ * returns the OLDEST uncollected round, waiting for that round only; the
+ * output buffers hold `capacity` entries each (TT_E_CONFIG, round kept in
+ * flight, when that round's b exceeds it). A round whose selector ran out of
+ * margin is re-run here (result.retries); a bf16 round whose observed error
+ * on its rescored set exceeds cfg.band is re-run in fp64
+ * (TT_ROUND_BAND_RERUN). tt_round (synchronous) requires no rounds in flight. */
 int tt_round_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
                    const int32_t* soa_dev, int64_t ld, uint64_t seed);
-int tt_round_collect(tt_ctx* ctx, int64_t* sel_index_host, double* sel_score_host, double* sel_cost_host,
-                     uint64_t* sel_identity_host, tt_round_result* result_host);
+int tt_round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index_host, double* sel_score_host,
+                     double* sel_cost_host, uint64_t* sel_identity_host, tt_round_result* result_host);
 
 /* Sharded round, draft half (async): this rank's K-entry list of (cost,
- * global index, identity) for the all-gather; unused slots get index -1.
+ * global index, identity) for the all-gather, ascending by (cost, index);
+ * unused slots get index -1. A rank whose selector could not certify its
+ * list (more than 4096 schedules tied at the threshold) writes index -2 in
+ * slot 0, and every rank's merged round then fails with TT_E_STATE.
  * cfg->first = global index of this shard's first candidate. */
 int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
                          const tt_round_config* cfg, const int32_t* soa_dev, int64_t ld, uint64_t seed,
                          double* cost_dev, int64_t* gidx_dev, uint64_t* identity_dev);
 /* Sharded round, verify half, async: merge + features + PaCM + select;
- * read with tt_round_collect. */
+ * read with tt_round_collect. m <= 4096 entries in any order, or up to
+ * 65,536 as m / k whole per-rank lists (tt_round_local_async's layout). The
+ * gathered lists must stay valid until the round is collected. */
 int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
                                  const tt_round_config* cfg, const double* cost_dev, const int64_t* gidx_dev,
                                  const uint64_t* identity_dev, int64_t m);

@@ -27,10 +27,14 @@ class RoundConfig(C.Structure):
 
 class RoundResult(C.Structure):
     _fields_ = [("selected", C.c_int64), ("drafted", C.c_int64), ("rescored", C.c_int64),
-                ("status", C.c_int32), ("_pad", C.c_int32)]
+                ("status", C.c_int32), ("retries", C.c_int32), ("band_err", C.c_double)]
 
 
 TT_PREC_FP64, TT_PREC_BF16 = 0, 1
+TT_ROUND_BAND_RERUN = 1 << 16
+# default certification band for bf16 rounds: a bound on |bf16 - fp64| scores
+# at h = 64 (measured max 3.2e-2 on random-init weights)
+TT_BF16_BAND = 6e-2
 
 # (name, restype, argtypes) — exactly the declarations of include/tt/tt.h
 _SIGS = [
@@ -79,7 +83,7 @@ _SIGS = [
     ("tt_round", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64, i64p, f64p,
                            f64p, u64p, P(RoundResult)]),
     ("tt_round_async", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64]),
-    ("tt_round_collect", C.c_int, [vp, i64p, f64p, f64p, u64p, P(RoundResult)]),
+    ("tt_round_collect", C.c_int, [vp, C.c_int64, i64p, f64p, f64p, u64p, P(RoundResult)]),
     ("tt_round_finish_merged", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, vp, vp, C.c_int64,
                                          i64p, f64p, f64p, u64p, P(RoundResult)]),
     ("tt_round_drafted", C.c_int, [vp, P(vp), P(vp), P(vp), P(vp)]),

@@ -21,11 +21,16 @@
 //     on insert (atomicMin keeps the first index).
 // Identical schedules have identical costs, so the threshold never splits
 // a duplicate group; selection is exact for any input.
+#include <algorithm>
 #include <cstdint>
+
+#include <cooperative_groups.h>
 
 #include "tt_block.cuh"
 #include "tt_device.cuh"
 #include "tt_kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace tt {
 
@@ -37,8 +42,9 @@ constexpr int kTableCap = 16384;       // hash slots of the fallback path
 constexpr int kSortE = 4;              // keys per thread in the 4096-entry sorts
 constexpr int kFinalE = 1;             // keys per thread in the 1024-entry sorts (1024 threads)
 constexpr uint64_t kEmpty = ~0ull;
-constexpr int kFastCap = 4096;               // survivors the fast path ranks
-constexpr int kSampleMax = 32768;            // sampled cost keys (top 32 bits) for the threshold
+constexpr int kFastCap = 8192;               // survivors the fast path ranks
+constexpr int kSampleMin = 4096;             // sampled cost keys (top 32 bits) for the threshold
+constexpr int kSampleMax = 32768;
 constexpr int64_t kFastMaxN = int64_t{16} << 20;  // fast path population limit
 
 static int grid_for(int64_t n, int threads, int max_blocks) {
@@ -419,52 +425,59 @@ __global__ void __launch_bounds__(1024) k_sel_small(DevSketch S, DevDevice D, Sr
 }
 
 // ------------------------------------------- fast path (sampled threshold) ----
-// N > 1024, four short kernels and no CTA-wide sorting network (a bitonic
-// sort of 4096 keys costs ~60 us on one SM; everything here is either
-// grid-wide or O(log) passes):
-//   k_fsel_cost:    K1 over the population, costs to HBM, a strided sample of
-//                   4096..32768 cost keys (top 32 bits); the last CTA (ticket) radix-selects the
-//                   sample key of rank ceil(1.5 need ns / n) + 3 as the
-//                   survivor threshold (~1.5x need survivors expected).
-//   k_fsel_compact: keys <= threshold appended (warp-aggregated) with a
-//                   schedule fingerprint (seeded: the exact identity the
-//                   generator returns; explicit: a 64-bit hash of the factor
-//                   columns, confirmed column by column on a match).
-//   k_fsel_rank:    all-pairs over the <= 4096 survivors, spread over the GPU:
-//                   each (survivor, 256-chunk) thread counts the keys below
-//                   it ((cost, index) order) and flags a duplicate when an
-//                   equal-cost survivor with a lower index is the same
-//                   schedule ("first discovery wins", draft.cpp:200-203).
-//   k_fsel_emit:    one CTA scatters survivors to their ranks and emits the K
-//                   lowest unique in ascending (cost, index) order.
+// N > 1024: ONE cooperative kernel (one 1024-thread CTA per SM, grid-wide
+// barriers between phases; no CTA-wide sorting network and no host round
+// trip):
+//   A  K1 over the population (a contiguous chunk per CTA), costs to HBM and
+//      a strided sample of 4096..32768 cost keys (top 32 bits).
+//   B  every CTA loads the whole sample and computes the same survivor
+//      threshold: the sample key of rank ceil(1.5 need ns / n) + 3 (~1.5x
+//      need survivors expected).
+//   C  keys <= threshold appended (warp-aggregated) with a schedule
+//      fingerprint (seeded: the exact identity the generator returns;
+//      explicit: a 64-bit hash of the factor columns, confirmed column by
+//      column on a match).
+//   D  all-pairs over the <= 8192 survivors in 32 x 32 blocks, one per warp,
+//      spread over the GPU: each survivor counts the keys below it ((cost,
+//      index) order) and flags a duplicate when an equal-cost survivor with a
+//      lower index is the same schedule ("first discovery wins",
+//      draft.cpp:200-203).
+//      Too few unique survivors (duplicates ate the margin): need doubles and
+//      B-D repeat over the costs already in HBM (K1 is never re-run).
+//   E  the CTAs holding survivors write the K lowest unique in ascending
+//      (cost, index) order: position = rank - duplicates ranked below.
 // Exactness never depends on the sample: every key <= threshold survives,
 // so whenever >= K unique schedules survive they include the true top-K;
-// otherwise NEED_MORE (the host retries with a larger need); > 4096
-// survivors report OVERFLOW (the identity-keyed hash path takes over).
+// > 8192 survivors (or no convergence) report OVERFLOW and the host takes
+// the identity-keyed hash path.
 constexpr int kFastThreads = 1024;
+constexpr int kMaxAttempts = 8;
 
-// %globaltimer marks (ns) of the fast selector's phases, read by ttdbg_select_clocks:
-// [0] first CTA start, [1] K1 done (last CTA begins the threshold), [2] threshold done,
-// [3] compact start, [4] rank start, [5] emit start, [6] emit end
-__device__ unsigned long long g_sel_ns[12];
+// %globaltimer marks (ns) of the fused selector's phases (CTA 0), read by
+// ttdbg_select_clocks (tools/probe_select.py): [0] start, [1] K1 done (all
+// CTAs), [2] threshold, [3] compact done, [4] rank done, [5] emit done,
+// [6] survivors, [7] attempts; [8 + 2b] CTA 0's arrival at barrier b,
+// [9 + 2b] the latest arrival (first attempt)
+
+__device__ unsigned long long g_sel_ns[24];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-constexpr int kFastE = kFastCap / kFastThreads;  // 4 keys per thread
-constexpr int kRankChunk = 128;
 
-__device__ __forceinline__ bool last_cta(SelState* st) {
-  __shared__ int am_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    am_last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
+// Grid-wide barrier of the cooperative launch (every CTA co-resident):
+// cooperative_groups' grid sync, 1.25 us on B200 at 148 CTAs against 2.3 us
+// for an atomic generation counter polled by one thread per CTA
+// (tools/barrier_bench.cu). mark >= 0 records CTA 0's arrival and the latest
+// arrival (probe).
+__device__ __forceinline__ void grid_barrier(int mark = -1) {
+  if (mark >= 0 && threadIdx.x == 0) {
+    const unsigned long long now = gtimer();
+    if (blockIdx.x == 0) g_sel_ns[8 + 2 * mark] = now;
+    atomicMax(&g_sel_ns[9 + 2 * mark], now);
   }
-  __syncthreads();
-  if (am_last) __threadfence();
-  return am_last != 0;
+  cg::this_grid().sync();
 }
 
 // Upper bound of the 64-bit cost key whose top 32 bits have rank r (0-based)
@@ -547,63 +560,6 @@ __device__ uint64_t block_sample_threshold(const uint32_t* keys, int n, int r, i
   return ((uint64_t)key32 << 32) | 0xffffffffull;
 }
 
-template <int NSP, int NRED, bool SEED>
-__global__ void __launch_bounds__(kFastThreads) k_fsel_cost(DevSketch S, DevDevice D, Src src, int64_t n,
-                                                            int toggles, int64_t need, double* __restrict__ cost,
-                                                            uint32_t* __restrict__ sample, SelState* __restrict__ st,
-                                                            int* __restrict__ rank_acc, int* __restrict__ dup,
-                                                            int* __restrict__ invalid) {
-  pdl_trigger();
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* keys = (uint32_t*)smem;  // the last CTA's copy of the sample
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[0] = gtimer();
-  __shared__ int hist[4096], hsum[4096], wt[32];
-  // n / 256 samples, clamped to [4096, 32768]: each sample stands for <= 512
-  // candidates, so the rank-r threshold keeps ~(r + 1) * stride survivors
-  const int64_t want = n / 256 > kFastCap ? (n / 256 < kSampleMax ? n / 256 : kSampleMax) : kFastCap;
-  int64_t stride = 1;  // a power of two: the per-candidate sample test is a mask, not a 64-bit modulo
-  while (stride * want < n) stride <<= 1;
-  bool bad = false;
-  // a contiguous chunk per CTA, so small populations still spread over every
-  // SM (the per-candidate fp64 division chains share each SM's fp64 pipe)
-  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t i_end = (blockIdx.x + 1) * chunk < n ? (blockIdx.x + 1) * chunk : n;
-  for (int64_t i = blockIdx.x * chunk + threadIdx.x; i < i_end; i += blockDim.x) {
-    Factors<NSP, NRED> F;
-    load_cand<NSP, NRED, SEED>(S, src, i, F, false);
-    if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
-    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles);
-    cost[i] = c;
-    if ((i & (stride - 1)) == 0) sample[i / stride] = (uint32_t)(cost_key(c) >> 32);
-  }
-  // zero the rank kernel's accumulators for this round
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kFastCap; e += gridDim.x * blockDim.x)
-    rank_acc[e] = 0, dup[e] = 0;
-  if (bad) atomicOr(invalid, 1);
-  if (!last_cta(st)) return;
-  if (threadIdx.x == 0) g_sel_ns[1] = gtimer();
-  const int ns = (int)((n + stride - 1) / stride);
-  for (int e = threadIdx.x; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
-  __syncthreads();
-  // expected survivors ~1.5x need (+3 samples): below need only ~3.5 sigma out
-  // (then NEED_MORE and a retry with a larger need)
-  int64_t r = (3 * need * ns + 2 * n - 1) / (2 * n) + 3;
-  const bool all = r >= ns - 1;
-  const uint64_t thr = all ? ~0ull : block_sample_threshold(keys, ns, (int)r, hist, hsum, wt);
-  if (threadIdx.x == 0) {
-    g_sel_ns[2] = gtimer();
-    st->prefix = thr;
-    st->shift = 0;
-    st->all = all ? 1 : 0;
-    st->need = need;
-    st->nsurv = 0;
-    st->status = 0;
-    st->count = 0;
-    st->done = 1;
-    st->ticket = 0;
-  }
-}
-
 // 64-bit fingerprint of a schedule's factor columns (explicit populations)
 template <int NSP, int NRED>
 __device__ __forceinline__ uint64_t fingerprint(const Factors<NSP, NRED>& F) {
@@ -611,41 +567,6 @@ __device__ __forceinline__ uint64_t fingerprint(const Factors<NSP, NRED>& F) {
 #pragma unroll
   for (int q = 0; q < Factors<NSP, NRED>::kN; ++q) h = scramble64(h ^ ((uint64_t)(uint32_t)F.f[q] + kGolden));
   return h;
-}
-
-template <int NSP, int NRED, bool SEED>
-__global__ void __launch_bounds__(256) k_fsel_compact(DevSketch S, Src src, const double* __restrict__ cost,
-                                                      int64_t n, SelState* __restrict__ st,
-                                                      uint64_t* __restrict__ skey, int64_t* __restrict__ sidx,
-                                                      uint64_t* __restrict__ sfp) {
-  pdl_wait();
-  pdl_trigger();
-  const uint64_t thr = st->prefix;
-  const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[3] = gtimer();
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    uint64_t key = 0;
-    bool keep = false;
-    if (i < n) {
-      key = cost_key(__ldcg(cost + i));
-      keep = key <= thr;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (!m) continue;
-    uint32_t pos0 = 0;
-    if (lane == 0) pos0 = atomicAdd(&st->nsurv, (uint32_t)__popc(m));
-    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
-    if (keep) {
-      const uint32_t p = pos0 + __popc(m & ((1u << lane) - 1u));
-      if (p < (uint32_t)kFastCap) {
-        Factors<NSP, NRED> F;
-        const uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, true);
-        skey[p] = key, sidx[p] = i;
-        sfp[p] = SEED ? id : fingerprint<NSP, NRED>(F);
-      }
-    }
-  }
 }
 
 template <int NSP, int NRED, bool SEED>
@@ -660,148 +581,218 @@ __device__ __forceinline__ bool same_schedule(const DevSketch& S, const Src& src
   return same;
 }
 
-template <int NSP, int NRED, bool SEED>
-__global__ void __launch_bounds__(kRankChunk) k_fsel_rank(DevSketch S, Src src, const SelState* __restrict__ st,
-                                                          const uint64_t* __restrict__ skey,
-                                                          const int64_t* __restrict__ sidx,
-                                                          const uint64_t* __restrict__ sfp,
-                                                          int* __restrict__ rank_acc, int* __restrict__ dup) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ uint64_t ck[kRankChunk], cf[kRankChunk];
-  __shared__ int64_t ci[kRankChunk];
-  const int m = (int)min(*(volatile const uint32_t*)&st->nsurv, (uint32_t)kFastCap);
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ns[4] = gtimer();
-  const int chunks = (m + kRankChunk - 1) / kRankChunk;
-  for (int blk = blockIdx.x; blk < chunks * chunks; blk += gridDim.x) {
-    const int ce = blk / chunks, cj = blk - ce * chunks;  // element chunk, comparison chunk
-    const int j0 = cj * kRankChunk;
-    __syncthreads();
-    if (j0 + (int)threadIdx.x < m) {
-      ck[threadIdx.x] = skey[j0 + threadIdx.x];
-      ci[threadIdx.x] = sidx[j0 + threadIdx.x];
-      cf[threadIdx.x] = sfp[j0 + threadIdx.x];
+template <int NSP, int NRED, bool SEED, bool WITH_ID>
+__global__ void __launch_bounds__(kFastThreads, 1)
+    k_fsel(DevSketch S, DevDevice D, Src src, int64_t n, int toggles, int64_t k, int64_t need,
+           double* __restrict__ cost, uint32_t* __restrict__ sample, SelState* __restrict__ st,
+           uint64_t* __restrict__ skey, int64_t* __restrict__ sidx, uint64_t* __restrict__ sfp,
+           int* __restrict__ rank_acc, int* __restrict__ dup, int* __restrict__ invalid,
+           int64_t* __restrict__ out_idx, double* __restrict__ out_cost, uint64_t* __restrict__ out_id,
+           int64_t* __restrict__ out_count) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* keys = (uint32_t*)smem;  // the whole sample, every CTA
+  __shared__ int hist[4096], hsum[4096], wt[32];
+  __shared__ uint32_t dmask[kFastCap / 32];
+  __shared__ int dcnt[kFastCap / 32], dpre[kFastCap / 32];
+  const int t = threadIdx.x;
+  if (blockIdx.x == 0 && t == 0) {
+    g_sel_ns[0] = gtimer();
+    for (int q = 9; q < 16; q += 2) g_sel_ns[q] = 0;
+  }
+  // n / 256 samples, clamped to [4096, 32768]: each sample stands for <= 512
+  // candidates, so the rank-r threshold keeps ~(r + 1) * stride survivors
+  const int64_t want = n / 256 > kSampleMin ? (n / 256 < kSampleMax ? n / 256 : kSampleMax) : kSampleMin;
+  int64_t stride = 1;  // a power of two: the per-candidate sample test is a mask
+  while (stride * want < n) stride <<= 1;
+  // ---- A: K1, a contiguous chunk per CTA (small populations still spread
+  // over every SM: the per-candidate fp64 division chains share each SM's pipe)
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t i_beg = blockIdx.x * chunk;
+  const int64_t i_end = i_beg + chunk < n ? i_beg + chunk : n;
+  bool bad = false;
+  for (int64_t i = i_beg + t; i < i_end; i += blockDim.x) {
+    Factors<NSP, NRED> F;
+    load_cand<NSP, NRED, SEED>(S, src, i, F, false);
+    if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
+    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles);
+    cost[i] = c;
+    if ((i & (stride - 1)) == 0) sample[i / stride] = (uint32_t)(cost_key(c) >> 32);
+  }
+  for (int e = blockIdx.x * blockDim.x + t; e < kFastCap; e += gridDim.x * blockDim.x) rank_acc[e] = 0, dup[e] = 0;
+  if (blockIdx.x == 0 && t < kMaxAttempts) st->att_surv[t] = 0, st->att_dup[t] = 0;
+  if (bad) atomicOr(invalid, 1);
+  grid_barrier(0);
+  if (blockIdx.x == 0 && t == 0) g_sel_ns[1] = gtimer();
+  // ---- B: the sample, every CTA
+  const int ns = (int)((n + stride - 1) / stride);
+  for (int e = t; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
+  __syncthreads();
+  const int lane = t & 31;
+  int status = 0, attempt = 0, m = 0, uniq = 0;
+  bool all = false;
+  for (;; ++attempt) {
+    // expected survivors ~1.5x need (+3 samples): below need only ~3.5 sigma out
+    const int64_t r = (3 * need * ns + 2 * n - 1) / (2 * n) + 3;
+    all = r >= ns - 1;
+    const uint64_t thr = all ? ~0ull : block_sample_threshold(keys, ns, (int)r, hist, hsum, wt);
+    if (blockIdx.x == 0 && t == 0) g_sel_ns[2] = gtimer();
+    if (attempt > 0)
+      for (int e = blockIdx.x * blockDim.x + t; e < kFastCap; e += gridDim.x * blockDim.x) rank_acc[e] = 0, dup[e] = 0;
+    // ---- C: compact this CTA's chunk (its costs are still in L2)
+    uint32_t* surv = &st->att_surv[attempt];
+    for (int64_t base = i_beg; base < i_end; base += blockDim.x) {
+      const int64_t i = base + t;
+      uint64_t key = 0;
+      bool keep = false;
+      if (i < i_end) {
+        key = cost_key(__ldcg(cost + i));
+        keep = key <= thr;
+      }
+      const unsigned msk = __ballot_sync(0xffffffffu, keep);
+      if (!msk) continue;
+      uint32_t pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(surv, (uint32_t)__popc(msk));
+      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+      if (keep) {
+        const uint32_t p = pos0 + __popc(msk & ((1u << lane) - 1u));
+        if (p < (uint32_t)kFastCap) {
+          Factors<NSP, NRED> F;
+          const uint64_t id = load_cand<NSP, NRED, SEED>(S, src, i, F, true);
+          skey[p] = key, sidx[p] = i;
+          sfp[p] = SEED ? id : fingerprint<NSP, NRED>(F);
+        }
+      }
     }
-    __syncthreads();
-    const int e = ce * kRankChunk + threadIdx.x;
-    if (e >= m) continue;
-    const uint64_t ke = skey[e], fe = sfp[e];
-    const int64_t ie = sidx[e];
-    const int jn = min(kRankChunk, m - j0);
-    int below = 0;
-    bool d = false;
-    for (int q = 0; q < jn; ++q) {
-      const uint64_t kq = ck[q];
-      const int64_t iq = ci[q];
-      const bool lt = kq < ke || (kq == ke && iq < ie);
-      below += lt;
-      if (kq == ke && iq < ie && cf[q] == fe && !d) d = same_schedule<NSP, NRED, SEED>(S, src, ie, iq);
+    grid_barrier(attempt == 0 ? 1 : -1);
+    if (blockIdx.x == 0 && t == 0) g_sel_ns[3] = gtimer();
+    const uint32_t m_raw = *(volatile uint32_t*)surv;
+    if (m_raw > (uint32_t)kFastCap) {
+      status = TT_SEL_OVERFLOW;
+      break;
     }
-    if (below) atomicAdd(rank_acc + e, below);
-    if (d) atomicOr(dup + e, 1);
+    m = (int)m_raw;
+    // ---- D: all-pairs ranking in 32 x 32 blocks, one per warp (comparison
+    // keys broadcast by shuffles); block b runs on CTA b % grid, warp b / grid,
+    // so every SM takes one block before any takes two
+    {
+      const int warp = t >> 5;
+      const int chunks = (m + 31) >> 5;
+      for (int blk = warp * gridDim.x + blockIdx.x; blk < chunks * chunks; blk += gridDim.x * (kFastThreads / 32)) {
+        const int ce = blk / chunks, cj = blk - ce * chunks;  // element chunk, comparison chunk
+        const int e = ce * 32 + lane, j = cj * 32 + lane;
+        const bool ev = e < m;
+        const uint64_t ke = ev ? __ldcg(skey + e) : ~0ull, fe = ev ? __ldcg(sfp + e) : 0;
+        const int64_t ie = ev ? __ldcg(sidx + e) : -1;
+        const uint64_t kj = j < m ? __ldcg(skey + j) : ~0ull, fj = j < m ? __ldcg(sfp + j) : 0;
+        const int64_t ij = j < m ? __ldcg(sidx + j) : INT64_MAX;
+        const int jn = min(32, m - cj * 32);
+        int below = 0;
+        bool d = false;
+        for (int q = 0; q < jn; ++q) {
+          const uint64_t kq = __shfl_sync(0xffffffffu, kj, q);
+          const int64_t iq = __shfl_sync(0xffffffffu, ij, q);
+          const uint64_t fq = __shfl_sync(0xffffffffu, fj, q);
+          const bool lt_ = kq < ke || (kq == ke && iq < ie);
+          below += lt_;
+          if (ev && kq == ke && iq < ie && fq == fe && !d) d = same_schedule<NSP, NRED, SEED>(S, src, ie, iq);
+        }
+        if (ev && below) atomicAdd(rank_acc + e, below);
+        if (ev && d && atomicOr(dup + e, 1) == 0) atomicAdd(&st->att_dup[attempt], 1u);
+      }
+    }
+    grid_barrier(attempt == 0 ? 2 : -1);
+    if (blockIdx.x == 0 && t == 0) g_sel_ns[4] = gtimer();
+    uniq = m - (int)*(volatile uint32_t*)&st->att_dup[attempt];
+    const bool everything = all || (int64_t)m >= n;
+    if (uniq >= k || everything) break;
+    if (attempt + 1 == kMaxAttempts) {  // no convergence: the host takes the hash path
+      status = TT_SEL_OVERFLOW;
+      break;
+    }
+    need *= 2;  // duplicates ate the margin: a looser threshold over the same costs
+  }
+  if (status) {
+    if (blockIdx.x == 0 && t == 0) {
+      st->status = status;
+      st->count = 0;
+      *out_count = 0;
+      if constexpr (WITH_ID) out_idx[0] = kRankFailed;  // sharded: the merge reports it on every rank
+      g_sel_ns[5] = gtimer(), g_sel_ns[6] = m, g_sel_ns[7] = attempt + 1;
+    }
+    return;
+  }
+  // ---- E: emit. Position of a unique survivor = its rank minus the
+  // duplicates ranked below it (a bitmap over ranks, prefix popcounts).
+  if (blockIdx.x > 0 && (int64_t)blockIdx.x * blockDim.x >= m) return;
+  for (int w = t; w < kFastCap / 32; w += blockDim.x) dmask[w] = 0;
+  __syncthreads();
+  for (int e = t; e < m; e += blockDim.x)
+    if (__ldcg(dup + e)) {
+      const int r = __ldcg(rank_acc + e);
+      atomicOr(&dmask[r >> 5], 1u << (r & 31));
+    }
+  __syncthreads();
+  for (int w = t; w < kFastCap / 32; w += blockDim.x) dcnt[w] = __popc(dmask[w]);
+  __syncthreads();
+  block_exclusive_scan(dcnt, dpre, kFastCap / 32, wt);
+  __syncthreads();
+  const int e = blockIdx.x * blockDim.x + t;
+  if (e < m && !__ldcg(dup + e)) {
+    const int r = __ldcg(rank_acc + e);
+    const int o = r - (dpre[r >> 5] + __popc(dmask[r >> 5] & ((1u << (r & 31)) - 1u)));
+    if (o < k) {
+      const int64_t i = __ldcg(sidx + e);
+      out_idx[o] = i + src.index_base;
+      out_cost[o] = key_cost(__ldcg(skey + e));
+      if constexpr (WITH_ID) out_id[o] = SEED ? __ldcg(sfp + e) : identity_at<NSP, NRED, SEED>(S, src, i);
+    }
+  }
+  if (blockIdx.x == 0 && t == 0) {
+    const int64_t cnt = uniq < k ? uniq : k;
+    *out_count = cnt;
+    st->count = cnt;
+    st->status = 0;
+    st->all = all ? 1 : 0;
+    st->need = need;
+    g_sel_ns[5] = gtimer(), g_sel_ns[6] = m, g_sel_ns[7] = attempt + 1;
   }
 }
 
-// WITH_ID: also write identities of the emitted entries (sharded rounds);
-// a separate instantiation keeps the common kernel's code small.
-template <int NSP, int NRED, bool SEED, bool WITH_ID>
-__global__ void __launch_bounds__(kFastThreads) k_fsel_emit(DevSketch S, Src src, int64_t n, int64_t k,
-                                                            SelState* __restrict__ st,
-                                                            const uint64_t* __restrict__ skey,
-                                                            const int64_t* __restrict__ sidx,
-                                                            const int* __restrict__ rank_acc,
-                                                            const int* __restrict__ dup,
-                                                            int64_t* __restrict__ out_idx,
-                                                            double* __restrict__ out_cost,
-                                                            uint64_t* __restrict__ out_id,
-                                                            int64_t* __restrict__ out_count) {
-  pdl_wait();
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* a = (uint64_t*)smem;
-  int64_t* bi = (int64_t*)(a + kFastCap);
-  int* flag = (int*)(bi + kFastCap);
-  int* pos = flag + kFastCap;
-  __shared__ int wt[32];
-  // the survivor count and every survivor slot are read together (one memory
-  // round trip): the slot arrays hold kFastCap entries, those >= nsurv unused
-  const uint32_t nsurv = st->nsurv;
-  int r_[kFastE], d_[kFastE];
-  uint64_t k_[kFastE];
-  int64_t b_[kFastE];
-#pragma unroll
-  for (int q = 0; q < kFastE; ++q) {
-    const int e = threadIdx.x + q * kFastThreads;
-    r_[q] = rank_acc[e], k_[q] = skey[e], b_[q] = sidx[e], d_[q] = dup[e];
-  }
-  if (threadIdx.x == 0) g_sel_ns[5] = gtimer(), g_sel_ns[7] = nsurv;
-  if (nsurv > (uint32_t)kFastCap) {
-    if (threadIdx.x == 0) st->status |= TT_SEL_OVERFLOW, *out_count = 0;
-    return;
-  }
-  const int m = (int)nsurv;
-  for (int e = threadIdx.x; e < kFastCap; e += blockDim.x) flag[e] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) g_sel_ns[8] = gtimer();
-#pragma unroll
-  for (int q = 0; q < kFastE; ++q) {
-    const int e = threadIdx.x + q * kFastThreads;
-    if (e < m) {
-      const int r = r_[q];  // a permutation of 0..m-1: (cost, index) keys are distinct
-      a[r] = k_[q];
-      bi[r] = b_[q];
-      flag[r] = d_[q] ? 0 : 1;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) g_sel_ns[9] = gtimer();
-  const int total = block_exclusive_scan(flag, pos, kFastCap, wt);
-  if (threadIdx.x == 0) g_sel_ns[10] = gtimer();
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    if (flag[e] && pos[e] < k) {
-      const int o = pos[e];
-      out_idx[o] = bi[e] + src.index_base;
-      out_cost[o] = key_cost(a[e]);
-      if constexpr (WITH_ID) out_id[o] = identity_at<NSP, NRED, SEED>(S, src, bi[e]);
-    }
-  }
-  if (threadIdx.x == 0) g_sel_ns[11] = gtimer();
-  if (threadIdx.x == 0) {
-    const int64_t cnt = total < k ? total : k;
-    *out_count = cnt;
-    st->count = cnt;
-    const bool everything = st->all || (int64_t)m >= n;
-    if (cnt < k && !everything) st->status |= TT_SEL_NEED_MORE;  // duplicates ate the margin
-    g_sel_ns[6] = gtimer();
-  }
-}
+static int g_num_sms = 0;
 
 template <int NSP, int NRED, bool SEED>
 static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
                      int64_t need, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
                      int64_t* out_count, cudaStream_t st) {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  constexpr size_t smem = kSampleMax * sizeof(uint32_t);
+  static bool init = false;
+  if (!init) {
+    set_smem(k_fsel<NSP, NRED, SEED, true>, smem), set_smem(k_fsel<NSP, NRED, SEED, false>, smem);
+    init = true;
+  }
+  // one CTA per SM (co-resident: a cooperative launch), >= 64 candidates each
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g_num_sms, n / 64));
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid), cfg.blockDim = dim3(kFastThreads), cfg.dynamicSmemBytes = smem, cfg.stream = st;
+  cfg.attrs = &attr, cfg.numAttrs = 1;
   if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);
   tt::note_launch();
-  static bool init_cost = false;
-  if (!init_cost) set_smem(k_fsel_cost<NSP, NRED, SEED>, kSampleMax * sizeof(uint32_t)), init_cost = true;
-  k_fsel_cost<NSP, NRED, SEED><<<grid_for(n, 128, 148), kFastThreads, kSampleMax * sizeof(uint32_t), st>>>(S, D, src, n, toggles, need, w.cost, w.sample, w.state,
-                                                          w.rank, w.dup, w.invalid);
-  if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
-  tt::note_launch();
-  launch_pdl(k_fsel_compact<NSP, NRED, SEED>, dim3(grid_for(n, 256, 148 * 4)), dim3(256), 0, st, S, src, w.cost, n,
-             w.state, w.skey, w.sidx, w.sfp);
-  tt::note_launch();
-  launch_pdl(k_fsel_rank<NSP, NRED, SEED>, dim3(2 * 148), dim3(kRankChunk), 0, st, S, src, w.state, w.skey, w.sidx,
-             w.sfp, w.rank, w.dup);
-  constexpr size_t emit_smem = (size_t)kFastCap * (2 * sizeof(uint64_t) + 2 * sizeof(int));
-  static bool init = false;
-  if (!init) set_smem(k_fsel_emit<NSP, NRED, SEED, true>, emit_smem), set_smem(k_fsel_emit<NSP, NRED, SEED, false>, emit_smem), init = true;
-  tt::note_launch();
   if (out_id)
-    launch_pdl(k_fsel_emit<NSP, NRED, SEED, true>, dim3(1), dim3(kFastThreads), emit_smem, st, S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
-                                                          out_idx, out_cost, out_id, out_count);
+    cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, true>, S, D, src, n, toggles, k, need, w.cost, w.sample, w.state,
+                       w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id, out_count);
   else
-    launch_pdl(k_fsel_emit<NSP, NRED, SEED, false>, dim3(1), dim3(kFastThreads), emit_smem, st, S, src, n, k, w.state, w.skey, w.sidx, w.rank, w.dup,
-                                                          out_idx, out_cost, out_id, out_count);
+    cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, false>, S, D, src, n, toggles, k, need, w.cost, w.sample,
+                       w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id,
+                       out_count);
+  if (w.k1_ev[1]) cudaEventRecord(w.k1_ev[1], st);
 }
 
 // ---------------------------------------------- hash fallback (ties) ----
@@ -904,7 +895,8 @@ __global__ void __launch_bounds__(1024) k_sel_finalize_hash(const double* __rest
 __global__ void __launch_bounds__(1024) k_merge(const double* __restrict__ cost, const int64_t* __restrict__ gidx,
                                                 const uint64_t* __restrict__ id, int m, int64_t k,
                                                 int64_t* __restrict__ out_idx, double* __restrict__ out_cost,
-                                                uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count) {
+                                                uint64_t* __restrict__ out_id, int64_t* __restrict__ out_count,
+                                                SelState* __restrict__ st) {
   extern __shared__ __align__(16) unsigned char smem[];
   SortSmem sm = carve_sort(smem, kSurvivorCap);
   __shared__ int wt[32];
@@ -916,6 +908,7 @@ __global__ void __launch_bounds__(1024) k_merge(const double* __restrict__ cost,
 #pragma unroll
   for (int e = 0; e < kSortE; ++e) {
     const int p = e * blockDim.x + threadIdx.x;
+    if (st && p < m && gidx[p] == kRankFailed) atomicOr(&st->status, TT_SEL_OVERFLOW);
     const bool v = p < m && gidx[p] >= 0;  // negative index = empty slot
     // position p in the low 12 bits finds the identity after the sort;
     // global indices < 2^51 keep the (index, p) order = index order
@@ -936,6 +929,103 @@ __global__ void __launch_bounds__(1024) k_merge(const double* __restrict__ cost,
   }
   __syncthreads();
   dedup_emit(sm.a, sm.b, sm.c, sm.flag, sm.pos, wt, valid, kSurvivorCap, k, 0, out_idx, out_cost, out_id, out_count);
+}
+
+// Merge of R = m / k per-rank lists, each ascending by (cost key, global
+// index) with its valid entries first (what tt_round_local_async emits):
+// m up to kMergeMax, beyond the one-CTA sort. Global indices are disjoint
+// across ranks, so (cost, index) keys are distinct and an entry's merged rank
+// is its own list position plus, for every other list, the number of that
+// list's entries below it. CTA (r, q) stages list q in shared memory and
+// binary-searches it for every entry of list r; an entry is a duplicate when
+// an equal-cost entry of another list with a lower index carries the same
+// identity (same schedule => same cost). Within a list entries are unique.
+constexpr int kMergeListMax = 8192;  // entries per list staged in shared memory
+
+__global__ void __launch_bounds__(512) k_merge_rank(const double* __restrict__ cost, const int64_t* __restrict__ gidx,
+                                                    const uint64_t* __restrict__ id, int R, int64_t k,
+                                                    int32_t* __restrict__ rank, int32_t* __restrict__ dup,
+                                                    SelState* __restrict__ st) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* qk = (uint64_t*)smem;  // list q: cost keys
+  int64_t* qi = (int64_t*)(qk + k);  // list q: global indices
+  __shared__ int lq;
+  const int r = blockIdx.x / R, q = blockIdx.x - (blockIdx.x / R) * R;
+  const int64_t* gq = gidx + (int64_t)q * k;
+  const int64_t* gr = gidx + (int64_t)r * k;
+  if (threadIdx.x == 0) lq = (int)k;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const int64_t g = gq[j];
+    qk[j] = cost_key(cost[(int64_t)q * k + j]);
+    qi[j] = g;
+    if (g < 0 && (j == 0 || gq[j - 1] >= 0)) lq = (int)j;  // the first empty slot
+  }
+  if (st && q == r && threadIdx.x == 0 && gr[0] == kRankFailed) atomicOr(&st->status, TT_SEL_OVERFLOW);
+  __syncthreads();
+  const int L = lq;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const int64_t ge = gr[j];
+    if (ge < 0) continue;
+    const int64_t e = (int64_t)r * k + j;
+    if (q == r) {  // own list: its position
+      atomicAdd(rank + e, (int)j);
+      continue;
+    }
+    const uint64_t ke = cost_key(cost[e]);
+    int lo = 0, hi = L;  // first position with (key, index) >= (ke, ge)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const bool below = qk[mid] < ke || (qk[mid] == ke && qi[mid] < ge);
+      if (below) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo) atomicAdd(rank + e, lo);
+    // equal-cost entries of list q with a lower index, nearest first
+    const uint64_t ie = id[e];
+    for (int p = lo - 1; p >= 0 && qk[p] == ke; --p)
+      if (id[(int64_t)q * k + p] == ie) {
+        atomicOr(dup + e, 1);
+        break;
+      }
+  }
+}
+
+// Scatter to merged order and emit the first kout non-duplicates (one CTA;
+// merged positions are walked in chunks until kout entries are out).
+__global__ void __launch_bounds__(1024) k_merge_emit(const double* __restrict__ cost, const int64_t* __restrict__ gidx,
+                                                     const uint64_t* __restrict__ id, int64_t m, int64_t kout,
+                                                     const int32_t* __restrict__ rank, const int32_t* __restrict__ dup,
+                                                     int32_t* __restrict__ ord, int64_t* __restrict__ out_idx,
+                                                     double* __restrict__ out_cost, uint64_t* __restrict__ out_id,
+                                                     int64_t* __restrict__ out_count) {
+  __shared__ int flag[1024], pos[1024], wt[32], nvalid;
+  if (threadIdx.x == 0) nvalid = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int64_t e = threadIdx.x; e < m; e += blockDim.x)
+    if (gidx[e] >= 0) ord[rank[e]] = (int32_t)e, ++mine;
+  if (mine) atomicAdd(&nvalid, mine);
+  __threadfence_block();
+  __syncthreads();
+  const int M = nvalid;
+  int64_t done = 0;
+  for (int base = 0; base < M && done < kout; base += blockDim.x) {
+    const int p = base + threadIdx.x;
+    const int e = p < M ? ord[p] : -1;
+    flag[threadIdx.x] = e >= 0 && !dup[e];
+    __syncthreads();
+    const int tot = block_exclusive_scan(flag, pos, blockDim.x, wt);
+    if (e >= 0 && flag[threadIdx.x] && done + pos[threadIdx.x] < kout) {
+      const int64_t o = done + pos[threadIdx.x];
+      out_idx[o] = gidx[e];
+      out_cost[o] = cost[e];
+      if (out_id) out_id[o] = id[e];
+    }
+    done += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out_count = done < kout ? done : kout;
 }
 
 // ------------------------------------------------------------ launchers ----
@@ -1070,19 +1160,37 @@ int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, 
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
 }
 
-int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
-                 double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st) {
-  if (m > kSurvivorCap) return -1;
-  const size_t sm = sort_smem_bytes(kSurvivorCap);
+int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k, int64_t* out_idx,
+                 double* out_cost, uint64_t* out_id, int64_t* out_count, SelState* state, int32_t* scratch,
+                 cudaStream_t st) {
+  if (m <= kSurvivorCap) {
+    const size_t sm = sort_smem_bytes(kSurvivorCap);
+    static bool init = false;
+    if (!init) set_smem(k_merge, sm), init = true;
+    tt::note_launch();
+    k_merge<<<1, kSurvivorCap / kSortE, sm, st>>>(cost, gidx, id, (int)m, k, out_idx, out_cost, out_id, out_count,
+                                                  state);
+    return 0;
+  }
+  if (m > kMergeMax || k < 1 || k > kMergeListMax || m % k) return -1;
+  const int R = (int)(m / k);
+  int32_t* rank = scratch;
+  int32_t* dup = scratch + m;
+  if (cudaMemsetAsync(scratch, 0, sizeof(int32_t) * 2 * m, st) != cudaSuccess) return -1;
+  const size_t sm = (size_t)k * 16;
   static bool init = false;
-  if (!init) set_smem(k_merge, sm), init = true;
+  if (!init) set_smem(k_merge_rank, (size_t)kMergeListMax * 16), init = true;
   tt::note_launch();
-  k_merge<<<1, kSurvivorCap / kSortE, sm, st>>>(cost, gidx, id, m, k, out_idx, out_cost, out_id, out_count);
+  k_merge_rank<<<R * R, 512, sm, st>>>(cost, gidx, id, R, k, rank, dup, state);
+  // merged order reuses the duplicate flags' successor: ord lives after rank/dup
+  tt::note_launch();
+  k_merge_emit<<<1, 1024, 0, st>>>(cost, gidx, id, m, k, rank, dup, scratch + 2 * m, out_idx, out_cost, out_id,
+                                   out_count);
   return 0;
 }
 
 }  // namespace tt
 
 extern "C" int ttdbg_select_clocks(unsigned long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 12 ? n : 12));
+  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 16 ? n : 16));
 }

@@ -17,7 +17,10 @@ namespace tt {
 constexpr int kSelTile = 4096;
 constexpr uint64_t kAll = ~0ull;
 
+// -0.0 and +0.0 map to one key: the reference comparator (scores[a] !=
+// scores[c]) treats them as equal and falls through to the draft cost
 __device__ __forceinline__ uint64_t ordered(double x) {
+  if (x == 0.0) x = 0.0;
   const uint64_t u = (uint64_t)__double_as_longlong(x);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
@@ -302,9 +305,10 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
                                                  const int64_t* __restrict__ n_dev, int64_t b,
                                                  const int64_t* __restrict__ idx, const uint64_t* __restrict__ id,
                                                  const SelState* __restrict__ sel, const int* __restrict__ rescored,
-                                                 int64_t* __restrict__ out) {
+                                                 const double* __restrict__ fast, int64_t* __restrict__ out) {
   __shared__ Key3 lists[32][33];
   __shared__ int avail;
+  __shared__ unsigned long long band_err;
   __shared__ int16_t rank_of[1024];  // output position of each selected candidate, -1 otherwise
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
   // every global read issued up front, independent of each other (one
@@ -318,11 +322,18 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
   const uint64_t id_t = in && id ? id[t] : 0;
   const int64_t st = t == 0 && sel ? (int64_t)sel->status : 0;
   const int64_t rs = t == 0 && rescored ? (int64_t)*rescored : 0;
-  if (t == 0) avail = 0;
+  const double f_t = in && fast ? fast[t] : 0.0;
+  if (t == 0) avail = 0, band_err = 0ull;
   rank_of[t] = -1;
   __syncthreads();
   const int64_t n = nd < n_max ? nd : n_max;
   const bool ok = t < n && !ex_t;
+  if (fast) {  // the certification's premise, checked on the rescored set
+    double err = ok ? fabs(s_t - f_t) : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, off));
+    if (lane == 0 && err > 0.0) atomicMax(&band_err, (unsigned long long)__double_as_longlong(err));
+  }
   Key3 k;
   k.a = ok ? ~ordered(s_t) : kAll;
   k.b = ok ? ordered(d_t) : kAll;
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
     }
   }
   __syncthreads();
-  int64_t* ix = out + 4;
+  int64_t* ix = out + kRecHead;
   double* sc = (double*)(ix + b);
   double* co = sc + b;
   uint64_t* ids = (uint64_t*)(co + b);
@@ -365,6 +376,8 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
     out[1] = n;
     out[2] = st;
     out[3] = rs;
+    out[4] = 0;
+    out[5] = (int64_t)band_err;
   }
 }
 
@@ -436,11 +449,11 @@ int launch_cert_band(const double* fast, const double* drafts, int64_t n_max, co
 
 int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
                   const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
-                  const int* rescored, int64_t* out, cudaStream_t st) {
+                  const int* rescored, const double* fast, int64_t* out, cudaStream_t st) {
   if (n_max > 1024 || b > 32 || b > n_max) return -1;
   const int nt = (int)((n_max + 31) / 32 * 32);
   tt::note_launch();
-  k_finish<<<1, nt, 0, st>>>(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, out);
+  k_finish<<<1, nt, 0, st>>>(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, fast, out);
   return 0;
 }
 
@@ -453,17 +466,31 @@ __global__ void k_gather(const int64_t* __restrict__ pos, const int64_t* __restr
                          const int64_t* __restrict__ drafted_count, const SelState* __restrict__ sel,
                          const int* __restrict__ status_b, const int* __restrict__ rescored,
                          const int64_t* __restrict__ idx, const double* __restrict__ cost,
-                         const uint64_t* __restrict__ id, const double* __restrict__ scores, int64_t b,
-                         int64_t* __restrict__ out) {
+                         const uint64_t* __restrict__ id, const double* __restrict__ scores,
+                         const double* __restrict__ fast, const uint8_t* __restrict__ excluded, int64_t n_max,
+                         int64_t b, int64_t* __restrict__ out) {
+  __shared__ unsigned long long band_err;
   const int64_t cnt = *pos_count;
   const int t = threadIdx.x;
+  if (t == 0) band_err = 0ull;
+  __syncthreads();
+  if (fast) {  // max |exact - fast| over the rescored (not excluded) candidates
+    const int64_t nd = *drafted_count < n_max ? *drafted_count : n_max;
+    double err = 0.0;
+    for (int64_t i = t; i < nd; i += blockDim.x)
+      if (!(excluded && excluded[i])) err = fmax(err, fabs(scores[i] - fast[i]));
+    if (err > 0.0) atomicMax(&band_err, (unsigned long long)__double_as_longlong(err));
+  }
+  __syncthreads();
   if (t == 0) {
     out[0] = cnt;
     out[1] = *drafted_count;
     out[2] = (int64_t)((sel ? sel->status : 0) | ((status_b ? *status_b : 0) << 8));
     out[3] = rescored ? *rescored : 0;
+    out[4] = 0;
+    out[5] = (int64_t)band_err;
   }
-  int64_t* ix = out + 4;
+  int64_t* ix = out + kRecHead;
   double* sc = (double*)(ix + b);
   double* co = sc + b;
   uint64_t* ids = (uint64_t*)(co + b);
@@ -483,8 +510,10 @@ __global__ void k_gather(const int64_t* __restrict__ pos, const int64_t* __restr
 
 int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
                   const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
-                  const uint64_t* id, const double* scores, int64_t b, int64_t* out, cudaStream_t st) {
-  tt::note_launch(), k_gather<<<1, 128, 0, st>>>(pos, pos_count, drafted_count, sel, status_b, rescored, idx, cost, id, scores, b, out);
+                  const uint64_t* id, const double* scores, const double* fast, const uint8_t* excluded,
+                  int64_t n_max, int64_t b, int64_t* out, cudaStream_t st) {
+  tt::note_launch(), k_gather<<<1, 128, 0, st>>>(pos, pos_count, drafted_count, sel, status_b, rescored, idx, cost, id,
+                                                 scores, fast, excluded, n_max, b, out);
   return 0;
 }
 

@@ -69,8 +69,8 @@ struct tt_ctx {
   size_t mix_cap = 0;
   // rounds in flight: each enqueued round copies its record into its own
   // pinned ring slot and records its own event, so a caller can keep up to
-  // kRing rounds in flight and collect them in order (the oldest uncollected
-  // round is dropped when the ring wraps)
+  // kRing rounds in flight and collect them in order (a 17th enqueue fails
+  // with E_STATE until the oldest is collected)
   static constexpr int kRing = 16;
   struct Pending {
     int slot;
@@ -81,6 +81,11 @@ struct tt_ctx {
     tt_device_spec dev;
     const int32_t* soa;
     uint64_t seed;
+    // merged rounds: the gathered lists (caller-owned until collected)
+    const double* m_cost;
+    const int64_t* m_gidx;
+    const uint64_t* m_id;
+    int64_t m;
   };
   std::deque<Pending> pend;
   int ring_next = 0;
@@ -370,32 +375,37 @@ int ensure_k(tt_ctx* ctx, int64_t k) {
 
 int ensure_b(tt_ctx* ctx, int64_t b) {
   if (b <= ctx->b_cap) return TT_OK;
-  // rounds in flight still copy into the old record buffers: finish them first
-  if (!ctx->pend.empty()) TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  ctx->pend.clear();
+  // rounds in flight copy their records into the old pinned slots: let them
+  // land, then carry each pending record over into the new, larger slot
+  for (const auto& p : ctx->pend) TT_CUDA(ctx, cudaEventSynchronize(ctx->ev_rec[p.slot]));
   graphs_clear(ctx);
   cudaFree(ctx->d_pos), cudaFree(ctx->d_pos_fast), cudaFree(ctx->d_record);
-  for (int r = 0; r < tt_ctx::kRing; ++r)
-    if (ctx->h_rec[r]) cudaFreeHost(ctx->h_rec[r]), ctx->h_rec[r] = nullptr;
+  ctx->d_pos = ctx->d_pos_fast = nullptr, ctx->d_record = nullptr;
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos, sizeof(int64_t) * b));
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos_fast, sizeof(int64_t) * b));
-  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_record, sizeof(int64_t) * (4 + 4 * b)));
-  for (int r = 0; r < tt_ctx::kRing; ++r)
-    TT_CUDA(ctx, cudaMallocHost((void**)&ctx->h_rec[r], sizeof(int64_t) * (4 + 4 * b)));
+  TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_record, sizeof(int64_t) * record_words(b)));
+  for (int r = 0; r < tt_ctx::kRing; ++r) {
+    int64_t* nh = nullptr;
+    TT_CUDA(ctx, cudaMallocHost((void**)&nh, sizeof(int64_t) * record_words(b)));
+    if (ctx->h_rec[r]) {
+      std::memcpy(nh, ctx->h_rec[r], sizeof(int64_t) * record_words(ctx->b_cap));
+      cudaFreeHost(ctx->h_rec[r]);
+    }
+    ctx->h_rec[r] = nh;
+  }
   ctx->b_cap = b;
   return TT_OK;
 }
 
 // Claims the next ring slot for a round about to be enqueued (record_copy
-// lands its record and validity flag there).
-int ring_claim(tt_ctx* ctx) {
-  const int slot = ctx->ring_next;
-  for (auto it = ctx->pend.begin(); it != ctx->pend.end(); ++it)
-    if (it->slot == slot) {  // the ring wrapped: drop the oldest uncollected round
-      ctx->pend.erase(ctx->pend.begin(), it + 1);
-      break;
-    }
-  return slot;
+// lands its record and validity flag there). A full ring is an error: the
+// caller collects before enqueueing a 17th round.
+int ring_claim(tt_ctx* ctx, int* slot) {
+  for (const auto& p : ctx->pend)
+    if (p.slot == ctx->ring_next)
+      return fail(ctx, TT_E_STATE, "round: 16 rounds already in flight on this context (tt_round_collect first)");
+  *slot = ctx->ring_next;
+  return TT_OK;
 }
 
 void ring_push(tt_ctx* ctx, tt_ctx::Pending p) {
@@ -520,12 +530,13 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (const char* g = getenv("TT_GRAPHS")) c->graphs = g[0] != '0';
   if (bad(cudaMalloc((void**)&c->sel.hist, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.hist, 0, 4096 * sizeof(uint32_t)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->sel.skey, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->sel.sidx, 4096 * sizeof(int64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.skey, 8192 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.sidx, 8192 * sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.sample, 32768 * sizeof(uint32_t)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->sel.sfp, 4096 * sizeof(uint64_t)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->sel.rank, 4096 * sizeof(int)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->sel.dup, 4096 * sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.sfp, 8192 * sizeof(uint64_t)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.rank, 8192 * sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.dup, 8192 * sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->sel.mscratch, kMergeMax * 3 * sizeof(int32_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.tkeys, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.tvals, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.tkeys, 0xff, 16384 * sizeof(uint64_t)))) return TT_E_CUDA;
@@ -550,7 +561,7 @@ void tt_ctx_destroy(tt_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (auto& pr : c->ev_live) cudaEventDestroy(pr.second.first), cudaEventDestroy(pr.second.second);
-  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.skey, c->sel.sidx, c->sel.sample, c->sel.sfp, c->sel.rank, c->sel.dup, c->sel.tkeys, c->sel.tvals, c->sel.state,
+  void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.skey, c->sel.sidx, c->sel.sample, c->sel.sfp, c->sel.rank, c->sel.dup, c->sel.tkeys, c->sel.tvals, c->sel.state, c->sel.mscratch,
                   c->sel.invalid,
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
@@ -712,8 +723,12 @@ int tt_explore1(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, uin
 int tt_topk_merge(tt_ctx* ctx, const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k,
                   int64_t* idx, double* out_cost, uint64_t* out_id, int64_t* count) {
   if (!ctx) return TT_E_STATE;
-  if (m < 0 || m > 4096) return fail(ctx, TT_E_STATE, "merge: at most 4096 gathered entries per call");
-  if (launch_merge(cost, gidx, id, (int)m, k, idx, out_cost, out_id, ctx->d_count, ctx->stream))
+  if (m < 0 || m > kMergeMax)
+    return fail(ctx, TT_E_STATE, "merge: at most " + std::to_string(kMergeMax) + " gathered entries per call");
+  if (m > kMergeSortMax && (k < 1 || m % k))
+    return fail(ctx, TT_E_STATE, "merge: more than 4096 entries must be whole per-rank lists of k");
+  if (launch_merge(cost, gidx, id, m, k, idx, out_cost, out_id, ctx->d_count, nullptr, ctx->sel.mscratch,
+                   ctx->stream))
     return fail(ctx, TT_E_STATE, "merge: launch");
   TT_LAUNCHED(ctx);
   TT_CUDA(ctx, cudaMemcpyAsync(count, ctx->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -870,21 +885,23 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
     TT_LAUNCHED(ctx);
     TT_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
   }
-  int rc = score_drafted(ctx, S, D, ref, cfg->k, cfg->precision, cfg->b, cfg->band > 0 ? cfg->band : 0.05,
+  int rc = score_drafted(ctx, S, D, ref, cfg->k, cfg->precision, cfg->b, cfg->band,
                          ctx->d_count);
   if (rc) return rc;
   const bool certified = cfg->precision != TT_PREC_FP64;
   prof_begin(ctx, 3);
   if (!by_id) TT_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));  // join
   const uint8_t* excl = certified ? ctx->d_excluded : nullptr;
+  const double* fast = certified ? ctx->d_score_fast : nullptr;
   if (launch_finish(ctx->d_score, ctx->d_cost, excl, cfg->k, ctx->d_count, cfg->b, ctx->d_idx, ctx->d_id,
-                    ctx->sel.state, ctx->d_sublist_count, ctx->d_record, ctx->stream)) {
+                    ctx->sel.state, ctx->d_sublist_count, fast, ctx->d_record, ctx->stream)) {
     // large draft sets / batches: tiled select_top, then the record gather
     if (launch_select_top(ctx->d_score, ctx->d_cost, excl, cfg->k, ctx->d_count, cfg->b, ctx->d_pos,
                           ctx->d_pos_count, ctx->d_status, ctx->stream))
       return fail(ctx, TT_E_CONFIG, "select_top: draft_size too large for the batch");
     launch_gather(ctx->d_pos, ctx->d_pos_count, ctx->d_count, ctx->sel.state, nullptr, ctx->d_sublist_count,
-                  ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, cfg->b, ctx->d_record, ctx->stream);
+                  ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, fast, excl, cfg->k, cfg->b, ctx->d_record,
+                  ctx->stream);
   }
   prof_end(ctx, 3);
   TT_LAUNCHED(ctx);
@@ -894,7 +911,7 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
 // The round's record and validity flag into its ring slot, then its event.
 // Outside any graph (the slot changes every round; the graphs do not).
 int record_copy(tt_ctx* ctx, int slot, int64_t b) {
-  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_rec[slot], ctx->d_record, sizeof(int64_t) * (4 + 4 * b), cudaMemcpyDeviceToHost,
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_rec[slot], ctx->d_record, sizeof(int64_t) * record_words(b), cudaMemcpyDeviceToHost,
                                ctx->stream));
   TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_inv[slot], ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   TT_CUDA(ctx, cudaEventRecord(ctx->ev_rec[slot], ctx->stream));
@@ -907,6 +924,8 @@ int check_round_cfg(tt_ctx* ctx, const tt_round_config* cfg) {
   if (cfg->b < 1) return fail(ctx, TT_E_CONFIG, "batch must be >= 1");
   if (cfg->k < cfg->b) return fail(ctx, TT_E_CONFIG, "draft_size must be >= batch");
   if (cfg->n < 2) return fail(ctx, TT_E_CONFIG, "pop_size must be >= 2");
+  if (cfg->precision == TT_PREC_BF16 && !(cfg->band > 0.0))
+    return fail(ctx, TT_E_CONFIG, "bf16 round: the certification band must be > 0 (a bound on |bf16 - fp64| scores)");
   if (!ctx->d_params) return fail(ctx, TT_E_STATE, "round: tt_pacm_load first");
   return TT_OK;
 }
@@ -933,8 +952,11 @@ int round_body(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_rou
   return verify_and_select(ctx, S, D, cfg, ref);
 }
 
+// retry_slot >= 0: a synchronous re-run of a collected round into its own
+// (already popped) ring slot; nothing is pushed
 int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
-                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need, bool hash = false) {
+                  const int32_t* soa, int64_t ld, uint64_t seed, int64_t need, bool hash = false,
+                  int retry_slot = -1) {
   DevSketch S;
   DevDevice D;
   int rc = compile_sketch(ctx, sk, S);
@@ -947,7 +969,8 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   if ((rc = ensure_feat(ctx, cfg->k))) return rc;
   if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
   if (cfg->precision == TT_PREC_BF16 && (rc = ensure_packed(ctx))) return rc;
-  const int slot = ring_claim(ctx);
+  int slot = retry_slot;
+  if (slot < 0 && (rc = ring_claim(ctx, &slot))) return rc;
   if (!ctx->graphs || ctx->prof) {
     if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash))) return rc;
   } else {
@@ -989,32 +1012,45 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   }
   // outside any capture: the record into this round's ring slot, then its event
   if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
-  ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, need, ld, hash, false, *cfg, *sk, *dev, soa, seed});
+  if (retry_slot < 0)
+    ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, need, ld, hash, false, *cfg, *sk, *dev, soa, seed,
+                                   nullptr, nullptr, nullptr, 0});
   return TT_OK;
 }
 
-int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* sel_cost, uint64_t* sel_id,
-                  tt_round_result* res, bool allow_retry) {
+int merged_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                   const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int retry_slot = -1);
+
+// The oldest round in flight into the caller's buffers (capacity entries
+// each). A round whose selector ran out of margin (NEED_MORE: duplicates;
+// OVERFLOW: > 4096 ties at the threshold) is re-run synchronously with a
+// larger target / the hash path; a tensor-core round whose observed score
+// error on the rescored set exceeds its band is re-run in fp64. Both re-runs
+// reuse the round's own ring slot.
+int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel_score, double* sel_cost,
+                  uint64_t* sel_id, tt_round_result* res, bool allow_retry) {
   if (ctx->pend.empty()) return fail(ctx, TT_E_STATE, "round: nothing enqueued");
-  // the oldest round in flight; wait for it only (the stream may already hold later rounds)
   const tt_ctx::Pending p = ctx->pend.front();
+  if (p.b > capacity)
+    return fail(ctx, TT_E_CONFIG, "round_collect: the oldest round selects " + std::to_string(p.b) +
+                                      " candidates, the buffers hold " + std::to_string(capacity));
   ctx->pend.pop_front();
-  int rc = TT_OK;
-  {
+  // wait for this round only (the stream may already hold later rounds)
+  auto wait_slot = [&]() -> int {
     const cudaError_t e1 = cudaEventSynchronize(ctx->ev_rec[p.slot]);
     const cudaError_t e2 = cudaGetLastError();
     if (e1 != cudaSuccess || e2 != cudaSuccess)
-      rc = fail(ctx, TT_E_CUDA, std::string("round: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
-  }
+      return fail(ctx, TT_E_CUDA, std::string("round: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    return TT_OK;
+  };
+  int rc = wait_slot();
   if (rc) return rc;
   const int64_t b = p.b;
   const int64_t* rec = ctx->h_rec[p.slot];
   const int* inv = ctx->h_inv[p.slot];
+  int retries = 0, extra = 0;
   const int retry_mask = TT_SEL_NEED_MORE | TT_SEL_OVERFLOW;
   if (((int)rec[2] & retry_mask) && allow_retry && !p.merged) {
-    // NEED_MORE: duplicates consumed the selector's margin → raise the
-    // target; OVERFLOW: > 4096 keys tie at the threshold → hash path.
-    // Re-run synchronously (behind any rounds still in flight).
     int64_t need = p.need;
     bool hash = p.hash;
     bool ok = false;
@@ -1027,24 +1063,33 @@ int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* se
         need *= 2;
       }
       tt_round_config cfg = p.cfg;
-      if ((rc = round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, need, hash))) return rc;
-      const tt_ctx::Pending q = ctx->pend.back();
-      ctx->pend.pop_back();
-      if ((rc = sync_check(ctx))) return rc;
-      rec = ctx->h_rec[q.slot], inv = ctx->h_inv[q.slot];
+      if ((rc = round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, need, hash, p.slot))) return rc;
+      if ((rc = wait_slot())) return rc;
+      ++retries;
       ok = !((int)rec[2] & retry_mask);
     }
     if (!ok && ((int)rec[2] & TT_SEL_NEED_MORE))
       return fail(ctx, TT_E_STATE, "draft selector did not converge");
   }
-  const int status = (int)rec[2];
-  const int sel_status = status & 0xff;
-  if (sel_status & TT_SEL_OVERFLOW)
+  if ((int)rec[2] & TT_SEL_OVERFLOW)
     return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
-  if (p.soa && *inv)
-    return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
+  if (p.soa && *inv) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
+  double band_err;
+  std::memcpy(&band_err, rec + 5, sizeof(double));
+  if (p.cfg.precision != TT_PREC_FP64 && band_err > p.cfg.band && allow_retry) {
+    // the observed bf16 error on the rescored set exceeds the certified band:
+    // the exclusions are not certified, so the round is re-run in fp64
+    tt_round_config cfg = p.cfg;
+    cfg.precision = TT_PREC_FP64;
+    rc = p.merged ? merged_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.m_cost, p.m_gidx, p.m_id, p.m, p.slot)
+                  : round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, p.need, p.hash, p.slot);
+    if (rc) return rc;
+    if ((rc = wait_slot())) return rc;
+    extra |= TT_ROUND_BAND_RERUN;
+    if ((int)rec[2] & retry_mask) return fail(ctx, TT_E_STATE, "draft selector: fp64 re-run did not converge");
+  }
   const int64_t selected = rec[0];
-  const int64_t* ix = rec + 4;
+  const int64_t* ix = rec + kRecHead;
   const double* sc = (const double*)(ix + b);
   const double* co = sc + b;
   const uint64_t* ids = (const uint64_t*)(co + b);
@@ -1058,9 +1103,45 @@ int round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* se
     res->selected = selected;
     res->drafted = rec[1];
     res->rescored = rec[3];
-    res->status = status;
+    res->status = (int32_t)rec[2] | extra;
+    res->retries = retries + (int32_t)rec[4];
+    res->band_err = band_err;
   }
   g_forward_calls.fetch_add((uint64_t)rec[1], std::memory_order_relaxed);
+  return TT_OK;
+}
+
+int merged_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                   const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int retry_slot) {
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if ((rc = check_round_cfg(ctx, cfg))) return rc;
+  if (m < 0 || m > kMergeMax)
+    return fail(ctx, TT_E_STATE, "merge: at most " + std::to_string(kMergeMax) + " gathered entries per call");
+  if (m > kMergeSortMax && m % cfg->k)
+    return fail(ctx, TT_E_STATE, "merge: more than 4096 entries must be whole per-rank lists of k");
+  if ((rc = ensure_k(ctx, cfg->k))) return rc;
+  if ((rc = ensure_b(ctx, cfg->b))) return rc;
+  if (cfg->precision == TT_PREC_BF16 && (rc = ensure_packed(ctx))) return rc;
+  int slot = retry_slot;
+  if (slot < 0 && (rc = ring_claim(ctx, &slot))) return rc;
+  prof_begin(ctx, 4);
+  if (launch_merge(cost, gidx, id, m, cfg->k, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->sel.state,
+                   ctx->sel.mscratch, ctx->stream))
+    return fail(ctx, TT_E_STATE, "merge launch");
+  prof_end(ctx, 4);
+  TT_LAUNCHED(ctx);
+  CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
+  if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
+  // no selector retry: the local lists are the ranks' own (a rank that could
+  // not certify its list marks it, and the merge reports OVERFLOW)
+  if (retry_slot < 0)
+    ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, -1, 0, false, true, *cfg, *sk, *dev, nullptr, 0, cost, gidx,
+                                   id, m});
   return TT_OK;
 }
 
@@ -1391,18 +1472,20 @@ int tt_round_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, 
   return round_enqueue(ctx, sk, dev, cfg, soa, ld, seed, cfg->k + cfg->k / 8 + 16);
 }
 
-int tt_round_collect(tt_ctx* ctx, int64_t* sel_index, double* sel_score, double* sel_cost, uint64_t* sel_id,
-                     tt_round_result* res) {
+int tt_round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel_score, double* sel_cost,
+                     uint64_t* sel_id, tt_round_result* res) {
   if (!ctx) return TT_E_STATE;
-  return round_collect(ctx, sel_index, sel_score, sel_cost, sel_id, res, true);
+  return round_collect(ctx, capacity, sel_index, sel_score, sel_cost, sel_id, res, true);
 }
 
 int tt_round(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
              const int32_t* soa, int64_t ld, uint64_t seed, int64_t* sel_index, double* sel_score, double* sel_cost,
              uint64_t* sel_id, tt_round_result* res) {
+  if (ctx && !ctx->pend.empty())
+    return fail(ctx, TT_E_STATE, "tt_round: rounds still in flight on this context (tt_round_collect them first)");
   int rc = tt_round_async(ctx, sk, dev, cfg, soa, ld, seed);
   if (rc) return rc;
-  return round_collect(ctx, sel_index, sel_score, sel_cost, sel_id, res, true);
+  return round_collect(ctx, cfg->b, sel_index, sel_score, sel_cost, sel_id, res, true);
 }
 
 int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
@@ -1421,6 +1504,14 @@ int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec*
   TT_CUDA(ctx, cudaMemsetAsync(gidx_out, 0xff, sizeof(int64_t) * cfg->k, ctx->stream));  // -1 = empty slot
   TT_CUDA(ctx, cudaMemsetAsync(cost_out, 0, sizeof(double) * cfg->k, ctx->stream));
   TT_CUDA(ctx, cudaMemsetAsync(id_out, 0, sizeof(uint64_t) * cfg->k, ctx->stream));
+  if (S.space < (uint64_t)cfg->n * 64) {
+    // a small schedule space: duplicates may exhaust the device selector's
+    // margin (> 4096 tied survivors), so select synchronously with the
+    // host-driven hash fallback rather than fail the merged round
+    int64_t cnt = 0;
+    return select_sync(ctx, S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k, cfg->toggles,
+                       cfg->first, gidx_out, cost_out, id_out, &cnt);
+  }
   if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
   prof_begin(ctx, 0);
   if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k,
@@ -1436,35 +1527,17 @@ int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sk, const tt_devi
                                  const tt_round_config* cfg, const double* cost, const int64_t* gidx,
                                  const uint64_t* id, int64_t m) {
   if (!ctx) return TT_E_STATE;
-  DevSketch S;
-  DevDevice D;
-  int rc = compile_sketch(ctx, sk, S);
-  if (rc) return rc;
-  if ((rc = compile_device(ctx, dev, D))) return rc;
-  if ((rc = check_round_cfg(ctx, cfg))) return rc;
-  if (m < 0 || m > 4096) return fail(ctx, TT_E_STATE, "merge: at most 4096 gathered entries per call");
-  if ((rc = ensure_k(ctx, cfg->k))) return rc;
-  if ((rc = ensure_b(ctx, cfg->b))) return rc;
-  const int slot = ring_claim(ctx);
-  prof_begin(ctx, 4);
-  if (launch_merge(cost, gidx, id, (int)m, cfg->k, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->stream))
-    return fail(ctx, TT_E_STATE, "merge launch");
-  prof_end(ctx, 4);
-  TT_LAUNCHED(ctx);
-  CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
-  if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
-  if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
-  // no retry: the local selections are the caller's
-  ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, -1, 0, false, true, *cfg, *sk, *dev, nullptr, 0});
-  return TT_OK;
+  return merged_enqueue(ctx, sk, dev, cfg, cost, gidx, id, m);
 }
 
 int tt_round_finish_merged(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
                            const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t* sel_index,
                            double* sel_score, double* sel_cost, uint64_t* sel_id, tt_round_result* res) {
+  if (ctx && !ctx->pend.empty())
+    return fail(ctx, TT_E_STATE, "tt_round_finish_merged: rounds still in flight (tt_round_collect them first)");
   int rc = tt_round_finish_merged_async(ctx, sk, dev, cfg, cost, gidx, id, m);
   if (rc) return rc;
-  return round_collect(ctx, sel_index, sel_score, sel_cost, sel_id, res, false);
+  return round_collect(ctx, cfg->b, sel_index, sel_score, sel_cost, sel_id, res, true);
 }
 
 int tt_profile_enable(tt_ctx* ctx, int on) {

@@ -36,6 +36,13 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 constexpr int64_t kSmallSelectMax = 1024;
 
+// Round record (the one device->host copy of a round), 8-byte words:
+// [0] selected, [1] drafted, [2] status, [3] rescored, [4] selector retries
+// (host), [5] band error bits (max |fast - fp64| over the rescored set), then
+// b population indices, b scores, b draft costs, b identities.
+constexpr int64_t kRecHead = 6;
+inline int64_t record_words(int64_t b) { return kRecHead + 4 * b; }
+
 enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2 };
 
 // Device-resident state of one top-K selection (k_draft.cu).
@@ -51,7 +58,9 @@ struct SelState {
   uint32_t unique;
   int64_t count;
   uint32_t nsurv;   // appended survivors
-  uint32_t ticket;  // CTAs finished in the current fast-select kernel (last one finalises)
+  uint32_t ticket;  // CTAs finished in the current kernel (last one finalises)
+  uint32_t bar_count, bar_gen;  // grid barrier of the cooperative fast selector (self-resetting)
+  uint32_t att_surv[8], att_dup[8];  // fast selector: survivors / duplicates per threshold attempt
 };
 
 struct SelScratch {
@@ -68,6 +77,7 @@ struct SelScratch {
   uint64_t* tvals = nullptr;
   SelState* state = nullptr;
   int* invalid = nullptr;
+  int32_t* mscratch = nullptr;  // cross-rank merge: 3 * kMergeMax words
   cudaEvent_t k1_ev[2] = {nullptr, nullptr};  // optional: recorded around the K1 cost kernel (profiling)
 };
 
@@ -97,8 +107,17 @@ int explore_cluster_size(int64_t n);  // CTAs of the explore cluster (flags per 
 int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int64_t n, int n_steps,
                         void* dev_base, size_t dev_stride, size_t dev_cost_off, uint64_t s_init, void* host_base, size_t host_stride, size_t host_cost_off,
                         volatile uint32_t* flags, cudaStream_t st);
-int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int m, int64_t k, int64_t* out_idx,
-                 double* out_cost, uint64_t* out_id, int64_t* out_count, cudaStream_t st);
+// Cross-rank merge of gathered (cost, global index, identity) lists: the k
+// lowest unique by (cost, index). m <= 4096: any order (one-CTA sort); larger
+// m: m / k per-rank lists of k, each ascending with empty slots (index -1)
+// at its tail, as tt_round_local_async emits them. An index of -2 marks a
+// rank whose selector failed: the merge ORs TT_SEL_OVERFLOW into *state.
+constexpr int64_t kMergeMax = 1 << 16;
+constexpr int64_t kMergeSortMax = 4096;  // one-CTA sort path (any order)
+constexpr int64_t kRankFailed = -2;      // index word of a rank whose selector failed
+int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k, int64_t* out_idx,
+                 double* out_cost, uint64_t* out_id, int64_t* out_count, SelState* state, int32_t* scratch,
+                 cudaStream_t st);
 // identities of the drafted set (side stream)
 int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
                             bool seeded, const int64_t* idx, const int64_t* count_dev, int64_t k_max, uint64_t* out,
@@ -167,14 +186,17 @@ int launch_band(const double* fast, const int64_t* n_dev, int64_t n_max, const i
 int launch_gd_step(double* params, const double* grads, int64_t n, double lr, cudaStream_t st);
 int launch_momentum(double* phi, const double* target, int64_t n, double m, cudaStream_t st);
 // select_top + the round record in one CTA (n <= 1024, b <= 32); -1 otherwise
+// fast (nullable): the tensor-core scores; record word [5] = max |scores - fast| over
+// the candidates not excluded (the fp64-rescored set)
 int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
                   const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
-                  const int* rescored, int64_t* out, cudaStream_t st);
+                  const int* rescored, const double* fast, int64_t* out, cudaStream_t st);
 // fast top-b + certification band in one CTA (n <= 1024, b <= 32); -1 otherwise
 int launch_cert_band(const double* fast, const double* drafts, int64_t n_max, const int64_t* n_dev, int64_t b,
                      double band, int32_t* sublist, int* sublist_count, uint8_t* excluded, cudaStream_t st);
 int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
                   const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
-                  const uint64_t* id, const double* scores, int64_t b, int64_t* out, cudaStream_t st);
+                  const uint64_t* id, const double* scores, const double* fast, const uint8_t* excluded,
+                  int64_t n_max, int64_t b, int64_t* out, cudaStream_t st);
 
 }  // namespace tt

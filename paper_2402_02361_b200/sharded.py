@@ -63,7 +63,7 @@ class ShardedRound:
         return payload
 
     def run_async(self, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, seed: int = 0,
-                  soa: torch.Tensor | None = None, precision: int = tt.TT_PREC_FP64, band: float = 0.0,
+                  soa: torch.Tensor | None = None, precision: int = tt.TT_PREC_FP64, band: float | None = None,
                   scaling: str = "strong", toggles: int = TT_TOGGLES_ALL):
         if scaling == "strong":
             first, n_local = shard_range(n, self.rank, self.world)

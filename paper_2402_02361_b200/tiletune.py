@@ -18,6 +18,7 @@ call goes through the C ABI (include/tt/tt.h) into sm_100a kernels.
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 from dataclasses import dataclass
 
@@ -25,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from ._capi import TTError, RoundConfig, RoundResult, TT_PREC_BF16, TT_PREC_FP64, lib
+from ._capi import TTError, RoundConfig, RoundResult, TT_BF16_BAND, TT_PREC_BF16, TT_PREC_FP64, TT_ROUND_BAND_RERUN, lib
 from .types import DeviceSpec, OpSpec, OracleSpec, Sketch, TT_TOGGLES_ALL
 
 __all__ = ["Context", "TTError", "TT_PREC_FP64", "TT_PREC_BF16", "random_init", "draft_cost", "draft_topk",
@@ -52,6 +53,9 @@ class Context:
             raise TTError(lib().tt_status_code(rc).decode(), f"tt_ctx_create({device}) failed (no usable CUDA device?)")
         self.h = h
         self.torch_device = torch.device("cuda", device)
+        # gathered lists of merged rounds in flight (the device reads them until
+        # the round is collected); None for the rounds that need nothing kept
+        self._inflight = collections.deque()
         if use_torch_stream:
             s = torch.cuda.current_stream(self.torch_device)
             # torch's default stream has handle 0 = the legacy default stream;
@@ -381,6 +385,8 @@ class RoundOutput:
     drafted: int
     rescored: int
     status: int
+    retries: int = 0
+    band_err: float = 0.0
 
     @property
     def selected(self) -> int:
@@ -388,6 +394,8 @@ class RoundOutput:
 
 
 def _round_cfg(n, k, b, precision, band, first, toggles):
+    if band is None:  # the bf16 path needs an explicit bound; fp64 ignores it
+        band = TT_BF16_BAND if precision == TT_PREC_BF16 else 0.0
     return RoundConfig(n, k, b, toggles, precision, band, first)
 
 
@@ -395,11 +403,11 @@ def _round_out(b, res, ix, sc, co, ids):
     m = res.selected
     return RoundOutput(np.frombuffer(ix, np.int64)[:m].copy(), np.frombuffer(sc, np.float64)[:m].copy(),
                        np.frombuffer(co, np.float64)[:m].copy(), np.frombuffer(ids, np.uint64)[:m].copy(),
-                       res.drafted, res.rescored, res.status)
+                       res.drafted, res.rescored, res.status, res.retries, res.band_err)
 
 
 def draft_verify_round(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, seed: int = 0,
-                       soa: torch.Tensor | None = None, precision: int = TT_PREC_FP64, band: float = 0.0,
+                       soa: torch.Tensor | None = None, precision: int = TT_PREC_FP64, band: float | None = None,
                        first: int = 0, toggles: int = TT_TOGGLES_ALL) -> RoundOutput:
     """Engine::round_draft_verify's compute (tuner.cpp:361-396): SA draft over
     n candidates -> dedup top-k -> features + PaCM -> select_top(b). Needs a
@@ -414,24 +422,27 @@ def draft_verify_round(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k:
 
 
 def round_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, seed: int = 0,
-                soa: torch.Tensor | None = None, precision: int = TT_PREC_FP64, band: float = 0.0, first: int = 0,
+                soa: torch.Tensor | None = None, precision: int = TT_PREC_FP64, band: float | None = None, first: int = 0,
                 toggles: int = TT_TOGGLES_ALL):
     cfg = _round_cfg(n, k, b, precision, band, first, toggles)
     ld = soa.stride(0) if soa is not None else 0
     ctx.check(lib().tt_round_async(ctx.h, C.byref(sketch), C.byref(dev), C.byref(cfg), _p(soa), ld,
                                    seed & (2**64 - 1)))
+    ctx._inflight.append(None)
 
 
 def round_collect(ctx: Context, b: int) -> RoundOutput:
     ix, sc, co, ids = (C.c_int64 * b)(), (C.c_double * b)(), (C.c_double * b)(), (C.c_uint64 * b)()
     res = RoundResult()
-    ctx.check(lib().tt_round_collect(ctx.h, ix, sc, co, ids, C.byref(res)))
+    ctx.check(lib().tt_round_collect(ctx.h, b, ix, sc, co, ids, C.byref(res)))
+    if ctx._inflight:
+        ctx._inflight.popleft()
     return _round_out(b, res, ix, sc, co, ids)
 
 
 def round_finish_merged(ctx: Context, sketch: Sketch, dev: DeviceSpec, cost: torch.Tensor, gidx: torch.Tensor,
                         ids: torch.Tensor, n: int, k: int, b: int, precision: int = TT_PREC_FP64,
-                        band: float = 0.0) -> RoundOutput:
+                        band: float | None = None) -> RoundOutput:
     cfg = _round_cfg(n, k, b, precision, band, 0, TT_TOGGLES_ALL)
     ix, sc, co, idv = (C.c_int64 * b)(), (C.c_double * b)(), (C.c_double * b)(), (C.c_uint64 * b)()
     res = RoundResult()
@@ -460,13 +471,13 @@ def unpack_gathered(gathered: torch.Tensor, world: int, k: int) -> torch.Tensor:
 
 
 def round_finish_merged_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, gathered: torch.Tensor, n: int, k: int,
-                              b: int, precision: int = TT_PREC_FP64, band: float = 0.0):
+                              b: int, precision: int = TT_PREC_FP64, band: float | None = None):
     """Verify half of a sharded round over the all-gathered [R, 3, k] lists."""
     g = unpack_gathered(gathered, gathered.numel() // (3 * k), k)
     cfg = _round_cfg(n, k, b, precision, band, 0, TT_TOGGLES_ALL)
-    ctx._merged = g  # keep alive until collected
     ctx.check(lib().tt_round_finish_merged_async(ctx.h, C.byref(sketch), C.byref(dev), C.byref(cfg), _p(g[0]),
                                                  _p(g[1]), _p(g[2]), g.shape[1]))
+    ctx._inflight.append(g)  # kept alive until collected
 
 
 STAGES = ["select", "pacm", "certify", "finish", "merge", "pacm_kernel", "features", "draft_cost"]

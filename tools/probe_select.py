@@ -1,4 +1,5 @@
-"""Phase timeline of the fast draft selector (%globaltimer marks, ns)."""
+"""Phase timeline of the fused draft selector k_fsel (%globaltimer marks of
+CTA 0, ns): K1, threshold, compact, rank (+ barriers), emit."""
 import ctypes as C
 import sys
 sys.path.insert(0, ".")
@@ -16,10 +17,11 @@ for name in ["r50_c3x3_64", "gemm1024", "bert_ffn1"]:
         for _ in range(3):
             tt.draft_topk(ctx, sk, dev, soa, 512)
         torch.cuda.synchronize()
-        c = (C.c_ulonglong * 12)()
-        L.ttdbg_select_clocks(c, 12)
+        c = (C.c_ulonglong * 16)()
+        L.ttdbg_select_clocks(c, 16)
         t = list(c)
-        print(f"{name} n={n}: K1 {(t[1]-t[0])/1e3:.1f} us | threshold {(t[2]-t[1])/1e3:.1f} | gap {(t[3]-t[2])/1e3:.1f} | "
-              f"compact {(t[4]-t[3])/1e3:.1f} | rank {(t[5]-t[4])/1e3:.1f} | emit {(t[6]-t[5])/1e3:.1f} | "
-              f"total {(t[6]-t[0])/1e3:.1f} us, survivors {t[7]} | emit: zero {(t[8]-t[5])/1e3:.1f} scatter {(t[9]-t[8])/1e3:.1f} scan {(t[10]-t[9])/1e3:.1f} out-loop {(t[11]-t[10])/1e3:.1f} tail {(t[6]-t[11])/1e3:.1f}")
+        bars = " ".join(f"b{b}: cta0 {(t[8+2*b]-t[0])/1e3:.1f} last {(t[9+2*b]-t[0])/1e3:.1f}" for b in range(3))
+        print(f"{name} n={n}: K1 {(t[1]-t[0])/1e3:.1f} us | threshold {(t[2]-t[1])/1e3:.1f} | "
+              f"compact {(t[3]-t[2])/1e3:.1f} | rank {(t[4]-t[3])/1e3:.1f} | emit {(t[5]-t[4])/1e3:.1f} | "
+              f"total {(t[5]-t[0])/1e3:.1f} us, survivors {t[6]}, attempts {t[7]} | arrivals (us from start) {bars}")
         del soa
