@@ -330,6 +330,7 @@ def run_ours(args, rank, world, local_rank):
         for c_ in cctx:
             c_.close()
 
+    b1m = None if args.no_bert else bert_1m(args, ctx, dev, params_host, rank, world, stream, flush)
     tot, etot, stot, atot = agg(times), agg(etimes), agg(stimes), agg(atimes)
     cands = n * world * len(sketches) * args.steps
     result = None
@@ -339,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
         stage_ms = {s: v[0] / max(v[1], 1) for s, v in (prof or {}).items()}
         roof = roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec)
         cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+        parity = parity_check(args, ctx, dev, sketches, names, pops, params, prec) if world == 1 else None
         ga = explore_ga(args, ctx, dev, sketches, names) if (world == 1 and not args.no_explore) else None
         result = {
             "metric": METRIC, "value": cands / tot, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -370,6 +372,8 @@ def run_ours(args, rank, world, local_rank):
                 "note": "the step's 7 subgraph rounds on 7 contexts/streams at once (independent tasks, "
                         "fixed weights); the headline `value` runs them one after another"},
             "explore_ga": ga,
+            "bert_1m": b1m,
+            "parity": parity,
             "gpu_launches": launches,
             "stage_ms_per_round": stage_ms,
             "roofline": roof,
@@ -377,6 +381,126 @@ def run_ours(args, rank, world, local_rank):
             "clocks": clocks,
         }
     return result
+
+
+BERT = ["bert_qkv", "bert_proj", "bert_ffn1", "bert_ffn2", "bert_bmm_qk", "bert_bmm_pv"]
+
+
+def bert_1m(args, ctx, dev, params_host, rank, world, stream, flush):
+    """BASELINE configs[2]: the six BERT-base subgraphs, 1,048,576 candidates
+    per subgraph round in total, strong-sharded by index range over the N
+    ranks: local K1 + selector on each shard -> one NCCL
+    all-gather of the [3, K] (cost, global index, identity) payloads ->
+    merge + PaCM verify + select_top on every rank. Populations resident in
+    HBM (each rank its shard), L2 flushed between steps, CUDA events, max over
+    ranks. Also times one profiled step per stage (local draft, all-gather,
+    merge + verify) on the context stream."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.sharded import shard_range
+    from paper_2402_02361_b200.types import WORKLOADS, make_sketch
+    n_total, k, b, seed = args.bert_n, args.k, args.b, args.seed
+    first, n_loc = shard_range(n_total, rank, world)
+    sks = [make_sketch(WORKLOADS[w]()) for w in BERT]
+    pops = [tt.random_init(ctx, sk, n_loc, seed, first=first) for sk in sks]
+    payload = torch.empty((3, k), dtype=torch.int64, device="cuda")
+    gathered = torch.empty((world * 3 * k,), dtype=torch.int64, device="cuda")
+    sels = []
+
+    def one(sk, soa, ev=None):
+        if world == 1:
+            tt.round_async(ctx, sk, dev, n_total, k, b, soa=soa, first=first)
+            return
+        tt.round_local_async(ctx, sk, dev, n_loc, k, b, first, payload, soa=soa)
+        if ev:
+            ev[0].record(stream)
+        dist.all_gather_into_tensor(gathered, payload.reshape(-1))
+        if ev:
+            ev[1].record(stream)
+        tt.round_finish_merged_async(ctx, sk, dev, gathered, n_total, k, b)
+
+    def step(keep=False, evs=None):
+        for i, (sk, soa) in enumerate(zip(sks, pops)):
+            one(sk, soa, None if evs is None else evs[i])
+            out = tt.round_collect(ctx, b)
+            if keep:
+                sels.append(out.index.tolist())
+
+    step(keep=True)  # warm-up, and the selections (checked against N = 1 by the caller's tests)
+    for _ in range(max(args.warmup - 1, 2)):
+        step()
+    torch.cuda.synchronize()
+    times = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot = float(t.item()) / 1e3
+    stages = None
+    if world > 1:  # one profiled step: local draft | all-gather | merge + verify + select, per round
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in sks]
+        starts, ends = [], []
+        for i, (sk, soa) in enumerate(zip(sks, pops)):
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            one(sk, soa, evs[i])
+            s1.record(stream)
+            tt.round_collect(ctx, b)
+            starts.append(s0), ends.append(s1)
+        torch.cuda.synchronize()
+        loc = [starts[i].elapsed_time(evs[i][0]) for i in range(len(sks))]
+        ag = [evs[i][0].elapsed_time(evs[i][1]) for i in range(len(sks))]
+        mg = [evs[i][1].elapsed_time(ends[i]) for i in range(len(sks))]
+        stages = {"local_draft_us": 1e3 * sum(loc) / len(loc), "all_gather_us": 1e3 * sum(ag) / len(ag),
+                  "merge_verify_us": 1e3 * sum(mg) / len(mg)}
+    cands = n_total * len(sks) * args.steps
+    info = {"value": cands / tot, "unit": UNIT, "ms_per_step": 1e3 * tot / args.steps, "scaling": "strong",
+            "config": f"BASELINE configs[2]: {len(sks)} BERT-base subgraph rounds/step, N={n_total} candidates per "
+                      f"round in total sharded over {world} GPU(s) ({n_loc} on rank {rank}), K={k}, b={b}, h=64, fp64",
+            "subgraphs": BERT, "selections_first_step": sels, "stage_us_per_round": stages}
+    if world > 1:
+        info["collective"] = {"backend": dist.get_backend(), "nranks": world,
+                              "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version()),
+                              "payload_bytes_per_rank": 3 * k * 8}
+    return info
+
+
+def parity_check(args, ctx, dev, sketches, names, pops, params, prec):
+    """Outside the timed region: one round per benchmarked subgraph on the
+    bench's own resident population, checked against the C oracle
+    (oracle/_build, test infrastructure) on the same seeded inputs: drafted
+    top-K, PaCM fp64 scores and the selection."""
+    from paper_2402_02361_b200 import tiletune as tt
+    R = _ref_setup(args)
+    rows, ok = {}, True
+    for name, sk, soa in zip(names, sketches, pops):
+        out = tt.draft_verify_round(ctx, sk, dev, args.n, args.k, args.b, soa=soa, precision=prec, band=args.band)
+        pop = R.O_random_init(sk, args.seed, args.n)
+        cost = R.O_draft_cost(sk, dev, pop)
+        idx, dc = R.O_draft_topk(sk, cost, pop, args.k)
+        st, bl = R.O_features(sk, dev, pop, idx)
+        sc = R.O_score(params, 64, st, bl)
+        sel = R.O_select_top(sc, dc, None, args.b)
+        same = bool((out.index == idx[sel]).all()) and bool((out.cost.view(np.uint64) == dc[sel].view(np.uint64)).all())
+        err = float(np.abs(out.score - sc[sel]).max())
+        rows[name] = {"identical_selection": same, "max_abs_score_err": err}
+        ok = ok and same
+    return {"checked": "one round per subgraph vs the C oracle (oracle/tt_oracle.c), same seeded population",
+            "all_identical": ok, "subgraphs": rows}
 
 
 FLOP_PER_CAND = 320640  # SURVEY.md §8(d): PaCM forward at h = 64, S = 6, B = 8
@@ -601,9 +725,25 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-explore", action="store_true", help="skip the explore_ga entry (e.g. under ncu)")
     ap.add_argument("--ref-rounds-per-step", type=int, default=1)
+    ap.add_argument("--bert-n", type=int, default=1 << 20, help="configs[2]: candidates per BERT round in total")
+    ap.add_argument("--no-bert", action="store_true", help="skip the configs[2] (BERT 1M, strong-sharded) entry")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start N ranks (one per GPU) the way the
+        # driver does, over torch.distributed.run on 127.0.0.1
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

@@ -255,11 +255,22 @@ int tt_round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index_host, dou
  * global index, identity) for the all-gather, ascending by (cost, index);
  * unused slots get index -1. A rank whose selector could not certify its
  * list (more than 4096 schedules tied at the threshold) writes index -2 in
- * slot 0, and every rank's merged round then fails with TT_E_STATE.
+ * slot 0, and every rank's merged round then fails with TT_E_STATE; a rank
+ * whose explicit population holds an invalid schedule writes -3, and every
+ * rank's merged round fails with TT_E_VALIDATE.
  * cfg->first = global index of this shard's first candidate. */
 int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
                          const tt_round_config* cfg, const int32_t* soa_dev, int64_t ld, uint64_t seed,
                          double* cost_dev, int64_t* gidx_dev, uint64_t* identity_dev);
+/* Synchronous draft half (same payload): the selector's host-driven retries
+ * (doubled margin, then the hash path for > 4096 ties) and the population
+ * check run here, so it fails only where tt_round fails (TT_E_VALIDATE for
+ * an invalid schedule, TT_E_STATE when even the hash path overflows). A
+ * merged round whose collect reports a rank's selector overflow is re-run
+ * with this on every rank (all ranks see the same merged status). */
+int tt_round_local(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
+                   const int32_t* soa_dev, int64_t ld, uint64_t seed, double* cost_dev, int64_t* gidx_dev,
+                   uint64_t* identity_dev);
 /* Sharded round, verify half, async: merge + features + PaCM + select;
  * read with tt_round_collect. m <= 4096 entries in any order, or up to
  * 65,536 as m / k whole per-rank lists (tt_round_local_async's layout). The

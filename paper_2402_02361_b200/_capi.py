@@ -89,6 +89,8 @@ _SIGS = [
     ("tt_round_drafted", C.c_int, [vp, P(vp), P(vp), P(vp), P(vp)]),
     ("tt_round_local_async", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64,
                                        vp, vp, vp]),
+    ("tt_round_local", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64,
+                                 vp, vp, vp]),
     ("tt_round_finish_merged_async", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, vp, vp,
                                                C.c_int64]),
     ("tt_profile_enable", C.c_int, [vp, C.c_int]),

@@ -17,6 +17,7 @@ import math
 import numpy as np
 
 from ._capi import TTError
+from .types import TT_OP_ELEMENTWISE
 
 # for_each_tensor (ranker.cpp:336-353): name, (rows, cols) as functions of h
 TENSORS = [("stmt_w1", lambda h: (24, h)), ("stmt_b1", lambda h: (1, h)), ("stmt_w2", lambda h: (h, h)),
@@ -174,11 +175,14 @@ def records_to_jsonl(records, tasks) -> str:
 
 def _valid(sk, f) -> bool:
     """validate_schedule (schedule.cpp:242-278): every axis' factors multiply
-    to its extent, unroll is one of the sketch's choices."""
+    to its extent, element-wise (arity-2) spatial slots are (b, t, 1, 1),
+    unroll is one of the sketch's choices."""
     n_sp, n_red = sk.op.n_spatial, sk.op.n_reduction
     for a in range(n_sp + n_red):
         c, w = (4 * a, 4) if a < n_sp else (4 * n_sp + 3 * (a - n_sp), 3)
         if any(v < 1 for v in f[c:c + w]) or math.prod(f[c:c + w]) != sk.op.extent[a]:
+            return False
+        if a < n_sp and sk.op.kind == TT_OP_ELEMENTWISE and (f[c + 2] != 1 or f[c + 3] != 1):
             return False
     return f[4 * n_sp + 3 * n_red] in [sk.unroll[u] for u in range(sk.n_unroll)]
 
@@ -204,7 +208,10 @@ def records_from_jsonl(text: str, tasks) -> list:
             axes = j["schedule"]["axes"]
             f = []
             for a in range(n_sp + n_red):
-                f += [int(v) for v in axes[names[a]]]
+                tup = [int(v) for v in axes[names[a]]]
+                if len(tup) != (4 if a < n_sp else 3):  # schedule.cpp:249,265: 4 per spatial, 3 per reduction
+                    raise TTError("E_VALIDATE", f"records line {lineno}: axis {names[a]} has {len(tup)} factors")
+                f += tup
             f.append(int(j["schedule"]["unroll"]))
             rec = {"task": task, "round": int(j["round"]), "schedule": f, "latency_s": float(j["latency_s"]),
                    "draft_cost": float(j["draft_cost"]), "model_score": float(j["model_score"])}

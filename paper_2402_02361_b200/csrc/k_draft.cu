@@ -909,6 +909,7 @@ __global__ void __launch_bounds__(1024) k_merge(const double* __restrict__ cost,
   for (int e = 0; e < kSortE; ++e) {
     const int p = e * blockDim.x + threadIdx.x;
     if (st && p < m && gidx[p] == kRankFailed) atomicOr(&st->status, TT_SEL_OVERFLOW);
+    if (st && p < m && gidx[p] == kRankInvalid) atomicOr(&st->status, TT_SEL_INVALID);
     const bool v = p < m && gidx[p] >= 0;  // negative index = empty slot
     // position p in the low 12 bits finds the identity after the sort;
     // global indices < 2^51 keep the (index, p) order = index order
@@ -962,6 +963,7 @@ __global__ void __launch_bounds__(512) k_merge_rank(const double* __restrict__ c
     if (g < 0 && (j == 0 || gq[j - 1] >= 0)) lq = (int)j;  // the first empty slot
   }
   if (st && q == r && threadIdx.x == 0 && gr[0] == kRankFailed) atomicOr(&st->status, TT_SEL_OVERFLOW);
+  if (st && q == r && threadIdx.x == 0 && gr[0] == kRankInvalid) atomicOr(&st->status, TT_SEL_INVALID);
   __syncthreads();
   const int L = lq;
   for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
@@ -1158,6 +1160,15 @@ int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, 
   if (seeded)
     return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, true><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
+}
+
+__global__ void k_mark_invalid(const int* __restrict__ invalid, int64_t* __restrict__ out_idx) {
+  if (*invalid) out_idx[0] = kRankInvalid;
+}
+
+int launch_mark_invalid(const int* invalid, int64_t* out_idx, cudaStream_t st) {
+  k_mark_invalid<<<1, 1, 0, st>>>(invalid, out_idx);
+  return cudaGetLastError() != cudaSuccess;
 }
 
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k, int64_t* out_idx,

@@ -544,6 +544,7 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaMalloc((void**)&c->sel.state, sizeof(SelState)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->sel.state, 0, sizeof(SelState)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->sel.invalid, sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMemset(c->sel.invalid, 0, sizeof(int)))) return TT_E_CUDA;  // seeded rounds copy it unset
   if (bad(cudaMalloc((void**)&c->d_count, sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_pos_count, sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_pos_fast_count, sizeof(int64_t)))) return TT_E_CUDA;
@@ -1071,8 +1072,11 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
     if (!ok && ((int)rec[2] & TT_SEL_NEED_MORE))
       return fail(ctx, TT_E_STATE, "draft selector did not converge");
   }
+  if ((int)rec[2] & TT_SEL_INVALID)
+    return fail(ctx, TT_E_VALIDATE, "a rank's population holds a schedule that fails validate_schedule");
   if ((int)rec[2] & TT_SEL_OVERFLOW)
-    return fail(ctx, TT_E_STATE, "draft selector overflow: more than 4096 unique schedules tie at the threshold");
+    return fail(ctx, TT_E_STATE, p.merged ? "draft selector overflow on a rank: re-run the draft half with tt_round_local"
+                                          : "draft selector overflow: more than 4096 unique schedules tie at the threshold");
   if (p.soa && *inv) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
   double band_err;
   std::memcpy(&band_err, rec + 5, sizeof(double));
@@ -1520,7 +1524,32 @@ int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec*
     return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
   prof_end(ctx, 0);
   TT_LAUNCHED(ctx);
+  // an explicit population with an invalid schedule marks the payload: every
+  // rank's merged round then fails with TT_E_VALIDATE
+  if (!seeded) {
+    if (launch_mark_invalid(ctx->sel.invalid, gidx_out, ctx->stream)) return fail(ctx, TT_E_CUDA, "mark launch");
+    TT_LAUNCHED(ctx);
+  }
   return TT_OK;
+}
+
+int tt_round_local(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                   const int32_t* soa, int64_t ld, uint64_t seed, double* cost_out, int64_t* gidx_out,
+                   uint64_t* id_out) {
+  if (!ctx) return TT_E_STATE;
+  DevSketch S;
+  DevDevice D;
+  int rc = compile_sketch(ctx, sk, S);
+  if (rc) return rc;
+  if ((rc = compile_device(ctx, dev, D))) return rc;
+  if ((rc = check_round_cfg(ctx, cfg))) return rc;
+  if (!S.id_exact) return fail(ctx, TT_E_STATE, "round: schedule space exceeds 2^64 identities");
+  TT_CUDA(ctx, cudaMemsetAsync(gidx_out, 0xff, sizeof(int64_t) * cfg->k, ctx->stream));
+  TT_CUDA(ctx, cudaMemsetAsync(cost_out, 0, sizeof(double) * cfg->k, ctx->stream));
+  TT_CUDA(ctx, cudaMemsetAsync(id_out, 0, sizeof(uint64_t) * cfg->k, ctx->stream));
+  int64_t cnt = 0;
+  return select_sync(ctx, S, D, soa, ld, seed_state(seed), cfg->first, soa == nullptr, cfg->n, cfg->k, cfg->toggles,
+                     cfg->first, gidx_out, cost_out, id_out, &cnt);
 }
 
 int tt_round_finish_merged_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev,

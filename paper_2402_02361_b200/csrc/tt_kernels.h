@@ -43,7 +43,7 @@ constexpr int64_t kSmallSelectMax = 1024;
 constexpr int64_t kRecHead = 6;
 inline int64_t record_words(int64_t b) { return kRecHead + 4 * b; }
 
-enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2 };
+enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2, TT_SEL_INVALID = 4 };
 
 // Device-resident state of one top-K selection (k_draft.cu).
 struct SelState {
@@ -111,10 +111,14 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
 // lowest unique by (cost, index). m <= 4096: any order (one-CTA sort); larger
 // m: m / k per-rank lists of k, each ascending with empty slots (index -1)
 // at its tail, as tt_round_local_async emits them. An index of -2 marks a
-// rank whose selector failed: the merge ORs TT_SEL_OVERFLOW into *state.
+// rank whose selector failed: the merge ORs TT_SEL_OVERFLOW into *state; -3
+// a rank whose explicit population held an invalid schedule (TT_SEL_INVALID).
 constexpr int64_t kMergeMax = 1 << 16;
 constexpr int64_t kMergeSortMax = 4096;  // one-CTA sort path (any order)
 constexpr int64_t kRankFailed = -2;      // index word of a rank whose selector failed
+constexpr int64_t kRankInvalid = -3;     // index word of a rank whose population failed validate_schedule
+// sharded draft half, explicit population: slot 0's index <- kRankInvalid when K1 flagged a schedule
+int launch_mark_invalid(const int* invalid, int64_t* out_idx, cudaStream_t st);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, SelState* state, int32_t* scratch,
                  cudaStream_t st);

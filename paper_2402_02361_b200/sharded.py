@@ -56,21 +56,23 @@ class ShardedRound:
         return self._bufs[k]
 
     def local(self, sketch: Sketch, dev: DeviceSpec, first: int, n: int, k: int, b: int = 1, seed: int = 0,
-              soa: torch.Tensor | None = None, toggles: int = TT_TOGGLES_ALL) -> torch.Tensor:
-        """Draft half: this rank's [3, k] payload (async on the ctx stream)."""
+              soa: torch.Tensor | None = None, toggles: int = TT_TOGGLES_ALL, sync: bool = False) -> torch.Tensor:
+        """Draft half: this rank's [3, k] payload (async on the ctx stream;
+        sync=True: tt_round_local, with the selector's host-driven retries)."""
         payload, _ = self._buffers(k)
-        tt.round_local_async(self.ctx, sketch, dev, n, k, b, first, payload, seed=seed, soa=soa, toggles=toggles)
+        fn = tt.round_local if sync else tt.round_local_async
+        fn(self.ctx, sketch, dev, n, k, b, first, payload, seed=seed, soa=soa, toggles=toggles)
         return payload
 
     def run_async(self, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, seed: int = 0,
                   soa: torch.Tensor | None = None, precision: int = tt.TT_PREC_FP64, band: float | None = None,
-                  scaling: str = "strong", toggles: int = TT_TOGGLES_ALL):
+                  scaling: str = "strong", toggles: int = TT_TOGGLES_ALL, sync_local: bool = False):
         if scaling == "strong":
             first, n_local = shard_range(n, self.rank, self.world)
             n_total = n
         else:
             first, n_local, n_total = self.rank * n, n, n * self.world
-        payload = self.local(sketch, dev, first, n_local, k, b, seed=seed, soa=soa, toggles=toggles)
+        payload = self.local(sketch, dev, first, n_local, k, b, seed=seed, soa=soa, toggles=toggles, sync=sync_local)
         _, gathered = self._buffers(k)
         if self.dist.get_backend(self.group) == "nccl":
             self.dist.all_gather_into_tensor(gathered, payload.reshape(-1), group=self.group)
@@ -80,5 +82,16 @@ class ShardedRound:
         tt.round_finish_merged_async(self.ctx, sketch, dev, gathered, n_total, k, b, precision=precision, band=band)
 
     def run(self, *a, **kw) -> tt.RoundOutput:
+        """One sharded round, collected. A rank whose device selector could
+        not certify its list marks its payload; every rank then sees the same
+        merged E_STATE and re-runs the draft half synchronously (host-driven
+        retries, hash path) — no extra agreement step is needed."""
+        b = a[4] if len(a) > 4 else kw["b"]
         self.run_async(*a, **kw)
-        return tt.round_collect(self.ctx, a[4] if len(a) > 4 else kw["b"])
+        try:
+            return tt.round_collect(self.ctx, b)
+        except tt.TTError as e:
+            if e.code != "E_STATE" or "tt_round_local" not in str(e) or kw.get("sync_local"):
+                raise
+        self.run_async(*a, **dict(kw, sync_local=True))
+        return tt.round_collect(self.ctx, b)

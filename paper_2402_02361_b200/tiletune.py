@@ -462,6 +462,17 @@ def round_local_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: 
                                          seed & (2**64 - 1), _p(out[0]), _p(out[1]), _p(out[2])))
 
 
+def round_local(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, first: int,
+                out: torch.Tensor, seed: int = 0, soa: torch.Tensor | None = None, toggles: int = TT_TOGGLES_ALL):
+    """Synchronous draft half (tt_round_local): the same payload with the
+    selector's host-driven retries (margin, hash path) and the population
+    check; raises where draft_verify_round would."""
+    cfg = _round_cfg(n, k, b, TT_PREC_FP64, 0.0, first, toggles)
+    ld = soa.stride(0) if soa is not None else 0
+    ctx.check(lib().tt_round_local(ctx.h, C.byref(sketch), C.byref(dev), C.byref(cfg), _p(soa), ld,
+                                   seed & (2**64 - 1), _p(out[0]), _p(out[1]), _p(out[2])))
+
+
 def unpack_gathered(gathered: torch.Tensor, world: int, k: int) -> torch.Tensor:
     """The all-gather output (world consecutive [3, k] payloads) as one
     [3, world * k] table: row 0 cost bits, row 1 global index, row 2 identity."""

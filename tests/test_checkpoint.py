@@ -205,3 +205,34 @@ def test_records_jsonl_errors_match_reference():
             ck.records_from_jsonl(text, tasks)
         assert e.value.code == code
         assert ref_records_from_jsonl(sk, text, 16) is None  # the reference rejects it too
+
+
+@live
+def test_records_jsonl_axis_structure_matches_reference():
+    """validate_schedule's per-axis rules (schedule.cpp:242-278): 4 factors per
+    spatial axis, 3 per reduction axis (a shifted list with the right total is
+    rejected), and element-wise (arity-2) slots admit only (b, t, 1, 1)."""
+    import json as _json
+
+    from paper_2402_02361_b200.types import make_elementwise, make_gemm, make_sketch
+    sk = make_sketch(make_gemm(64, 64, 64))
+    names = _names(sk)
+    tasks = {"op": (sk, names)}
+    line = ck.records_to_jsonl(_records(sk, 1, 3), tasks).splitlines()[0]
+    j = _json.loads(line)
+    ax = j["schedule"]["axes"]
+    a0, a1 = names[0], names[1]
+    ax[a0], ax[a1] = ax[a0] + [1], ax[a1][:3]  # products unchanged, tuple sizes 5 and 3
+    shifted = _json.dumps(j, separators=(",", ":")) + "\n"
+    esk = make_sketch(make_elementwise(64, 48))
+    enames = _names(esk)
+    etasks = {"op": (esk, enames)}
+    je = _json.loads(ck.records_to_jsonl(_records(esk, 1, 3), etasks).splitlines()[0])
+    e0 = je["schedule"]["axes"][enames[0]]
+    je["schedule"]["axes"][enames[0]] = [1, 1, e0[0] * e0[1], 1]  # extent 64 in the o slot
+    degenerate = _json.dumps(je, separators=(",", ":")) + "\n"
+    for s_, t_, text in [(sk, tasks, shifted), (esk, etasks, degenerate)]:
+        with pytest.raises(TTError) as e:
+            ck.records_from_jsonl(text, t_)
+        assert e.value.code == "E_VALIDATE"
+        assert ref_records_from_jsonl(s_, text, 4) is None

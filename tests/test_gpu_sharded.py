@@ -23,15 +23,20 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, name, n, k, b, seed, prec, q):
+def _worker(rank, world, port, name, n, k, b, seed, prec, q, backend="gloo"):
     import torch.distributed as dist
     from paper_2402_02361_b200 import tiletune as tt
     from paper_2402_02361_b200.sharded import ShardedRound
     from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev_id = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev_id)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev_id))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ctx = tt.Context(0)
+        ctx = tt.Context(dev_id)
         tt.PaCM(ctx, tt.init_params(64, derive_seed(seed, TAG_INIT)), 64)
         out = ShardedRound(ctx).run(make_sketch(WORKLOADS[name]()), reference_device(), n, k, b, seed=seed,
                                     precision=prec)
@@ -42,6 +47,44 @@ def _worker(rank, world, port, name, n, k, b, seed, prec, q):
         raise
     finally:
         dist.destroy_process_group()
+
+
+def _run_ranks(world, name, n, k, b, seed, prec, backend):
+    c = mp.get_context("spawn")
+    q = c.Queue()
+    port = _port()
+    procs = [c.Process(target=_worker, args=(r, world, port, name, n, k, b, seed, prec, q, backend))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=180) for _ in procs))
+    assert all(v[0] != "error" for v in res.values()), res
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs for an NCCL group")
+@pytest.mark.parametrize("name", ["bert_ffn1", "bert_bmm_qk"])
+def test_sharded_nccl_equal_single(name):
+    """The bench's N > 1 transport: ranks on distinct GPUs, NCCL all-gather
+    (NVLink), config-3 shape (strong-sharded population), selection equal to
+    the single-GPU round bit for bit on every rank."""
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    n, k, b, seed = 1 << 20, 512, 10, 42
+    world = min(torch.cuda.device_count(), 8)
+    ctx = tt.Context(0)
+    tt.PaCM(ctx, tt.init_params(64, derive_seed(seed, TAG_INIT)), 64)
+    ref = tt.draft_verify_round(ctx, make_sketch(WORKLOADS[name]()), reference_device(), n, k, b, seed=seed)
+    ctx.close()
+    res = _run_ranks(world, name, n, k, b, seed, 0, "nccl")
+    for r in range(world):
+        idx, sc, ids = res[r]
+        assert idx == ref.index.tolist(), r
+        assert np.abs(np.array(sc) - ref.score).max() <= 1e-12
+        assert ids == ref.identity.tolist()
 
 
 @pytest.mark.parametrize("name,n,prec", [("gemm1024", 20000, 0), ("r50_c3x3_512", 65536, 1)])
@@ -70,3 +113,64 @@ def test_sharded_two_ranks_equal_single(name, n, prec):
         assert idx == ref.index.tolist(), r
         assert np.abs(np.array(sc) - ref.score).max() <= (1e-12 if prec == 0 else 6e-2)
         assert ids == ref.identity.tolist()
+
+
+def _two_rank_payloads(tt, ctx, sk, dev, n, k, b, seed, soa=None, sync=False):
+    outs = []
+    for r in range(2):
+        o = torch.empty((3, k), dtype=torch.int64, device="cuda")
+        fn = tt.round_local if sync else tt.round_local_async
+        fn(ctx, sk, dev, n, k, b, r * n, o, seed=seed, soa=None if soa is None else soa[r])
+        outs.append(o)
+    return torch.cat([o.reshape(-1) for o in outs])
+
+
+def test_local_sync_equals_async_and_single():
+    """tt_round_local (host-driven retries) emits the same payload as the
+    async draft half; merged, both equal the single-GPU round."""
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    ctx = tt.Context(0)
+    tt.PaCM(ctx, tt.init_params(64, derive_seed(3, TAG_INIT)), 64)
+    sk, dev = make_sketch(WORKLOADS["bert_qkv"]()), reference_device()
+    n, k, b = 30000, 512, 10
+    ga = _two_rank_payloads(tt, ctx, sk, dev, n, k, b, 3)
+    gs = _two_rank_payloads(tt, ctx, sk, dev, n, k, b, 3, sync=True)
+    assert torch.equal(ga, gs)
+    tt.round_finish_merged_async(ctx, sk, dev, gs, 2 * n, k, b)
+    got = tt.round_collect(ctx, b)
+    want = tt.draft_verify_round(ctx, sk, dev, 2 * n, k, b, seed=3)
+    assert (got.index == want.index).all() and (got.identity == want.identity).all()
+    ctx.close()
+
+
+def test_failed_rank_fails_every_merged_round():
+    """A payload marked by a failed selector (index -2) or by an invalid
+    explicit population (-3, written by the draft half itself) makes the
+    merged round fail loudly instead of returning a short selection."""
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    ctx = tt.Context(0)
+    tt.PaCM(ctx, tt.init_params(64, derive_seed(3, TAG_INIT)), 64)
+    sk, dev = make_sketch(WORKLOADS["gemm1024"]()), reference_device()
+    n, k, b = 20000, 512, 10
+    g = _two_rank_payloads(tt, ctx, sk, dev, n, k, b, 5)
+    g2 = g.clone().view(2, 3, k)
+    g2[1, 1, 0] = -2
+    tt.round_finish_merged_async(ctx, sk, dev, g2.reshape(-1), 2 * n, k, b)
+    with pytest.raises(tt.TTError) as e:
+        tt.round_collect(ctx, b)
+    assert e.value.code == "E_STATE" and "tt_round_local" in str(e.value)
+    # explicit populations: rank 1's holds a schedule whose factors do not multiply to the extent
+    pops = [tt.random_init(ctx, sk, n, 5, first=r * n) for r in range(2)]
+    pops[1][0, 17] += 1
+    g3 = _two_rank_payloads(tt, ctx, sk, dev, n, k, b, 0, soa=pops)
+    assert int(g3.view(2, 3, k)[1, 1, 0]) == -3
+    tt.round_finish_merged_async(ctx, sk, dev, g3, 2 * n, k, b)
+    with pytest.raises(tt.TTError) as e:
+        tt.round_collect(ctx, b)
+    assert e.value.code == "E_VALIDATE"
+    with pytest.raises(tt.TTError) as e:  # the synchronous half reports it directly
+        _two_rank_payloads(tt, ctx, sk, dev, n, k, b, 0, soa=pops, sync=True)
+    assert e.value.code == "E_VALIDATE"
+    ctx.close()
