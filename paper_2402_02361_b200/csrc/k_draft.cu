@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     // expected survivors ~1.5x need (+3 samples): below need only ~3.5 sigma out
     const int64_t r = (3 * need * ns + 2 * n - 1) / (2 * n) + 3;
     all = r >= ns - 1;
+    if (blockIdx.x == 0 && t == 0) g_sel_ns[19] = gtimer();
     const uint64_t thr = all ? ~0ull : block_sample_threshold(keys, ns, (int)r, hist, hsum, wt);
     if (blockIdx.x == 0 && t == 0) g_sel_ns[2] = gtimer();
     if (attempt > 0)
@@ -724,6 +725,7 @@ __global__ void __launch_bounds__(kFastThreads, 1)
   // ---- E: emit. Position of a unique survivor = its rank minus the
   // duplicates ranked below it (a bitmap over ranks, prefix popcounts).
   if (blockIdx.x > 0 && (int64_t)blockIdx.x * blockDim.x >= m) return;
+  if (blockIdx.x == 0 && t == 0) g_sel_ns[16] = gtimer();
   for (int w = t; w < kFastCap / 32; w += blockDim.x) dmask[w] = 0;
   __syncthreads();
   for (int e = t; e < m; e += blockDim.x)
@@ -732,10 +734,12 @@ __global__ void __launch_bounds__(kFastThreads, 1)
       atomicOr(&dmask[r >> 5], 1u << (r & 31));
     }
   __syncthreads();
+  if (blockIdx.x == 0 && t == 0) g_sel_ns[17] = gtimer();
   for (int w = t; w < kFastCap / 32; w += blockDim.x) dcnt[w] = __popc(dmask[w]);
   __syncthreads();
   block_exclusive_scan(dcnt, dpre, kFastCap / 32, wt);
   __syncthreads();
+  if (blockIdx.x == 0 && t == 0) g_sel_ns[18] = gtimer();
   const int e = blockIdx.x * blockDim.x + t;
   if (e < m && !__ldcg(dup + e)) {
     const int r = __ldcg(rank_acc + e);
@@ -1203,5 +1207,5 @@ int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, in
 }  // namespace tt
 
 extern "C" int ttdbg_select_clocks(unsigned long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 16 ? n : 16));
+  return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 24 ? n : 24));
 }
