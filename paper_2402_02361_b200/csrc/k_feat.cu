@@ -30,16 +30,6 @@ namespace tt {
 
 constexpr int kFeatThreads = 512;  // 16 warps; warp w evaluates row slot w (w + 16, ...)
 
-template <int NSP, int NRED>
-__device__ __forceinline__ void feat_load(const DevSketch& S, const CandRef& r, int64_t pos, Factors<NSP, NRED>& F) {
-  if (r.soa) {
-    load_factors<NSP, NRED>(r.soa, r.ld, r.idx[pos] - r.index_base, F, true);
-  } else if (r.seeded) {
-    generate<NSP, NRED>(S, r.s0, (uint64_t)r.idx[pos], F);
-  } else {
-    from_identity<NSP, NRED>(S, r.id[pos], F);
-  }
-}
 
 __device__ __forceinline__ void st_row_bf16(uint8_t* tile, int row, const double* v, int width) {
 #pragma unroll

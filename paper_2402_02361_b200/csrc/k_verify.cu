@@ -1,0 +1,98 @@
+// k_verify.cu — the verify half of a round in ONE kernel for the tuner's
+// model geometry: hybrid feature rows of the drafted candidates
+// (extract_features, features.cpp:98-257) computed by the CTA that scores
+// them, straight into its shared-memory operand staging, then the fp64 PaCM
+// forward (run_forward, ranker.cpp:159-209) of tt_pacm64.cuh. Replaces
+// k_feat_rows + k_pacm64_h64 (one launch and one HBM/L2 round trip of the
+// feature rows fewer per round). Same arithmetic as both: scores are
+// identical to the two-kernel path.
+//
+// Per pass of G = 4 candidates: lanes 0-3 of warp 0 derive each candidate's
+// shared information (factors -> tile table -> symbols -> penalties); then
+// warp w evaluates feature row w of the 4 candidates (warp-uniform row code,
+// as k_feat_rows), 8 lanes per candidate sharing the row's log1p calls, and
+// writes it transposed into the candidate's staging.
+#include <cstdint>
+
+#include "tt_features.cuh"
+#include "tt_kernels.h"
+#include "tt_pacm64.cuh"
+
+namespace tt {
+
+template <int NSP, int NRED>
+__global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice D, CandRef ref,
+                                                       const int64_t* __restrict__ count_dev, int64_t k_max,
+                                                       const double* __restrict__ params,
+                                                       double* __restrict__ score_out) {
+  using namespace f64;
+  __shared__ CandInfo<NSP, NRED> ci[G];
+  const int S = 2 * SK.n_in + 2;
+  const int B = SK.kind == TT_OP_ELEMENTWISE ? 1 : 3 * SK.n_in + 2;
+  pacm_h64_body(S, B, count_dev, k_max, params, score_out, [&](int64_t e0, int64_t count, double* MISC) {
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    for (int v = t; v < G * kMisc; v += T) MISC[v] = 0.0;  // padding rows, xb^T row 23, idle slots
+    if (warp == 0 && lane < G && e0 + lane < count) {
+      Factors<NSP, NRED> F;
+      feat_load<NSP, NRED>(SK, ref, e0 + lane, F);
+      H64_MARK(19, 0);
+      cand_info<NSP, NRED>(SK, D, F, ci[lane]);
+      H64_MARK(20, 0);
+    }
+    __syncthreads();
+    H64_MARK(21, 0);
+    // warp w: feature row w of the G candidates, 8 lanes per candidate; every
+    // lane derives the row's arguments, then applies the log1p of values
+    // slot, slot + 8, slot + 16 only (3 instead of up to 14 per lane)
+    const int cc = lane >> 3, slot = lane & 7;
+    if (warp < S + B && e0 + cc < count) {
+      double v[TT_STMT_WIDTH];
+      uint32_t lm;
+      feature_args<double, NSP, NRED>(SK, D, ci[cc], warp, v, &lm);
+      double* m = MISC + cc * kMisc + (warp < S ? warp : 24 * 8 + (warp - S));
+      const int width = warp < S ? TT_STMT_WIDTH : TT_BLOCK_WIDTH;
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int k = slot + 8 * u;
+        if (k < width) {
+          double x = 0.0;
+#pragma unroll
+          for (int q = 0; q < TT_STMT_WIDTH; ++q)  // register-indexed select
+            if (q == k) x = v[q];
+          m[k * 8] = (lm >> k & 1u) ? lg<double>(x) : x;
+        }
+      }
+    }
+  });
+}
+
+int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                    const double* params, int h, double* score_out, cudaStream_t st) {
+  const int ns = 2 * S.n_in + 2, nb = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
+  if (h != f64::H || ns > 8 || nb > 8 || k_max <= 0) return -1;
+  const int64_t ctas = (k_max + f64::G - 1) / f64::G;
+  const dim3 grid((unsigned)(ctas < 148 ? ctas : 148));
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
+    static bool attr = false;  // per instance, once
+    if (!attr) {
+      cudaFuncSetAttribute(k_verify64<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f64::kSmem);
+      attr = true;
+    }
+    tt::note_launch();
+    launch_pdl(k_verify64<NSP, NRED>, grid, dim3(f64::T), f64::kSmem, st, S, D, ref, count_dev, k_max, params,
+               score_out);
+  }));
+}
+
+}  // namespace tt
+
+extern "C" int ttdbg_verify64_clocks(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_clk_h64, sizeof(long long) * (n < 24 ? n : 24));
+}
+extern "C" int ttdbg_verify64_span(unsigned long long* out, int reset) {
+  if (reset) {
+    const unsigned long long init[4] = {~0ull, ~0ull, 0ull, 0ull};
+    return (int)cudaMemcpyToSymbol(tt::g_h64_ns, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, tt::g_h64_ns, sizeof(unsigned long long) * 4);
+}

@@ -817,11 +817,20 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
   if (rc) return rc;
   if (precision == TT_PREC_FP64) {
     prof_begin(ctx, 1);
+    prof_begin(ctx, 5);
+    // the tuner geometry: features + PaCM in one kernel (k_verify64)
+    const int fused = launch_verify64(S, D, ref, count_dev, k_max, ctx->d_params, ctx->h, ctx->d_score, ctx->stream);
+    if (fused == 0) {
+      prof_end(ctx, 5);
+      prof_end(ctx, 1);
+      TT_LAUNCHED(ctx);
+      TT_CUDA(ctx, cudaMemsetAsync(ctx->d_sublist_count, 0, sizeof(int), ctx->stream));
+      return TT_OK;
+    }
     prof_begin(ctx, 6);
     if (launch_feat_rows(S, D, ref, count_dev, k_max, nullptr, nullptr, ctx->d_xs, ctx->d_xb, nullptr, ctx->stream))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     prof_end(ctx, 6);
-    prof_begin(ctx, 5);
     if (launch_pacm64(ctx->d_xs, ctx->d_xb, ns, nb, count_dev, k_max, nullptr, nullptr, ctx->d_params, ctx->h, 0,
                       ctx->d_score, ctx->stream))
       return fail(ctx, TT_E_CONFIG, "fp64 PaCM: hidden width too large for shared memory");

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "tt_device.cuh"
+#include "tt_kernels.h"
 
 namespace tt {
 
@@ -39,6 +40,18 @@ __device__ __forceinline__ double rdiv<double>(double a, double b) {
 template <>
 __device__ __forceinline__ float rdiv<float>(float a, float b) {
   return __fdiv_rn(a, b);
+}
+
+// Factors of drafted position `pos` (explicit SoA, counter stream or identity).
+template <int NSP, int NRED>
+__device__ __forceinline__ void feat_load(const DevSketch& S, const CandRef& r, int64_t pos, Factors<NSP, NRED>& F) {
+  if (r.soa) {
+    load_factors<NSP, NRED>(r.soa, r.ld, r.idx[pos] - r.index_base, F, true);
+  } else if (r.seeded) {
+    generate<NSP, NRED>(S, r.s0, (uint64_t)r.idx[pos], F);
+  } else {
+    from_identity<NSP, NRED>(S, r.id[pos], F);
+  }
 }
 
 // Everything a candidate's rows share; computed once per thread.
@@ -77,10 +90,14 @@ __device__ __forceinline__ int64_t inner_vec(const int32_t (&vin)[NA], uint32_t 
   return fp_mask<NA>(vin, mask);
 }
 
-// Writes row `row` (statement rows first) into out[0..width).
+// The arguments of row `row` (statement rows first): out value k is
+// lg(arg[k]) where bit k of *logm is set, arg[k] itself otherwise — so the
+// (expensive) log1p calls of a row can be spread over lanes. feature_row
+// applies them in place.
 template <typename R, int NSP, int NRED>
-__device__ __forceinline__ void feature_row(const DevSketch& S, const DevDevice& D,
-                                            const CandInfo<NSP, NRED>& C, int row, R* out) {
+__device__ __forceinline__ void feature_args(const DevSketch& S, const DevDevice& D,
+                                             const CandInfo<NSP, NRED>& C, int row, R* out, uint32_t* logm) {
+  uint32_t lm = 0;
   constexpr int NA = NSP + NRED;
   const int n_in = S.n_in;
   const int n_stmt = 2 * n_in + 2;
@@ -110,30 +127,45 @@ __device__ __forceinline__ void feature_row(const DevSketch& S, const DevDevice&
     }
     const Symbols& y = C.y;
     const Penalties& p = C.p;
-    out[0] = lg<R>((R)y.s1);
-    out[1] = lg<R>((R)y.s2);
-    out[2] = lg<R>((R)y.s3);
-    out[3] = lg<R>((R)y.s4);
-    out[4] = lg<R>((R)s5);
-    out[5] = lg<R>((R)y.s6);
-    out[6] = lg<R>((R)s7);
-    out[7] = lg<R>((R)s8);
+    out[0] = (R)y.s1;
+    lm |= 1u << 0;
+    out[1] = (R)y.s2;
+    lm |= 1u << 1;
+    out[2] = (R)y.s3;
+    lm |= 1u << 2;
+    out[3] = (R)y.s4;
+    lm |= 1u << 3;
+    out[4] = (R)s5;
+    lm |= 1u << 4;
+    out[5] = (R)y.s6;
+    lm |= 1u << 5;
+    out[6] = (R)s7;
+    lm |= 1u << 6;
+    out[7] = (R)s8;
+    lm |= 1u << 7;
     out[8] = (R)p.p_l0_m;
-    out[9] = lg<R>((R)p.p_l0_c);
+    out[9] = (R)p.p_l0_c;
+    lm |= 1u << 9;
     out[10] = (R)p.p_l1_m;
     out[11] = (R)p.p_l1_c;
     out[12] = (R)p.alpha;
     out[13] = (R)p.p_l2_c;
     out[14] = (R)p_l2_m_of(s7, D);
-    out[15] = lg<R>((R)S.flops);
-    out[16] = lg<R>((R)C.traffic);
-    out[17] = lg<R>(rdiv<R>((R)s8, (R)(s5 > 1 ? s5 : 1)));
+    out[15] = (R)S.flops;
+    lm |= 1u << 15;
+    out[16] = (R)C.traffic;
+    lm |= 1u << 16;
+    out[17] = rdiv<R>((R)s8, (R)(s5 > 1 ? s5 : 1));
+    lm |= 1u << 17;
     out[18] = rdiv<R>((R)y.s4, (R)D.pu_l1_n_l1);
-    out[19] = lg<R>(rdiv<R>((R)y.s6, (R)D.pu_l2));
-    out[20] = lg<R>((R)C.unroll);
+    out[19] = rdiv<R>((R)y.s6, (R)D.pu_l2);
+    lm |= 1u << 19;
+    out[20] = (R)C.unroll;
+    lm |= 1u << 20;
     out[21] = (R)S.fused;
     out[22] = (R)kind / (R)4;
     out[23] = (R)1;
+    *logm = lm;
     return;
   }
   // ---- dataflow blocks ----
@@ -141,7 +173,10 @@ __device__ __forceinline__ void feature_row(const DevSketch& S, const DevDevice&
 #pragma unroll
   for (int t = 0; t < TT_BLOCK_WIDTH; ++t) out[t] = (R)0;
   out[22] = (R)1;
-  if (S.kind == TT_OP_ELEMENTWISE) return;  // single zero block (features.cpp:153-158)
+  if (S.kind == TT_OP_ELEMENTWISE) {  // single zero block (features.cpp:153-158)
+    *logm = 0;
+    return;
+  }
   int flow, access, rank, depth;
   int64_t alloc, volume, distinct, stride, per_lane, s7;
   bool contiguous, red;
@@ -215,19 +250,40 @@ __device__ __forceinline__ void feature_row(const DevSketch& S, const DevDevice&
   }
   out[flow] = (R)1;
   out[6 + access] = (R)1;
-  out[9] = lg<R>((R)alloc);
-  out[10] = lg<R>((R)volume);
-  out[11] = lg<R>(rdiv<R>((R)volume, (R)(distinct > 1 ? distinct : 1)));
-  out[12] = lg<R>((R)stride);
+  out[9] = (R)alloc;
+  lm |= 1u << 9;
+  out[10] = (R)volume;
+  lm |= 1u << 10;
+  out[11] = rdiv<R>((R)volume, (R)(distinct > 1 ? distinct : 1));
+  lm |= 1u << 11;
+  out[12] = (R)stride;
+  lm |= 1u << 12;
   out[13] = contiguous ? (R)1 : (R)0;
-  out[14] = lg<R>(rdiv<R>((R)S.flops, (R)(volume > 1 ? volume : 1)));
-  out[15] = lg<R>((R)lanes);
-  out[16] = lg<R>((R)per_lane);
+  out[14] = rdiv<R>((R)S.flops, (R)(volume > 1 ? volume : 1));
+  lm |= 1u << 14;
+  out[15] = (R)lanes;
+  lm |= 1u << 15;
+  out[16] = (R)per_lane;
+  lm |= 1u << 16;
   out[17] = (R)rank / (R)8;
   out[18] = (R)depth / (R)16;
   out[19] = red ? (R)1 : (R)0;
-  out[20] = lg<R>((R)C.unroll);
-  out[21] = lg<R>((R)s7);
+  out[20] = (R)C.unroll;
+  lm |= 1u << 20;
+  out[21] = (R)s7;
+  lm |= 1u << 21;
+  *logm = lm;
+}
+
+// Writes row `row` (statement rows first) into out[0..width).
+template <typename R, int NSP, int NRED>
+__device__ __forceinline__ void feature_row(const DevSketch& S, const DevDevice& D,
+                                            const CandInfo<NSP, NRED>& C, int row, R* out) {
+  uint32_t lm;
+  feature_args<R, NSP, NRED>(S, D, C, row, out, &lm);
+#pragma unroll
+  for (int k = 0; k < TT_STMT_WIDTH; ++k)
+    if (lm >> k & 1u) out[k] = lg<R>(out[k]);
 }
 
 }  // namespace tt

@@ -147,6 +147,10 @@ int launch_feat_rows(const DevSketch& S, const DevDevice& D, CandRef ref, const 
                      cudaStream_t st);
 
 // k_pacm64.cu — fp64 PaCM on feature rows (parity mode / certification)
+// k_verify.cu: features + fp64 PaCM of the drafted set in one kernel (h = 64,
+// <= 8 statement rows and dataflow blocks, attention on); -1 = not applicable
+int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
+                    const double* params, int h, double* score_out, cudaStream_t st);
 int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_block, const int64_t* count_dev,
                   int64_t k_max, const int32_t* sublist, const int* sublist_count, const double* params, int h,
                   int attention_identity, double* score_out, cudaStream_t st);
