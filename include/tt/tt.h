@@ -174,14 +174,24 @@ int tt_select_top(tt_ctx* ctx, const double* scores_dev, const double* drafts_de
 /* train(params, {one task}, cfg) (ranker.cpp:459-512) on the device, fp64:
  * dataset loss -> for each epoch: batch of <= `batch` records drawn by the
  * partial Fisher-Yates of RngStream(derive_seed(seed, "rain")), forward,
- * LambdaRank loss + score gradient (ranker.cpp:394-441, host), per-sample
- * score_backward (ranker.cpp:211-261), gradients summed in the reference's
- * sample/row order, p -= lr * g. params_dev (flattened RankerParams) is
- * updated in place; features are device rows [n][n_stmt][24] /
- * [n][n_block][23]; latencies host. Synchronous. */
+ * LambdaRank loss + score gradient (ranker.cpp:394-441, device, see
+ * tt_rank_loss), per-sample score_backward (ranker.cpp:211-261), gradients
+ * summed in the reference's sample/row order, p -= lr * g. No host round
+ * trip between epochs (batches drawn up front); scratch cached on the
+ * context. params_dev (flattened RankerParams) is updated in place; features
+ * are device rows [n][n_stmt][24] / [n][n_block][23]; latencies host.
+ * Synchronous. */
 int tt_pacm_train(tt_ctx* ctx, double* params_dev, int h, const double* stmt_dev, const double* block_dev, int n_stmt,
                   int n_block, const double* latencies_host, int64_t n, int epochs, double lr, int batch,
                   uint64_t seed, int attention_identity, double* initial_loss_host, double* final_loss_host);
+/* lambda_rank_loss(scores, latencies) (ranker.cpp:394-441) on the device:
+ * loss to the host, d loss / d score into grad_dev (may be NULL). Pair terms
+ * are the reference's expressions; each item's gradient and the loss are
+ * summed in a fixed order of their own (deterministic, equal to the
+ * reference up to summation order). TT_E_STATE for n < 2 or a latency <= 0,
+ * as the reference. Synchronous. */
+int tt_rank_loss(tt_ctx* ctx, const double* scores_dev, const double* latencies_dev, int64_t n, double* loss_host,
+                 double* grad_dev);
 /* train's GD update p -= lr * g (ranker.cpp:502-506). Async. */
 int tt_gd_step(tt_ctx* ctx, double* params_dev, const double* grads_dev, int64_t n, double lr);
 /* momentum_update phi' = t + m (phi - t) (momentum.cpp:28-46); TT_E_STATE

@@ -259,6 +259,15 @@ int ref_momentum_update(double* phi, const double* target, int h, double m) {
   });
 }
 
+int ref_rank_loss(const double* scores, const double* latencies, int64_t n, double* loss, double* grad) {
+  return guard([&] {
+    RankLossResult r = lambda_rank_loss(std::vector<double>(scores, scores + n),
+                                        std::vector<double>(latencies, latencies + n));
+    *loss = r.loss;
+    if (grad) std::memcpy(grad, r.grad.data(), sizeof(double) * (size_t)n);
+  });
+}
+
 int ref_train(double* params, int h, int n_stmt, int n_block, const double* stmt,
               const double* block, const double* latencies, int64_t k, int epochs, double lr,
               int batch, uint64_t seed, double* initial_loss, double* final_loss) {

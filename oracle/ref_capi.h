@@ -37,6 +37,8 @@ int ref_score_batch(const double* params, int h, int n_stmt, int n_block, const 
 int ref_select_top(const double* scores, const double* drafts, const uint8_t* excluded,
                    int64_t n, int64_t b, int64_t* idx_out);
 int ref_momentum_update(double* phi, const double* target, int h, double m);
+/* lambda_rank_loss (ranker.cpp:394-441): loss and score gradient */
+int ref_rank_loss(const double* scores, const double* latencies, int64_t n, double* loss, double* grad);
 /* train(params, {one task}, cfg) with labels given (ranker.cpp:459-512) */
 int ref_train(double* params, int h, int n_stmt, int n_block, const double* stmt,
               const double* block, const double* latencies, int64_t k, int epochs, double lr,

@@ -932,3 +932,67 @@ int64_t tto_explore(const tt_sketch* sk, const tt_device_spec* dev, int n_steps,
   free(pop), free(next), free(cost), free(pool);
   return np;
 }
+
+/* ---- lambda_rank_loss (ranker.cpp:394-441) ---------------------------------- */
+static double tto_log2d(double x) { return log(x) * 1.4426950408889634074; } /* ranker.cpp:33-35 */
+static double tto_softplus(double x) { return x > 30.0 ? x : log1p(exp(x)); } /* ranker.cpp:37-40 */
+static double tto_sigmoid(double x) {                                         /* ranker.cpp:42-50 */
+  if (x >= 0) {
+    double e = exp(-x);
+    return 1.0 / (1.0 + e);
+  }
+  double e = exp(x);
+  return e / (1.0 + e);
+}
+
+static const double* g_rank_scores; /* qsort comparator context (single-threaded checker) */
+static int cmp_rank(const void* a, const void* b) {
+  const int64_t i = *(const int64_t*)a, j = *(const int64_t*)b;
+  if (g_rank_scores[i] != g_rank_scores[j]) return g_rank_scores[i] > g_rank_scores[j] ? -1 : 1;
+  return i < j ? -1 : (i > j);
+}
+static int cmp_desc(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x > y ? -1 : (x < y);
+}
+
+int tto_rank_loss(const double* scores, const double* lat, int64_t n, double* loss, double* grad) {
+  if (n < 2) return -1;
+  double min_lat = lat[0];
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(lat[i] > 0.0)) return -1;
+    min_lat = lat[i] < min_lat ? lat[i] : min_lat;
+  }
+  double* gain = (double*)malloc(sizeof(double) * n);
+  double* disc = (double*)malloc(sizeof(double) * n);
+  double* ideal = (double*)malloc(sizeof(double) * n);
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * n);
+  for (int64_t i = 0; i < n; ++i) gain[i] = exp2(min_lat / lat[i]) - 1.0;
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  g_rank_scores = scores;
+  qsort(order, (size_t)n, sizeof(int64_t), cmp_rank); /* desc, ties by index: a strict total order */
+  for (int64_t pos = 0; pos < n; ++pos) disc[order[pos]] = 1.0 / tto_log2d((double)pos + 2.0);
+  memcpy(ideal, gain, sizeof(double) * n);
+  qsort(ideal, (size_t)n, sizeof(double), cmp_desc);
+  double max_dcg = 0.0;
+  for (int64_t pos = 0; pos < n; ++pos) max_dcg += ideal[pos] / tto_log2d((double)pos + 2.0);
+  double L = 0.0;
+  if (grad)
+    for (int64_t i = 0; i < n; ++i) grad[i] = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      if (!(lat[i] < lat[j])) continue;
+      const double w = fabs(gain[i] - gain[j]) * fabs(disc[i] - disc[j]) / max_dcg;
+      if (w == 0.0) continue;
+      const double d = scores[i] - scores[j];
+      L += w * tto_softplus(-d);
+      const double slope = w * tto_sigmoid(-d);
+      if (grad) {
+        grad[i] -= slope;
+        grad[j] += slope;
+      }
+    }
+  *loss = L;
+  free(gain), free(disc), free(ideal), free(order);
+  return 0;
+}

@@ -94,6 +94,10 @@ int tto_select_top(const double* scores, const double* drafts, const uint8_t* ex
  * train (ranker.cpp:502-506). */
 void tto_momentum_update(double* phi, const double* target, int64_t n, double m);
 void tto_gd_step(double* params, const double* grads, int64_t n, double lr);
+/* lambda_rank_loss (ranker.cpp:394-441), literal: the n^2 pairs in (i, j)
+ * order, one running loss, grad[i] -= slope / grad[j] += slope as they come.
+ * Returns 0, or -1 for n < 2 or a latency <= 0 (the reference's kState). */
+int tto_rank_loss(const double* scores, const double* latencies, int64_t n, double* loss, double* grad);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,7 @@ _SIGS = [
     ("tt_oracle_best", C.c_int, [vp, P(Sketch), P(OracleSpec), u64p, f64p]),
     ("tt_pacm_train", C.c_int, [vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, f64p, C.c_int64, C.c_int, C.c_double,
                                  C.c_int, C.c_uint64, C.c_int, f64p, f64p]),
+    ("tt_rank_loss", C.c_int, [vp, vp, vp, C.c_int64, f64p, vp]),
     ("tt_gd_step", C.c_int, [vp, vp, vp, C.c_int64, C.c_double]),
     ("tt_momentum_update", C.c_int, [vp, vp, vp, C.c_int64, C.c_double]),
     ("tt_round", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64, i64p, f64p,

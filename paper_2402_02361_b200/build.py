@@ -24,8 +24,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I" + os.path.join(ROOT, "include")]
 # translation units whose fp64 arithmetic must match the reference bit for
 # bit are built without FMA contraction
-EXACT = {"k_draft.cu", "k_verify.cu", "k_explore.cu", "k_feat.cu", "k_oracle.cu", "k_pacm64.cu", "k_select.cu", "k_train.cu", "tt_api.cu"}
-SOURCES = ["k_draft.cu", "k_verify.cu", "k_explore.cu", "k_feat.cu", "k_oracle.cu", "k_pacm64.cu", "k_select.cu", "k_pacm_tc.cu", "k_train.cu", "tt_api.cu"]
+EXACT = {"k_draft.cu", "k_verify.cu", "k_rank.cu", "k_explore.cu", "k_feat.cu", "k_oracle.cu", "k_pacm64.cu", "k_select.cu", "k_train.cu", "tt_api.cu"}
+SOURCES = ["k_draft.cu", "k_verify.cu", "k_rank.cu", "k_explore.cu", "k_feat.cu", "k_oracle.cu", "k_pacm64.cu", "k_select.cu", "k_pacm_tc.cu", "k_train.cu", "tt_api.cu"]
 HEADERS = ["tt_device.cuh", "tt_pacm64.cuh", "tt_features.cuh", "tt_block.cuh", "tt_kernels.h", "tt_tc.cuh"]
 
 

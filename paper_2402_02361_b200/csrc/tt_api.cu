@@ -60,6 +60,17 @@ struct tt_ctx {
   uint8_t* d_tiles = nullptr;
   // merge inputs
   int64_t m_cap = 0;
+  // training scratch (tt_pacm_train / tt_rank_loss), grow-only
+  struct Train {
+    double *slots = nullptr, *work = nullptr, *grads = nullptr, *dscore = nullptr, *scores = nullptr,
+           *rank = nullptr, *lat = nullptr, *loss = nullptr;
+    int32_t* list = nullptr;
+    int* bad = nullptr;
+    int64_t slots_cap = 0, work_cap = 0, grads_cap = 0, dscore_cap = 0, scores_cap = 0, rank_cap = 0, lat_cap = 0,
+            loss_cap = 0, list_cap = 0, bad_cap = 0;
+  } tr;
+  double* h_loss = nullptr;  // pinned: training losses read back once per call
+  int64_t h_loss_cap = 0;
   // multi-step explore (GA): one generation on the device, its pinned host mirror
   size_t ex_dcap = 0, ex_hcap = 0;
   void* d_ex = nullptr;  // two device generation slots + the RNG state
@@ -567,7 +578,8 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_idx, c->d_cost, c->d_id, c->d_score, c->d_score_fast, c->d_count, c->d_excluded,
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
-                  c->d_tiles, c->d_ex, c->d_mix};
+                  c->d_tiles, c->d_ex, c->d_mix, c->tr.slots, c->tr.work, c->tr.grads, c->tr.dscore,
+                  c->tr.scores, c->tr.rank, c->tr.lat, c->tr.loss, c->tr.list, c->tr.bad};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int r = 0; r < tt_ctx::kRing; ++r) {
@@ -576,6 +588,7 @@ void tt_ctx_destroy(tt_ctx* c) {
     if (c->ev_rec[r]) cudaEventDestroy(c->ev_rec[r]);
   }
   if (c->h_ex) cudaFreeHost(c->h_ex);
+  if (c->h_loss) cudaFreeHost(c->h_loss);
   for (cudaEvent_t e : c->ex_ev) cudaEventDestroy(e);
   graphs_clear(c);
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
@@ -1328,56 +1341,16 @@ struct HostRng {
 uint64_t mix64_h(uint64_t x) { return scramble64(x + kGolden); }
 uint64_t derive_seed_h(uint64_t base, uint64_t a) { return mix64_h(base ^ mix64_h(a)); }
 
-double softplus_h(double x) { return x > 30.0 ? x : std::log1p(std::exp(x)); }
-double sigmoid_h(double x) {
-  if (x >= 0) {
-    const double e = std::exp(-x);
-    return 1.0 / (1.0 + e);
-  }
-  const double e = std::exp(x);
-  return e / (1.0 + e);
-}
-double log2_h(double x) { return std::log(x) * 1.4426950408889634074; }
-
-// LambdaRank loss and its score gradient (ranker.cpp:394-441): pairs (i, j)
-// with i strictly faster, weighted by |Δgain| |Δdiscount| / max DCG under
-// the current score ranking (descending, ties by index).
-int lambda_rank_h(tt_ctx* ctx, const std::vector<double>& sc, const std::vector<double>& lat, double* loss,
-                  std::vector<double>* grad) {
-  const size_t n = sc.size();
-  if (n != lat.size()) return fail(ctx, TT_E_STATE, "rank loss: length mismatch");
-  if (n < 2) return fail(ctx, TT_E_STATE, "rank loss: need at least two items");
-  double min_lat = lat[0];
-  for (double l : lat) {
-    if (!(l > 0.0)) return fail(ctx, TT_E_STATE, "rank loss: latencies must be positive");
-    min_lat = l < min_lat ? l : min_lat;
-  }
-  std::vector<double> gain(n), discount(n);
-  for (size_t i = 0; i < n; ++i) gain[i] = std::exp2(min_lat / lat[i]) - 1.0;
-  std::vector<size_t> order(n);
-  for (size_t i = 0; i < n; ++i) order[i] = i;
-  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return sc[a] != sc[b] ? sc[a] > sc[b] : a < b; });
-  for (size_t pos = 0; pos < n; ++pos) discount[order[pos]] = 1.0 / log2_h((double)pos + 2.0);
-  std::vector<double> ideal = gain;
-  std::sort(ideal.begin(), ideal.end(), [](double a, double b) { return a > b; });
-  double max_dcg = 0.0;
-  for (size_t pos = 0; pos < n; ++pos) max_dcg += ideal[pos] / log2_h((double)pos + 2.0);
-  double L = 0.0;
-  if (grad) grad->assign(n, 0.0);
-  for (size_t i = 0; i < n; ++i)
-    for (size_t j = 0; j < n; ++j) {
-      if (!(lat[i] < lat[j])) continue;
-      const double w = std::fabs(gain[i] - gain[j]) * std::fabs(discount[i] - discount[j]) / max_dcg;
-      if (w == 0.0) continue;
-      const double d = sc[i] - sc[j];
-      L += w * softplus_h(-d);
-      if (grad) {
-        const double slope = w * sigmoid_h(-d);
-        (*grad)[i] -= slope;
-        (*grad)[j] += slope;
-      }
-    }
-  *loss = L;
+// grow-only scratch, doubling (the MoA loop's dataset grows by b records a
+// round; no graph invalidation: training is never captured)
+template <class T>
+int tgrow(tt_ctx* ctx, T*& p, int64_t& cap, int64_t want) {
+  if (want <= cap && p) return TT_OK;
+  if (want < 2 * cap) want = 2 * cap;
+  if (p) cudaFree(p);
+  p = nullptr, cap = 0;
+  TT_CUDA(ctx, cudaMalloc((void**)&p, sizeof(T) * (size_t)(want > 0 ? want : 1)));
+  cap = want;
   return TT_OK;
 }
 
@@ -1385,6 +1358,37 @@ int lambda_rank_h(tt_ctx* ctx, const std::vector<double>& sc, const std::vector<
 
 extern "C" {
 
+int tt_rank_loss(tt_ctx* ctx, const double* scores, const double* latencies, int64_t n, double* loss_host,
+                 double* grad) {
+  if (!ctx) return TT_E_STATE;
+  if (n < 2) return fail(ctx, TT_E_STATE, "rank loss: need at least two items");
+  if (n > (int64_t)1 << 20) return fail(ctx, TT_E_CONFIG, "rank loss: at most 2^20 items");
+  auto& T = ctx->tr;
+  int rc;
+  if ((rc = tgrow(ctx, T.rank, T.rank_cap, (int64_t)rank_work_doubles((int)n)))) return rc;
+  if ((rc = tgrow(ctx, T.loss, T.loss_cap, 1))) return rc;
+  if ((rc = tgrow(ctx, T.bad, T.bad_cap, 1))) return rc;
+  TT_CUDA(ctx, cudaMemsetAsync(T.bad, 0, sizeof(int), ctx->stream));
+  if (launch_rank_loss(scores, latencies, nullptr, (int)n, T.rank, T.bad, T.loss, 0, grad, ctx->stream))
+    return fail(ctx, TT_E_CUDA, "rank loss launch");
+  TT_LAUNCHED(ctx);
+  int bad = 0;
+  double l = 0.0;
+  TT_CUDA(ctx, cudaMemcpyAsync(&bad, T.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(ctx, cudaMemcpyAsync(&l, T.loss, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if ((rc = sync_check(ctx))) return rc;
+  if (bad) return fail(ctx, TT_E_STATE, "rank loss: latencies must be positive");
+  if (loss_host) *loss_host = l;
+  return TT_OK;
+}
+
+// train(params, {one task}, cfg) (ranker.cpp:459-512), entirely on the
+// device: every epoch's batch indices are drawn on the host up front (the
+// reference's RngStream and partial Fisher-Yates) and uploaded once; each
+// epoch is forward (k_train_fwd) -> LambdaRank loss + score gradient
+// (k_rank_*) -> score_backward + gradient sums (k_train_bwd/accum) -> GD,
+// with no host round trip; the losses come back in one copy at the end.
+// Scratch is cached on the context.
 int tt_pacm_train(tt_ctx* ctx, double* params, int h, const double* stmt, const double* block, int n_stmt,
                   int n_block, const double* latencies, int64_t n, int epochs, double lr, int batch, uint64_t seed,
                   int attention_identity, double* initial_loss, double* final_loss) {
@@ -1393,73 +1397,82 @@ int tt_pacm_train(tt_ctx* ctx, double* params, int h, const double* stmt, const 
   if (epochs < 0) return fail(ctx, TT_E_STATE, "train: epochs must be >= 0");
   if (h < 1 || n_stmt < 1 || n_block < 1 || n_stmt > 14 || n_block > 20)
     return fail(ctx, TT_E_STATE, "train: unsupported model / feature geometry");
+  if (n > (int64_t)1 << 20) return fail(ctx, TT_E_CONFIG, "train: at most 2^20 records");
+  for (int64_t i = 0; i < n; ++i)
+    if (!(latencies[i] > 0.0)) return fail(ctx, TT_E_STATE, "rank loss: latencies must be positive");
+  const int64_t take = (batch > 0 && batch < n) ? batch : n;
   const size_t slot = train_slot_doubles(n_stmt, n_block, h);
   const int64_t np = tt_param_count(h);
   const int ctas = 8 * 148;
-  const int64_t mmax = n;  // every record is scored for the dataset loss
-  double *slots = nullptr, *work = nullptr, *grads = nullptr, *dscore = nullptr, *scores = nullptr;
-  int32_t* list = nullptr;
-  auto release = [&]() {
-    cudaFree(slots), cudaFree(work), cudaFree(grads), cudaFree(dscore), cudaFree(scores), cudaFree(list);
-  };
-  if (cudaMalloc((void**)&slots, sizeof(double) * slot * mmax) != cudaSuccess ||
-      cudaMalloc((void**)&work, sizeof(double) * train_work_doubles(n_stmt, n_block, h, ctas)) != cudaSuccess ||
-      cudaMalloc((void**)&grads, sizeof(double) * np) != cudaSuccess ||
-      cudaMalloc((void**)&dscore, sizeof(double) * mmax) != cudaSuccess ||
-      cudaMalloc((void**)&scores, sizeof(double) * mmax) != cudaSuccess ||
-      cudaMalloc((void**)&list, sizeof(int32_t) * mmax) != cudaSuccess) {
-    release();
-    return fail(ctx, TT_E_CUDA, "train: allocation failed");
+  auto& T = ctx->tr;
+  int rc;
+  if ((rc = tgrow(ctx, T.slots, T.slots_cap, (int64_t)(slot * n)))) return rc;
+  if ((rc = tgrow(ctx, T.work, T.work_cap, (int64_t)train_work_doubles(n_stmt, n_block, h, ctas)))) return rc;
+  if ((rc = tgrow(ctx, T.grads, T.grads_cap, np))) return rc;
+  if ((rc = tgrow(ctx, T.dscore, T.dscore_cap, n))) return rc;
+  if ((rc = tgrow(ctx, T.scores, T.scores_cap, n))) return rc;
+  if ((rc = tgrow(ctx, T.rank, T.rank_cap, (int64_t)rank_work_doubles((int)n)))) return rc;
+  if ((rc = tgrow(ctx, T.lat, T.lat_cap, n))) return rc;
+  if ((rc = tgrow(ctx, T.loss, T.loss_cap, (int64_t)epochs + 2))) return rc;
+  if ((rc = tgrow(ctx, T.list, T.list_cap, take * (int64_t)(epochs > 0 ? epochs : 1)))) return rc;
+  if ((rc = tgrow(ctx, T.bad, T.bad_cap, 1))) return rc;
+  if (ctx->h_loss_cap < (int64_t)epochs + 2) {
+    if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
+    ctx->h_loss = nullptr, ctx->h_loss_cap = 0;
+    TT_CUDA(ctx, cudaMallocHost((void**)&ctx->h_loss, sizeof(double) * (epochs + 2)));
+    ctx->h_loss_cap = epochs + 2;
   }
-  std::vector<double> lat(latencies, latencies + n), sc(n), lt;
-  auto dataset_loss = [&](double* out) -> int {  // ranker.cpp:445-455
-    launch_train_fwd(stmt, block, n_stmt, n_block, nullptr, (int)n, params, h, attention_identity, slots, scores,
-                     ctx->stream);
-    TT_LAUNCHED(ctx);
-    TT_CUDA(ctx, cudaMemcpyAsync(sc.data(), scores, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    return lambda_rank_h(ctx, sc, lat, out, nullptr);
-  };
-  int rc = TT_OK;
-  double l0 = 0.0, l1 = 0.0;
-  if ((rc = dataset_loss(&l0))) {
-    release();
-    return rc;
-  }
-  HostRng rng(derive_seed_h(seed, 0x7261696eULL));
-  std::vector<int32_t> idx(n);
-  std::vector<double> bs, bl, g;
-  for (int epoch = 0; epoch < epochs && !rc; ++epoch) {
-    for (int64_t i = 0; i < n; ++i) idx[i] = (int32_t)i;
-    int64_t take = n;
-    if (batch > 0 && batch < n) {  // partial Fisher-Yates (ranker.cpp:478-486)
-      take = batch;
-      for (int64_t i = 0; i < take; ++i) std::swap(idx[i], idx[i + (int64_t)rng.index((uint64_t)(n - i))]);
+  // every epoch's batch (ranker.cpp:475-486), host RNG, one upload
+  std::vector<int32_t> lists((size_t)take * (epochs > 0 ? epochs : 1));
+  {
+    HostRng rng(derive_seed_h(seed, 0x7261696eULL));
+    std::vector<int32_t> idx((size_t)n);
+    for (int e = 0; e < epochs; ++e) {
+      for (int64_t i = 0; i < n; ++i) idx[i] = (int32_t)i;
+      if (take < n)  // partial Fisher-Yates
+        for (int64_t i = 0; i < take; ++i) std::swap(idx[i], idx[i + (int64_t)rng.index((uint64_t)(n - i))]);
+      std::copy(idx.begin(), idx.begin() + take, lists.begin() + (size_t)e * take);
     }
-    TT_CUDA(ctx, cudaMemcpyAsync(list, idx.data(), sizeof(int32_t) * take, cudaMemcpyHostToDevice, ctx->stream));
-    launch_train_fwd(stmt, block, n_stmt, n_block, list, (int)take, params, h, attention_identity, slots, scores,
-                     ctx->stream);
-    TT_LAUNCHED(ctx);
-    bs.resize(take), bl.resize(take);
-    TT_CUDA(ctx, cudaMemcpyAsync(bs.data(), scores, sizeof(double) * take, cudaMemcpyDeviceToHost, ctx->stream));
-    TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    for (int64_t i = 0; i < take; ++i) bl[i] = lat[idx[i]];
-    double el = 0.0;
-    if ((rc = lambda_rank_h(ctx, bs, bl, &el, &g))) break;
-    if (lr == 0.0) continue;
-    TT_CUDA(ctx, cudaMemcpyAsync(dscore, g.data(), sizeof(double) * take, cudaMemcpyHostToDevice, ctx->stream));
-    launch_train_bwd(n_stmt, n_block, (int)take, params, h, attention_identity, dscore, slots, work, ctas,
-                     ctx->stream);
-    launch_train_accum(n_stmt, n_block, (int)take, h, attention_identity, slots, grads, ctx->stream);
-    launch_gd_step(params, grads, np, lr, ctx->stream);  // p -= lr * g (ranker.cpp:502-506)
-    TT_LAUNCHED(ctx);
-    TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // g / bs host buffers reused next epoch
   }
-  if (!rc) rc = dataset_loss(&l1);
-  release();
-  if (rc) return rc;
-  if (initial_loss) *initial_loss = l0;
-  if (final_loss) *final_loss = l1;
+  TT_CUDA(ctx, cudaMemcpyAsync(T.lat, latencies, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  if (epochs > 0)
+    TT_CUDA(ctx, cudaMemcpyAsync(T.list, lists.data(), sizeof(int32_t) * lists.size(), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+  TT_CUDA(ctx, cudaMemsetAsync(T.bad, 0, sizeof(int), ctx->stream));
+  auto dataset_loss = [&](double* out) -> int {  // ranker.cpp:445-455
+    launch_train_fwd(stmt, block, n_stmt, n_block, nullptr, (int)n, params, h, attention_identity, T.slots,
+                     T.scores, ctx->stream);
+    TT_LAUNCHED(ctx);
+    if (launch_rank_loss(T.scores, T.lat, nullptr, (int)n, T.rank, T.bad, out, 0, nullptr, ctx->stream))
+      return fail(ctx, TT_E_CUDA, "rank loss launch");
+    return TT_OK;
+  };
+  if ((rc = dataset_loss(T.loss))) return rc;
+  for (int e = 0; e < epochs; ++e) {
+    const int32_t* list = T.list + (size_t)e * take;
+    launch_train_fwd(stmt, block, n_stmt, n_block, list, (int)take, params, h, attention_identity, T.slots, T.scores,
+                     ctx->stream);
+    TT_LAUNCHED(ctx);
+    // epoch loss (ranker.cpp:491-492) into loss[2 + e], score gradient into dscore
+    if (launch_rank_loss(T.scores, T.lat, list, (int)take, T.rank, T.bad, T.loss + 2 + e, 0,
+                         lr == 0.0 ? nullptr : T.dscore, ctx->stream))
+      return fail(ctx, TT_E_CUDA, "rank loss launch");
+    if (lr == 0.0) continue;
+    launch_train_bwd(n_stmt, n_block, (int)take, params, h, attention_identity, T.dscore, T.slots, T.work, ctas,
+                     ctx->stream);
+    launch_train_accum(n_stmt, n_block, (int)take, h, attention_identity, T.slots, T.grads, ctx->stream);
+    launch_gd_step(params, T.grads, np, lr, ctx->stream);  // p -= lr * g (ranker.cpp:502-506)
+    TT_LAUNCHED(ctx);
+  }
+  if ((rc = dataset_loss(T.loss + 1))) return rc;
+  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_loss, T.loss, sizeof(double) * (epochs + 2), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  int bad = 0;
+  TT_CUDA(ctx, cudaMemcpyAsync(&bad, T.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if ((rc = sync_check(ctx))) return rc;
+  if (bad) return fail(ctx, TT_E_STATE, "rank loss: latencies must be positive");
+  if (initial_loss) *initial_loss = ctx->h_loss[0];
+  if (final_loss) *final_loss = ctx->h_loss[1];
   return TT_OK;
 }
 

@@ -147,6 +147,14 @@ int launch_feat_rows(const DevSketch& S, const DevDevice& D, CandRef ref, const 
                      cudaStream_t st);
 
 // k_pacm64.cu — fp64 PaCM on feature rows (parity mode / certification)
+// k_rank.cu: LambdaRank loss + score gradient (lambda_rank_loss,
+// ranker.cpp:394-441) of m <= 2^20 items, scores[i] with latency
+// lat[list ? list[i] : i]; *loss (+)= the loss, dscore[i] = the gradient (may
+// be null); *bad |= 1 when a latency is not positive. work: rank_work_doubles.
+int rank_chunks(int m);
+size_t rank_work_doubles(int m);
+int launch_rank_loss(const double* scores, const double* lat, const int32_t* list, int m, double* work, int* bad,
+                     double* loss, int accumulate, double* dscore, cudaStream_t st);
 // k_verify.cu: features + fp64 PaCM of the drafted set in one kernel (h = 64,
 // <= 8 statement rows and dataflow blocks, attention on); -1 = not applicable
 int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,

@@ -355,6 +355,16 @@ def train(ctx: Context, params: torch.Tensor, h: int, stmt: torch.Tensor, block:
     return l0.value, l1.value
 
 
+def rank_loss(ctx: Context, scores: torch.Tensor, latencies: torch.Tensor, with_grad: bool = True):
+    """lambda_rank_loss(scores, latencies) (ranker.cpp:394-441) on the device:
+    (loss, d loss / d score or None)."""
+    scores, latencies = scores.contiguous(), latencies.contiguous()
+    grad = ctx.empty((scores.shape[0],), torch.float64) if with_grad else None
+    loss = C.c_double(0)
+    ctx.check(lib().tt_rank_loss(ctx.h, _p(scores), _p(latencies), scores.shape[0], C.byref(loss), _p(grad)))
+    return loss.value, grad
+
+
 def momentum_adapt(ctx: Context, phi: torch.Tensor, m: float, h: int, stmt: torch.Tensor, block: torch.Tensor,
                    latencies, **cfg):
     """momentum_adapt (momentum.cpp:48-56): target = phi, train(target),

@@ -50,6 +50,7 @@ def oracle():
             "tto_select_top": (C.c_int, [f64p, f64p, u8p, C.c_int64, C.c_int64, i64p]),
             "tto_momentum_update": (None, [f64p, f64p, C.c_int64, C.c_double]),
             "tto_gd_step": (None, [f64p, f64p, C.c_int64, C.c_double]),
+            "tto_rank_loss": (C.c_int, [f64p, f64p, C.c_int64, f64p, f64p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -78,6 +79,7 @@ def ref():
             "ref_score_batch": (C.c_int, [f64p, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_int64, C.c_int, C.c_int, f64p, u64p]),
             "ref_select_top": (C.c_int, [f64p, f64p, u8p, C.c_int64, C.c_int64, i64p]),
             "ref_momentum_update": (C.c_int, [f64p, f64p, C.c_int, C.c_double]),
+            "ref_rank_loss": (C.c_int, [f64p, f64p, C.c_int64, f64p, f64p]),
             "ref_train": (C.c_int, [f64p, C.c_int, C.c_int, C.c_int, f64p, f64p, f64p, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_uint64, f64p, f64p]),
             "ref_noiseless_latency": (C.c_int, [sk, dv, C.c_double, C.c_double, C.c_double, i32p, C.c_int64, C.c_int64, f64p]),
             "ref_measure": (C.c_int, [sk, P(OracleSpec), i32p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, f64p,
@@ -245,3 +247,21 @@ def R_oracle_best(sk, oracle, cap=1 << 30):
     lat = C.c_double(0)
     check(ref().ref_oracle_best(C.byref(sk), C.byref(oracle), cap, ptr(soa, i32p), C.byref(lat)))
     return soa, lat.value
+
+
+def O_rank_loss(scores, lat):
+    """lambda_rank_loss via the C restatement: (loss, grad) or None (kState)."""
+    scores, lat = np.ascontiguousarray(scores, np.float64), np.ascontiguousarray(lat, np.float64)
+    g = np.zeros(len(scores))
+    loss = C.c_double(0)
+    rc = oracle().tto_rank_loss(ptr(scores, f64p), ptr(lat, f64p), len(scores), C.byref(loss), ptr(g, f64p))
+    return None if rc else (loss.value, g)
+
+
+def R_rank_loss(scores, lat):
+    """lambda_rank_loss of the compiled reference: (loss, grad) or None (Error)."""
+    scores, lat = np.ascontiguousarray(scores, np.float64), np.ascontiguousarray(lat, np.float64)
+    g = np.zeros(len(scores))
+    loss = C.c_double(0)
+    rc = ref().ref_rank_loss(ptr(scores, f64p), ptr(lat, f64p), len(scores), C.byref(loss), ptr(g, f64p))
+    return None if rc else (loss.value, g)

@@ -78,3 +78,38 @@ def test_momentum_adapt_composes(ctx):
     assert rel(target.cpu().numpy(), G["train/p1"]) <= 1e-12
     want = target.cpu().numpy() + 0.99 * (phi0.cpu().numpy() - target.cpu().numpy())
     assert (phi.cpu().numpy() == want).all()
+
+
+@pytest.mark.parametrize("n,ties", [(2, False), (16, False), (256, True), (1000, True)])
+def test_rank_loss_matches_oracle(ctx, n, ties):
+    """tt_rank_loss (device LambdaRank) against the oracle's literal
+    ranker.cpp:394-441: the pair terms are the same expressions, only the
+    summation order differs (per-item gradient, fixed chunk order), so the
+    bar is 1e-13 relative to the largest |gradient| / the loss."""
+    rng = np.random.default_rng(100 + n)
+    sc = rng.normal(size=n)
+    lat = rng.uniform(1e-4, 1e-3, size=n)
+    if ties:
+        sc[::3] = sc[0]
+        lat[::4] = lat[1]
+    loss, g = tt.rank_loss(ctx, torch.from_numpy(sc).cuda(), torch.from_numpy(lat).cuda())
+    lo, go = R.O_rank_loss(sc, lat)
+    assert abs(loss - lo) <= 1e-13 * abs(lo)
+    assert np.abs(g.cpu().numpy() - go).max() <= 1e-13 * np.abs(go).max()
+
+
+def test_rank_loss_closed_forms_and_errors(ctx):
+    import math
+    loss, g = tt.rank_loss(ctx, torch.tensor([0.0, 0.0], dtype=torch.float64, device="cuda"),
+                           torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda"))
+    g0, g1 = 1.0, 2.0 ** 0.5 - 1.0
+    max_dcg = g0 / math.log2(2.0) + g1 / math.log2(3.0)
+    w = abs(g0 - g1) * abs(1.0 / math.log2(2.0) - 1.0 / math.log2(3.0)) / max_dcg
+    assert abs(loss - w * math.log(2.0)) <= 1e-12 * w * math.log(2.0)
+    g = g.cpu().numpy()
+    assert g[0] == -g[1]  # both endpoints evaluate the same slope
+    for sc, lat in [([1.0], [1.0]), ([1.0, 2.0], [1.0, 0.0])]:
+        with pytest.raises(tt.TTError) as e:
+            tt.rank_loss(ctx, torch.tensor(sc, dtype=torch.float64, device="cuda"),
+                         torch.tensor(lat, dtype=torch.float64, device="cuda"))
+        assert e.value.code == "E_STATE"

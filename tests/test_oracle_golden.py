@@ -310,3 +310,32 @@ def test_live_scores(h):
     p = R.O_init_params(h, 11)
     assert (bits(p) == bits(R.R_init_params(h, 11))).all()
     assert np.abs(R.O_score(p, h, st, bl) - R.R_score(p, h, rst, rbl)).max() <= 1e-12
+
+
+# ---- lambda_rank_loss (ranker.cpp:394-441): the oracle against the reference's
+# closed forms (test_ranker.cpp "rank loss closed forms") and, live, bit for bit
+def test_rank_loss_closed_forms():
+    import math
+    r = R.O_rank_loss([40.0, 30.0, 20.0, 10.0], [1.0, 2.0, 3.0, 4.0])
+    assert r[0] < 1e-4
+    loss, g = R.O_rank_loss([0.0, 0.0], [1.0, 2.0])
+    g0, g1 = 2.0 - 1.0, 2.0 ** 0.5 - 1.0
+    max_dcg = g0 / math.log2(2.0) + g1 / math.log2(3.0)
+    w = abs(g0 - g1) * abs(1.0 / math.log2(2.0) - 1.0 / math.log2(3.0)) / max_dcg
+    assert abs(loss - w * math.log(2.0)) <= 1e-12 * w * math.log(2.0)
+    assert g[0] == -g[1]
+    assert R.O_rank_loss([1.0], [1.0]) is None
+    assert R.O_rank_loss([1.0, 2.0], [1.0, 0.0]) is None
+
+
+@pytest.mark.skipif(not R.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("n,ties", [(2, False), (16, False), (64, True), (300, True)])
+def test_rank_loss_matches_reference(n, ties):
+    rng = np.random.default_rng(n)
+    sc = rng.normal(size=n)
+    lat = rng.uniform(1e-4, 1e-3, size=n)
+    if ties:  # repeated scores and latencies: index tie-breaks and skipped pairs
+        sc[::3] = sc[0]
+        lat[::4] = lat[1]
+    o, r = R.O_rank_loss(sc, lat), R.R_rank_loss(sc, lat)
+    assert o[0] == r[0] and (o[1] == r[1]).all()
