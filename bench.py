@@ -639,25 +639,67 @@ def _ref_setup(args):
     return R
 
 
-def cpu_baseline(args, budget_s=20.0):
-    """The reference's own round (oracle/_ref) on the host cores, on a
-    bounded sample of the workload: whole subgraph rounds until budget_s."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def strict_round(R, workload, n, k, b, seed, threads):
+    """The strict CPU bound of one round (oracle/_ref ref_round_strict): the reference's own
+    draft_cost / extract_features / score_batch / select_top over the resident population,
+    parallel_for + nth_element top-K, no string keys. Returns seconds (population given)."""
+    import ctypes as C
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    sk = make_sketch(WORKLOADS[workload]())
+    dev = reference_device()
+    params = R.R_init_params(64, derive_seed(seed, TAG_INIT))
+    pop = R.R_random_init(sk, seed, n)
+    sel, secs = np.zeros(b, np.int64), np.zeros(4)
+    R.check(R.ref().ref_round_strict(C.byref(sk), C.byref(dev), R.ptr(pop, R.i32p), pop.shape[1], n, k, b,
+                                     R.ptr(params, R.f64p), 64, threads, R.ptr(sel, R.i64p), R.ptr(secs, R.f64p)))
+    return float(secs.sum())
+
+
+def cpu_baseline(args, reps=5):
+    """The CPU reference on the box's host cores, on a bounded sample of the
+    workload: `reps` whole subgraph rounds (cycling the subgraphs) per setting, median
+    candidates/s. `value` = the reference's own round (explore(n_steps=1) +
+    extract_features + score_batch + select_top, oracle/_ref) on all host threads;
+    beside it the same at 1 thread and the strict hand-composed bound (ref_round_strict)
+    at 1 and all threads."""
     R = _ref_setup(args)
     if not R.ref_available():
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref missing"}
-    threads = os.cpu_count() or 1
-    done, secs, rounds = 0, 0.0, 0
-    t_end = time.time() + budget_s
+    nproc = os.cpu_count() or 1
     names = R50 if args.workload == "r50" else [args.workload]
-    while time.time() < t_end and rounds < 64:
-        w = names[rounds % len(names)]
-        s, _ = ref_round(R, w, args.n, args.k, args.b, args.seed + rounds, threads)
-        secs += s
-        done += args.n
-        rounds += 1
-    return {"value": done / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{rounds} reference rounds (explore(n_steps=1)+extract_features+score_batch+select_top, "
-                      f"threads={threads}) over {names[:rounds]}... N={args.n}, K={args.k}"}
+
+    def median_rate(fn, threads):
+        rates = []
+        for r in range(reps):
+            w = names[r % len(names)]
+            rates.append(args.n / fn(w, threads, r))
+        return statistics.median(rates), rates
+
+    api = lambda w, th, r: ref_round(R, w, args.n, args.k, args.b, args.seed + r, th)[0]  # noqa: E731
+    strict = lambda w, th, r: strict_round(R, w, args.n, args.k, args.b, args.seed + r, th)  # noqa: E731
+    v_all, r_all = median_rate(api, nproc)
+    v_one, _ = median_rate(api, 1)
+    s_all, _ = median_rate(strict, nproc)
+    s_one, _ = median_rate(strict, 1)
+    return {"value": v_all, "unit": UNIT, "cores": nproc, "kind": "reference",
+            "sample": f"median of {reps} whole reference rounds (explore(n_steps=1)+extract_features+score_batch+"
+                      f"select_top, N={args.n}, K={args.k}) over {names[:reps]}",
+            "cpu_model": cpu_model(), "rates_all_threads": r_all,
+            "reference_api_1_thread": v_one,
+            "strict_bound": {"value": s_all, "value_1_thread": s_one, "unit": UNIT, "threads": nproc,
+                             "what": "the reference's own draft_cost (parallel_for) + nth_element top-K with exact "
+                                     "dedup + extract_features + score_batch + select_top over the resident "
+                                     "population: no explore() string-key bookkeeping (ref_round_strict)"}}
 
 
 def ref_round(R, workload, n, k, b, seed, threads):

@@ -3,6 +3,7 @@
 // the reference's own public headers (proj/core/include/tiletune/*.hpp).
 #include "ref_capi.h"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -411,6 +412,71 @@ int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t
       for (std::size_t i = 0; i < ex.drafted.size(); ++i) put_sched(*sk, ex.drafted[i], drafted_soa, k, (int64_t)i);
     if (drafted_cost)
       for (std::size_t i = 0; i < ex.drafted.size(); ++i) drafted_cost[i] = ex.draft_costs[i];
+  });
+}
+
+/* A strict CPU bound for the round: the reference's own
+ * per-schedule functions composed by hand, without explore()'s serial
+ * string-key bookkeeping. The population is given (resident, like the
+ * device's `value`); draft_cost over it in parallel_for; the k lowest unique
+ * by (cost, index) via nth_element + sort + exact factor comparison among
+ * equal costs (equal schedules have equal costs; the lowest index is the
+ * first discovery, as in explore); extract_features in parallel;
+ * score_batch; select_top. Same drafted set and selection as ref_round on
+ * the same population. seconds: [0] draft + top-k, [1] features, [2] scores,
+ * [3] select. sel_pop_idx: population indices of the b selections. */
+int ref_round_strict(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld, int64_t n,
+                     int64_t k, int64_t b, const double* params, int h, int threads, int64_t* sel_pop_idx,
+                     double* seconds) {
+  return guard([&] {
+    Sketch s = to_sketch(*sk);
+    DeviceSpec d = to_dev(*dev);
+    RankerParams p = unflatten(params, h);
+    std::vector<Schedule> pop((size_t)n);
+    parallel_for((size_t)n, threads, [&](std::size_t i) { pop[i] = get_sched(*sk, soa, ld, (int64_t)i); });
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<double> cost((size_t)n);
+    parallel_for((size_t)n, threads, [&](std::size_t i) { cost[i] = draft_cost(s, pop[i], d).total; });
+    auto before = [&](int64_t a, int64_t c) { return cost[a] != cost[c] ? cost[a] < cost[c] : a < c; };
+    auto same = [&](const Schedule& x, const Schedule& y) {
+      return x.unroll == y.unroll && x.spatial_factors == y.spatial_factors &&
+             x.reduction_factors == y.reduction_factors;
+    };
+    std::vector<int64_t> ord((size_t)n), kept;
+    int64_t want = std::min<int64_t>(n, 2 * k + 64);
+    for (;;) {
+      for (int64_t i = 0; i < n; ++i) ord[i] = i;
+      std::nth_element(ord.begin(), ord.begin() + (want - 1), ord.end(), before);
+      std::sort(ord.begin(), ord.begin() + want, before);
+      kept.clear();
+      for (int64_t q = 0; q < want && (int64_t)kept.size() < k; ++q) {
+        const int64_t i = ord[q];
+        bool dup = false;
+        for (auto it = kept.rbegin(); it != kept.rend() && cost[*it] == cost[i]; ++it)
+          if (same(pop[*it], pop[i])) {
+            dup = true;
+            break;
+          }
+        if (!dup) kept.push_back(i);
+      }
+      if ((int64_t)kept.size() >= k || want == n) break;
+      want = std::min<int64_t>(n, 2 * want);
+    }
+    seconds[0] = secs_since(t0);
+    auto t1 = std::chrono::steady_clock::now();
+    std::vector<HybridFeature> feats(kept.size());
+    parallel_for(feats.size(), threads, [&](std::size_t i) { feats[i] = extract_features(s, pop[kept[i]], d); });
+    seconds[1] = secs_since(t1);
+    auto t2 = std::chrono::steady_clock::now();
+    std::vector<double> scores = score_batch(p, feats, {}, threads);
+    seconds[2] = secs_since(t2);
+    auto t3 = std::chrono::steady_clock::now();
+    std::vector<double> dcost(kept.size());
+    for (std::size_t i = 0; i < kept.size(); ++i) dcost[i] = cost[kept[i]];
+    std::vector<char> excluded(scores.size(), 0);
+    auto sel = select_top(scores, dcost, excluded, (std::size_t)b);
+    seconds[3] = secs_since(t3);
+    for (int64_t i = 0; i < b; ++i) sel_pop_idx[i] = kept[sel[i]];
   });
 }
 

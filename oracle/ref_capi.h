@@ -83,6 +83,10 @@ int ref_records_from_jsonl(const tt_sketch* sk, const char* task, const char* te
  * explore(n_steps=1) -> extract_features x K -> score_batch -> select_top.
  * Writes the selected b schedules' ranks into sel_idx (positions within the
  * drafted list) and wall seconds per stage into seconds[4]. */
+/* strict CPU bound of the round over a given population (see ref_capi.cpp) */
+int ref_round_strict(const tt_sketch* sk, const tt_device_spec* dev, const int32_t* soa, int64_t ld, int64_t n,
+                     int64_t k, int64_t b, const double* params, int h, int threads, int64_t* sel_pop_idx,
+                     double* seconds);
 int ref_round(const tt_sketch* sk, const tt_device_spec* dev, int64_t n, int64_t k, int64_t b,
               uint64_t seed, const double* params, int h, int threads, int64_t* sel_idx,
               double* sel_scores, int32_t* drafted_soa, double* drafted_cost,

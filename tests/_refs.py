@@ -85,6 +85,8 @@ def ref():
             "ref_measure": (C.c_int, [sk, P(OracleSpec), i32p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, f64p,
                                       f64p]),
             "ref_oracle_best": (C.c_int, [sk, P(OracleSpec), C.c_uint64, i32p, f64p]),
+            "ref_round_strict": (C.c_int, [sk, dv, i32p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, f64p, C.c_int,
+                                           C.c_int, i64p, f64p]),
             "ref_round": (C.c_int, [sk, dv, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, f64p, C.c_int, C.c_int, i64p, f64p, i32p, f64p, i64p, f64p]),
         }
         for name, (res, args) in sig.items():

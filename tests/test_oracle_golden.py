@@ -339,3 +339,26 @@ def test_rank_loss_matches_reference(n, ties):
         lat[::4] = lat[1]
     o, r = R.O_rank_loss(sc, lat), R.R_rank_loss(sc, lat)
     assert o[0] == r[0] and (o[1] == r[1]).all()
+
+
+@pytest.mark.skipif(not R.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name", ["gemm1024", "r50_c3x3_64"])
+def test_strict_cpu_round_selects_what_the_reference_round_selects(name):
+    """bench.py's strict CPU bound (ref_round_strict: the reference's own
+    per-schedule functions without explore's string keys) must select the
+    same schedules as the reference's round on the same population."""
+    import ctypes as C
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    sk, dev = make_sketch(WORKLOADS[name]()), reference_device()
+    n, k, b, seed = 4096, 256, 10, 5
+    params = R.R_init_params(64, derive_seed(seed, TAG_INIT))
+    sel, sc, cnt, secs = np.zeros(b, np.int64), np.zeros(b), C.c_int64(0), np.zeros(4)
+    dsoa, dcost = np.zeros((sk.cols, k), np.int32), np.zeros(k)
+    R.check(R.ref().ref_round(C.byref(sk), C.byref(dev), n, k, b, seed, R.ptr(params, R.f64p), 64, 4,
+                              R.ptr(sel, R.i64p), R.ptr(sc, R.f64p), R.ptr(dsoa, R.i32p), R.ptr(dcost, R.f64p),
+                              C.byref(cnt), R.ptr(secs, R.f64p)))
+    pop = R.R_random_init(sk, seed, n)
+    sel2 = np.zeros(b, np.int64)
+    R.check(R.ref().ref_round_strict(C.byref(sk), C.byref(dev), R.ptr(pop, R.i32p), pop.shape[1], n, k, b,
+                                     R.ptr(params, R.f64p), 64, 4, R.ptr(sel2, R.i64p), R.ptr(secs, R.f64p)))
+    assert (pop[:, sel2] == dsoa[:, sel]).all()
