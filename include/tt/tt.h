@@ -272,6 +272,27 @@ int tt_round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index_host, dou
 int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev,
                          const tt_round_config* cfg, const int32_t* soa_dev, int64_t ld, uint64_t seed,
                          double* cost_dev, int64_t* gidx_dev, uint64_t* identity_dev);
+/* ------------------------------------------ multi-GPU -- */
+/* One process per GPU. Rank 0 creates a unique id (128 bytes) and shares it
+ * with the others out of band (MPI, a file, torch.distributed...); every rank
+ * then calls tt_comm_init on its context. NCCL (libnccl.so.2) is loaded at
+ * run time: TT_E_NCCL when it is missing or a collective fails. */
+int tt_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+int tt_comm_init(tt_ctx* ctx, int nranks, int rank, const uint8_t* id /* 128 bytes */);
+int tt_comm_destroy(tt_ctx* ctx);
+/* The sharded round in one call (tuner.cpp:361-396 over R GPUs): cfg->n is
+ * the GLOBAL population, split by index range (the first n % R ranks take one
+ * extra candidate, cfg->first offsets the whole range); this rank drafts its
+ * shard (soa_shard = its slice with ld, or NULL for the counter-based
+ * stream of `seed`), one ncclAllGather of the K-entry (cost, global index,
+ * identity) lists on the context stream, merge, verify, select — every rank
+ * returns the same selection, equal to tt_round over the whole population.
+ * A rank whose device selector overflowed makes every rank re-run its draft
+ * half with tt_round_local. Synchronous, collective. */
+int tt_round_sharded(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, const tt_round_config* cfg,
+                     const int32_t* soa_shard_dev, int64_t ld, uint64_t seed, int64_t* sel_index_host,
+                     double* sel_score_host, double* sel_cost_host, uint64_t* sel_identity_host,
+                     tt_round_result* result_host);
 /* Synchronous draft half (same payload): the selector's host-driven retries
  * (doubled margin, then the hash path for > 4096 ties) and the population
  * check run here, so it fails only where tt_round fails (TT_E_VALIDATE for

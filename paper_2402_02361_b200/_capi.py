@@ -90,6 +90,11 @@ _SIGS = [
     ("tt_round_drafted", C.c_int, [vp, P(vp), P(vp), P(vp), P(vp)]),
     ("tt_round_local_async", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64,
                                        vp, vp, vp]),
+    ("tt_comm_unique_id", C.c_int, [vp]),
+    ("tt_comm_init", C.c_int, [vp, C.c_int, C.c_int, vp]),
+    ("tt_comm_destroy", C.c_int, [vp]),
+    ("tt_round_sharded", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64,
+                                   i64p, f64p, f64p, u64p, P(RoundResult)]),
     ("tt_round_local", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, C.c_int64, C.c_uint64,
                                  vp, vp, vp]),
     ("tt_round_finish_merged_async", C.c_int, [vp, P(Sketch), P(DeviceSpec), P(RoundConfig), vp, vp, vp,

@@ -1,6 +1,8 @@
 // tt_api.cu — the C ABI of include/tt/tt.h: context, validation, plan
 // compilation (tt_sketch -> DevSketch) and the round orchestration.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen()ed by tt_comm_init
 
 #include <algorithm>
 #include <atomic>
@@ -71,6 +73,12 @@ struct tt_ctx {
   } tr;
   double* h_loss = nullptr;  // pinned: training losses read back once per call
   int64_t h_loss_cap = 0;
+  // NCCL communicator of tt_round_sharded (tt_comm_init); payload / gathered
+  // [R][3][K] / merged [3][R K] int64 device buffers
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+  int64_t* d_gather = nullptr;
+  int64_t gather_cap = 0;
   // multi-step explore (GA): one generation on the device, its pinned host mirror
   size_t ex_dcap = 0, ex_hcap = 0;
   void* d_ex = nullptr;  // two device generation slots + the RNG state
@@ -571,6 +579,7 @@ void tt_ctx_destroy(tt_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) tt_comm_destroy(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (auto& pr : c->ev_live) cudaEventDestroy(pr.second.first), cudaEventDestroy(pr.second.second);
   void* ptrs[] = {c->sel.cost, c->sel.hist, c->sel.skey, c->sel.sidx, c->sel.sample, c->sel.sfp, c->sel.rank, c->sel.dup, c->sel.tkeys, c->sel.tvals, c->sel.state, c->sel.mscratch,
@@ -579,7 +588,7 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
                   c->d_tiles, c->d_ex, c->d_mix, c->tr.slots, c->tr.work, c->tr.grads, c->tr.dscore,
-                  c->tr.scores, c->tr.rank, c->tr.lat, c->tr.loss, c->tr.list, c->tr.bad};
+                  c->tr.scores, c->tr.rank, c->tr.lat, c->tr.loss, c->tr.list, c->tr.bad, c->d_gather};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int r = 0; r < tt_ctx::kRing; ++r) {
@@ -1977,3 +1986,127 @@ int tt_draft_set(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, in
   *count_host = cnt;
   return TT_OK;
 }
+
+// ------------------------------------------------------------------------
+// NCCL: the sharded round inside the C ABI. libnccl is loaded
+// at run time (dlopen), so the library has no link-time NCCL dependency;
+// in a process that already loaded NCCL (e.g. torch), the same library is used.
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+      return a;
+    }
+    a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    a.all_gather = (decltype(a.all_gather))dlsym(h, "ncclAllGather");
+    a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+    a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_unique_id && a.comm_init_rank && a.all_gather && a.comm_destroy && a.error_string;
+    if (!a.ok) a.why = "libnccl lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+int nccl_fail(tt_ctx* ctx, ncclResult_t r, const char* what) {
+  return fail(ctx, TT_E_NCCL, std::string(what) + ": " + nccl().error_string(r));
+}
+}  // namespace
+
+extern "C" {
+
+int tt_comm_unique_id(uint8_t* id_out) {
+  NcclApi& a = nccl();
+  if (!a.ok) return TT_E_NCCL;
+  ncclUniqueId id;
+  if (a.get_unique_id(&id) != ncclSuccess) return TT_E_NCCL;
+  std::memcpy(id_out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return TT_OK;
+}
+
+int tt_comm_init(tt_ctx* ctx, int nranks, int rank, const uint8_t* id) {
+  if (!ctx) return TT_E_STATE;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, TT_E_CONFIG, "comm: rank outside [0, nranks)");
+  if (ctx->comm) return fail(ctx, TT_E_STATE, "comm: already initialised on this context");
+  NcclApi& a = nccl();
+  if (!a.ok) return fail(ctx, TT_E_NCCL, "comm: " + a.why);
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t c = nullptr;
+  cudaSetDevice(ctx->device);
+  const ncclResult_t r = a.comm_init_rank(&c, nranks, uid, rank);
+  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommInitRank");
+  ctx->comm = c, ctx->nranks = nranks, ctx->rank = rank;
+  return TT_OK;
+}
+
+int tt_comm_destroy(tt_ctx* ctx) {
+  if (!ctx) return TT_E_STATE;
+  if (!ctx->comm) return TT_OK;
+  cudaStreamSynchronize(ctx->stream);
+  const ncclResult_t r = nccl().comm_destroy((ncclComm_t)ctx->comm);
+  ctx->comm = nullptr, ctx->nranks = 1, ctx->rank = 0;
+  return r == ncclSuccess ? TT_OK : nccl_fail(ctx, r, "ncclCommDestroy");
+}
+
+int tt_round_sharded(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
+                     const int32_t* soa_shard, int64_t ld, uint64_t seed, int64_t* sel_index, double* sel_score,
+                     double* sel_cost, uint64_t* sel_id, tt_round_result* res) {
+  if (!ctx) return TT_E_STATE;
+  if (!cfg) return fail(ctx, TT_E_STATE, "null round config");
+  if (!ctx->comm) return fail(ctx, TT_E_STATE, "round_sharded: tt_comm_init first");
+  if (!ctx->pend.empty())
+    return fail(ctx, TT_E_STATE, "round_sharded: rounds still in flight (tt_round_collect them first)");
+  const int R = ctx->nranks, r = ctx->rank;
+  const int64_t k = cfg->k, n = cfg->n;
+  if (n < R) return fail(ctx, TT_E_CONFIG, "round_sharded: fewer candidates than ranks");
+  if ((int64_t)R * k > kMergeMax) return fail(ctx, TT_E_CONFIG, "round_sharded: ranks * draft_size > 65536");
+  // shard_range (sharded.py): the first n % R ranks take one extra candidate
+  const int64_t base = n / R, extra = n % R;
+  tt_round_config local = *cfg;
+  local.first = cfg->first + r * base + std::min<int64_t>(r, extra);
+  local.n = base + (r < extra ? 1 : 0);
+  int rc;
+  if ((rc = tgrow(ctx, ctx->d_gather, ctx->gather_cap, 3 * k * (int64_t)(2 * R + 1)))) return rc;
+  int64_t* payload = ctx->d_gather;             // [3][k]: cost bits, global index, identity
+  int64_t* gathered = payload + 3 * k;          // [R][3][k]
+  int64_t* merged = gathered + 3 * k * R;       // [3][R k]
+  auto draft = [&](bool sync) {
+    return (sync ? tt_round_local : tt_round_local_async)(ctx, sk, dev, &local, soa_shard, ld, seed, (double*)payload,
+                                                          payload + k, (uint64_t*)(payload + 2 * k));
+  };
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if ((rc = draft(attempt > 0))) return rc;
+    const ncclResult_t nr = nccl().all_gather(payload, gathered, (size_t)(3 * k), ncclInt64, (ncclComm_t)ctx->comm,
+                                              ctx->stream);
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllGather");
+    for (int row = 0; row < 3; ++row)  // R consecutive [3][k] payloads -> one [3][R k] table
+      TT_CUDA(ctx, cudaMemcpy2DAsync(merged + row * R * k, k * 8, gathered + row * k, 3 * k * 8, k * 8, R,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+    tt_round_config m = *cfg;
+    m.first = 0;
+    rc = tt_round_finish_merged(ctx, sk, dev, &m, (const double*)merged, merged + R * k,
+                                (const uint64_t*)(merged + 2 * R * k), R * k, sel_index, sel_score, sel_cost, sel_id,
+                                res);
+    // a rank's selector overflow is seen by every rank in the merged status:
+    // all re-run the draft half synchronously (host-driven retries, hash path)
+    if (rc == TT_E_STATE && attempt == 0 && ctx->err.find("tt_round_local") != std::string::npos) continue;
+    return rc;
+  }
+  return rc;
+}
+
+}  // extern "C"

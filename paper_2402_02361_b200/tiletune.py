@@ -472,6 +472,38 @@ def round_local_async(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: 
                                          seed & (2**64 - 1), _p(out[0]), _p(out[1]), _p(out[2])))
 
 
+def comm_unique_id() -> bytes:
+    """NCCL unique id for tt_comm_init (create on rank 0, share out of band)."""
+    buf = (C.c_uint8 * 128)()
+    rc = lib().tt_comm_unique_id(buf)
+    if rc:
+        raise TTError("E_NCCL", "tt_comm_unique_id failed (libnccl.so.2 missing?)")
+    return bytes(buf)
+
+
+def comm_init(ctx: Context, nranks: int, rank: int, uid: bytes):
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    ctx.check(lib().tt_comm_init(ctx.h, nranks, rank, buf))
+
+
+def comm_destroy(ctx: Context):
+    ctx.check(lib().tt_comm_destroy(ctx.h))
+
+
+def round_sharded(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, seed: int = 0,
+                  soa_shard: torch.Tensor | None = None, precision: int = TT_PREC_FP64, band: float | None = None,
+                  first: int = 0, toggles: int = TT_TOGGLES_ALL) -> RoundOutput:
+    """tt_round_sharded: the whole sharded round (n = global population) over
+    the context's NCCL communicator; every rank gets the same selection."""
+    cfg = _round_cfg(n, k, b, precision, band, first, toggles)
+    ix, sc, co, idv = (C.c_int64 * b)(), (C.c_double * b)(), (C.c_double * b)(), (C.c_uint64 * b)()
+    res = RoundResult()
+    ld = soa_shard.stride(0) if soa_shard is not None else 0
+    ctx.check(lib().tt_round_sharded(ctx.h, C.byref(sketch), C.byref(dev), C.byref(cfg), _p(soa_shard), ld,
+                                     seed & (2**64 - 1), ix, sc, co, idv, C.byref(res)))
+    return _round_out(b, res, ix, sc, co, idv)
+
+
 def round_local(ctx: Context, sketch: Sketch, dev: DeviceSpec, n: int, k: int, b: int, first: int,
                 out: torch.Tensor, seed: int = 0, soa: torch.Tensor | None = None, toggles: int = TT_TOGGLES_ALL):
     """Synchronous draft half (tt_round_local): the same payload with the

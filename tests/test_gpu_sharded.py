@@ -174,3 +174,70 @@ def test_failed_rank_fails_every_merged_round():
         _two_rank_payloads(tt, ctx, sk, dev, n, k, b, 0, soa=pops, sync=True)
     assert e.value.code == "E_VALIDATE"
     ctx.close()
+
+
+def test_c_abi_sharded_round_single_rank():
+    """tt_comm_init + tt_round_sharded (the collective inside the C ABI,
+    NCCL loaded at run time) on a one-rank communicator: equal to tt_round."""
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    ctx = tt.Context(0)
+    tt.PaCM(ctx, tt.init_params(64, derive_seed(9, TAG_INIT)), 64)
+    tt.comm_init(ctx, 1, 0, tt.comm_unique_id())
+    sk, dev = make_sketch(WORKLOADS["bert_ffn2"]()), reference_device()
+    n, k, b = 100000, 512, 10
+    got = tt.round_sharded(ctx, sk, dev, n, k, b, seed=9)
+    want = tt.draft_verify_round(ctx, sk, dev, n, k, b, seed=9)
+    assert (got.index == want.index).all() and (got.identity == want.identity).all()
+    soa = tt.random_init(ctx, sk, n, 9)
+    got2 = tt.round_sharded(ctx, sk, dev, n, k, b, soa_shard=soa)
+    assert (got2.index == want.index).all()
+    tt.comm_destroy(ctx)
+    ctx.close()
+
+
+def _c_abi_worker(rank, world, uid_q, name, n, k, b, seed, q):
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    try:
+        torch.cuda.set_device(rank)
+        ctx = tt.Context(rank)
+        tt.PaCM(ctx, tt.init_params(64, derive_seed(seed, TAG_INIT)), 64)
+        if rank == 0:
+            uid = tt.comm_unique_id()
+            for _ in range(world - 1):
+                uid_q.put(uid)
+        else:
+            uid = uid_q.get(timeout=60)
+        tt.comm_init(ctx, world, rank, uid)
+        out = tt.round_sharded(ctx, make_sketch(WORKLOADS[name]()), reference_device(), n, k, b, seed=seed)
+        q.put((rank, out.index.tolist()))
+        tt.comm_destroy(ctx)
+        ctx.close()
+    except Exception as e:
+        q.put((rank, "error " + repr(e)))
+        raise
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs for an NCCL group")
+def test_c_abi_sharded_round_multi_gpu():
+    """The C-ABI collective over R GPUs (no torch.distributed): every rank's
+    selection equals the one-GPU round over the whole population."""
+    from paper_2402_02361_b200 import tiletune as tt
+    from paper_2402_02361_b200.types import TAG_INIT, WORKLOADS, derive_seed, make_sketch, reference_device
+    name, n, k, b, seed = "bert_qkv", 1 << 20, 512, 10, 21
+    world = min(torch.cuda.device_count(), 8)
+    ctx = tt.Context(0)
+    tt.PaCM(ctx, tt.init_params(64, derive_seed(seed, TAG_INIT)), 64)
+    want = tt.draft_verify_round(ctx, make_sketch(WORKLOADS[name]()), reference_device(), n, k, b, seed=seed)
+    ctx.close()
+    c = mp.get_context("spawn")
+    q, uq = c.Queue(), c.Queue()
+    procs = [c.Process(target=_c_abi_worker, args=(r, world, uq, name, n, k, b, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(120)
+    for r in range(world):
+        assert res[r] == want.index.tolist(), (r, res[r])
