@@ -1146,24 +1146,34 @@ int launch_select(const DevSketch& S, const DevDevice& D, const int32_t* soa, in
 // Runs on the context's side stream, overlapped with features + PaCM: the
 // exact identity (mixed-radix composition ranks) is a long serial chain per
 // candidate and only the b selections' identities are reported.
+// sync (optional, the fused verify's handshake): sync[1] block ticket, sync[2]
+// completed-kernel epoch, advanced once every identity is written.
 template <int NSP, int NRED, bool SEED>
 __global__ void __launch_bounds__(128) k_drafted_identity(DevSketch S, Src src, const int64_t* __restrict__ idx,
                                                           const int64_t* __restrict__ count_dev, int64_t k_max,
-                                                          uint64_t* __restrict__ out) {
+                                                          uint64_t* __restrict__ out, unsigned* __restrict__ sync) {
   const int64_t cnt = count_dev ? (*count_dev < k_max ? *count_dev : k_max) : k_max;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < cnt; p += (int64_t)gridDim.x * blockDim.x)
     out[p] = identity_at<NSP, NRED, SEED>(S, src, idx[p] - src.index_base);
+  if (!sync) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&sync[1], 1u) == gridDim.x - 1) {
+    sync[1] = 0u;
+    __threadfence();
+    atomicAdd(&sync[2], 1u);
+  }
 }
 
 int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
                             bool seeded, const int64_t* idx, const int64_t* count_dev, int64_t k_max, uint64_t* out,
-                            cudaStream_t st) {
+                            cudaStream_t st, unsigned* sync) {
   if (k_max <= 0) return 0;
   Src src{soa, ld, s0, first, first};
   const int g = grid_for(k_max, 128, 148);
   if (seeded)
-    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, true><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
-  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out)));
+    return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, true><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out, sync)));
+  return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out, sync)));
 }
 
 __global__ void k_mark_invalid(const int* __restrict__ invalid, int64_t* __restrict__ out_idx) {

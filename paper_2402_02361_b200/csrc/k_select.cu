@@ -10,20 +10,12 @@
 #include <cstdint>
 
 #include "tt_block.cuh"
+#include "tt_finish.cuh"
 #include "tt_kernels.h"
 
 namespace tt {
 
 constexpr int kSelTile = 4096;
-constexpr uint64_t kAll = ~0ull;
-
-// -0.0 and +0.0 map to one key: the reference comparator (scores[a] !=
-// scores[c]) treats them as equal and falls through to the draft cost
-__device__ __forceinline__ uint64_t ordered(double x) {
-  if (x == 0.0) x = 0.0;
-  const uint64_t u = (uint64_t)__double_as_longlong(x);
-  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
 
 constexpr int kTopbE = 4;  // keys per thread
 
@@ -279,106 +271,14 @@ int launch_momentum(double* phi, const double* target, int64_t n, double m, cuda
 }
 
 // ------------------------------------------------------------ finish ----
-// The round's select_top (ranker.cpp:514-532: score desc, draft cost asc,
-// position asc; excluded never chosen) fused with the record gather for the
-// single device->host copy: [0] selected, [1] drafted, [2] status, [3]
-// rescored, then b population indices, b scores, b draft costs, b
-// identities. n <= 1024, b <= 32: every warp sorts its 32 keys with
-// shuffles (15 exchange steps, no shared-memory network), then warp 0 runs a
-// b-step tournament over the warps' sorted lists.
-__device__ __forceinline__ void warp_sort32(Key3& k) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const Key3 o = k.shfl_xor(stride);
-      const bool lower = (lane & stride) == 0, up = (lane & size) == 0;
-      const bool take = (lower == up) ? o.lt(k) : k.lt(o);
-      if (take) k = o;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scores, const double* __restrict__ drafts,
                                                  const uint8_t* __restrict__ excluded, int64_t n_max,
                                                  const int64_t* __restrict__ n_dev, int64_t b,
                                                  const int64_t* __restrict__ idx, const uint64_t* __restrict__ id,
                                                  const SelState* __restrict__ sel, const int* __restrict__ rescored,
                                                  const double* __restrict__ fast, int64_t* __restrict__ out) {
-  __shared__ Key3 lists[32][33];
-  __shared__ int avail;
-  __shared__ unsigned long long band_err;
-  __shared__ int16_t rank_of[1024];  // output position of each selected candidate, -1 otherwise
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
-  // every global read issued up front, independent of each other (one
-  // memory round trip): the count, this thread's candidate, and the record
-  // fields it writes if it is selected
-  const int64_t nd = n_dev ? *n_dev : n_max;
-  const bool in = t < n_max;
-  const double s_t = in ? scores[t] : 0.0, d_t = in ? drafts[t] : 0.0;
-  const bool ex_t = in && excluded && excluded[t];
-  const int64_t ix_t = in ? idx[t] : -1;
-  const uint64_t id_t = in && id ? id[t] : 0;
-  const int64_t st = t == 0 && sel ? (int64_t)sel->status : 0;
-  const int64_t rs = t == 0 && rescored ? (int64_t)*rescored : 0;
-  const double f_t = in && fast ? fast[t] : 0.0;
-  if (t == 0) avail = 0, band_err = 0ull;
-  rank_of[t] = -1;
-  __syncthreads();
-  const int64_t n = nd < n_max ? nd : n_max;
-  const bool ok = t < n && !ex_t;
-  if (fast) {  // the certification's premise, checked on the rescored set
-    double err = ok ? fabs(s_t - f_t) : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, off));
-    if (lane == 0 && err > 0.0) atomicMax(&band_err, (unsigned long long)__double_as_longlong(err));
-  }
-  Key3 k;
-  k.a = ok ? ~ordered(s_t) : kAll;
-  k.b = ok ? ordered(d_t) : kAll;
-  k.c = ok ? (uint32_t)t : 0xffffffffu;
-  const unsigned bal = __ballot_sync(0xffffffffu, ok);
-  if (lane == 0 && bal) atomicAdd(&avail, __popc(bal));
-  warp_sort32(k);
-  lists[warp][lane] = k;
-  if (lane == 0) lists[warp][32].a = kAll, lists[warp][32].b = kAll, lists[warp][32].c = 0xffffffffu;
-  __syncthreads();
-  const int64_t keep = b < avail ? b : avail;
-  if (warp == 0) {  // tournament: lane w holds the head of warp w's list
-    int head = 0;
-    for (int it = 0; it < keep; ++it) {
-      Key3 h;
-      if (lane < nw) h = lists[lane][head];
-      else h.a = kAll, h.b = kAll, h.c = 0xffffffffu;
-      Key3 m = h;
-      int who = lane;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const Key3 o = m.shfl_xor(off);
-        const int ow = __shfl_xor_sync(0xffffffffu, who, off);
-        if (o.lt(m)) m = o, who = ow;
-      }
-      if (lane == 0) rank_of[m.c] = (int16_t)it;
-      if (lane == who) ++head;
-    }
-  }
-  __syncthreads();
-  int64_t* ix = out + kRecHead;
-  double* sc = (double*)(ix + b);
-  double* co = sc + b;
-  uint64_t* ids = (uint64_t*)(co + b);
-  const int r = rank_of[t];
-  if (r >= 0) ix[r] = ix_t, sc[r] = s_t, co[r] = d_t, ids[r] = id_t;  // the selected candidate writes its own entry
-  if (t >= keep && t < b) ix[t] = -1, sc[t] = 0.0, co[t] = 0.0, ids[t] = 0;
-  if (t == 0) {
-    out[0] = keep;
-    out[1] = n;
-    out[2] = st;
-    out[3] = rs;
-    out[4] = 0;
-    out[5] = (int64_t)band_err;
-  }
+  __shared__ FinishSmem fs;
+  finish_block(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, fast, out, fs);
 }
 
 // Certification band for the tensor-core path, one CTA (n <= 1024,

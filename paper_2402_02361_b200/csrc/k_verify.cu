@@ -15,18 +15,38 @@
 #include <cstdint>
 
 #include "tt_features.cuh"
+#include "tt_finish.cuh"
 #include "tt_kernels.h"
 #include "tt_pacm64.cuh"
 
 namespace tt {
 
+// Finish fused in (FinishArgs.record != nullptr): every candidate's identity
+// is written next to its features (no side-stream identity kernel), and the
+// last CTA to finish (ticket) runs select_top + the record gather
+// (tt_finish.cuh) over the whole drafted set in shared memory the PaCM
+// passes are done with.
+__device__ unsigned long long g_fin_ns[3];  // the last CTA's finish: start, end, identities ready (%globaltimer)
+
+struct FinishArgs {
+  const double* drafts;     // draft costs of the drafted set
+  const int64_t* idx;       // population indices
+  uint64_t* ids;            // identities (from the side stream, or known)
+  const SelState* sel;      // selector status
+  int64_t b;
+  int64_t* record;          // the round record (null: no finish)
+  unsigned* sync;           // see VerifyFinish
+  int wait_ids;
+};
+
 template <int NSP, int NRED>
 __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice D, CandRef ref,
                                                        const int64_t* __restrict__ count_dev, int64_t k_max,
                                                        const double* __restrict__ params,
-                                                       double* __restrict__ score_out) {
+                                                       double* __restrict__ score_out, FinishArgs fin) {
   using namespace f64;
   __shared__ CandInfo<NSP, NRED> ci[G];
+  __shared__ bool last;
   const int S = 2 * SK.n_in + 2;
   const int B = SK.kind == TT_OP_ELEMENTWISE ? 1 : 3 * SK.n_in + 2;
   pacm_h64_body(S, B, count_dev, k_max, params, score_out, [&](int64_t e0, int64_t count, double* MISC) {
@@ -64,12 +84,56 @@ __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice 
       }
     }
   });
+  if (!fin.record) return;
+  // ---- finish: the last CTA done runs select_top + the record over all scores
+  __threadfence();  // this CTA's scores / identities before its ticket
+  __syncthreads();
+  __shared__ int ids_ready;
+  if (threadIdx.x == 0) last = atomicAdd(&fin.sync[0], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) {
+    fin.sync[0] = 0u;  // for the next launch (graph replays)
+    g_fin_ns[0] = gtimer64();
+    int ok = 1;
+    if (fin.wait_ids) {  // the side-stream identity kernel of this round (epoch handshake)
+      const unsigned want = atomicAdd(&fin.sync[3], 1u) + 1u;
+      const unsigned long long t0 = gtimer64();
+      while ((int)(atomicAdd(&fin.sync[2], 0u) - want) < 0) {
+        if (gtimer64() - t0 > 2000000ull) {  // 2 ms: never expected; compute them here instead
+          ok = 0;
+          break;
+        }
+        __nanosleep(256);
+      }
+    }
+    ids_ready = ok;
+    g_fin_ns[2] = gtimer64();
+  }
+  __syncthreads();
+  __threadfence();
+  if (!ids_ready) {  // fallback: every drafted candidate's identity, one per thread
+    const int64_t cnt = *count_dev < k_max ? *count_dev : k_max;
+    for (int64_t p = threadIdx.x; p < cnt; p += blockDim.x) {
+      Factors<NSP, NRED> F;
+      feat_load<NSP, NRED>(SK, ref, p, F);
+      fin.ids[p] = identity_of<NSP, NRED>(SK, F);
+    }
+    __syncthreads();
+  }
+  extern __shared__ __align__(128) double smf[];
+  finish_block(score_out, fin.drafts, nullptr, k_max, count_dev, fin.b, fin.idx, fin.ids, fin.sel, nullptr, nullptr,
+               fin.record, *reinterpret_cast<FinishSmem*>(smf));
+  if (threadIdx.x == 0) g_fin_ns[1] = gtimer64();
 }
 
 int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
-                    const double* params, int h, double* score_out, cudaStream_t st) {
+                    const double* params, int h, double* score_out, cudaStream_t st, const VerifyFinish* vf) {
   const int ns = 2 * S.n_in + 2, nb = S.kind == TT_OP_ELEMENTWISE ? 1 : 3 * S.n_in + 2;
   if (h != f64::H || ns > 8 || nb > 8 || k_max <= 0) return -1;
+  if (vf && !verify64_finish_ok(k_max, vf->b)) return -1;  // finish_block: one key per thread
+  FinishArgs fin{};
+  if (vf) fin = FinishArgs{vf->drafts, vf->idx, vf->ids, vf->sel, vf->b, vf->record, vf->sync, vf->wait_ids};
   const int64_t ctas = (k_max + f64::G - 1) / f64::G;
   const dim3 grid((unsigned)(ctas < 148 ? ctas : 148));
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
@@ -80,7 +144,7 @@ int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const i
     }
     tt::note_launch();
     launch_pdl(k_verify64<NSP, NRED>, grid, dim3(f64::T), f64::kSmem, st, S, D, ref, count_dev, k_max, params,
-               score_out);
+               score_out, fin);
   }));
 }
 
@@ -94,5 +158,10 @@ extern "C" int ttdbg_verify64_span(unsigned long long* out, int reset) {
     const unsigned long long init[4] = {~0ull, ~0ull, 0ull, 0ull};
     return (int)cudaMemcpyToSymbol(tt::g_h64_ns, init, sizeof(init));
   }
-  return (int)cudaMemcpyFromSymbol(out, tt::g_h64_ns, sizeof(unsigned long long) * 4);
+  int rc = (int)cudaMemcpyFromSymbol(out, tt::g_h64_ns, sizeof(unsigned long long) * 4);
+  return rc ? rc : (int)cudaMemcpyFromSymbol(out + 4, tt::g_fin_ns, sizeof(unsigned long long) * 3);
+}
+
+extern "C" int ttdbg_verify64_finish_clocks(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_fin_clk, sizeof(long long) * 8);
 }

@@ -49,6 +49,7 @@ struct tt_ctx {
   int64_t* d_pos_fast_count = nullptr;
   int* d_status = nullptr;
   int64_t* d_record = nullptr;
+  unsigned* d_ticket = nullptr;  // k_verify64's last-CTA ticket (zero between launches)
   // PaCM params
   double* d_params = nullptr;
   int h = 0;
@@ -156,6 +157,11 @@ void prof_k1_collect(tt_ctx* c) {
   c->sel.k1_ev[0] = c->sel.k1_ev[1] = nullptr;
 }
 
+void prof_drop(tt_ctx* c, int stage) {  // an opened stage that did not run
+  if (!c->ev_open[stage]) return;
+  c->ev_pool.push_back(c->ev_open[stage]);
+  c->ev_open[stage] = nullptr;
+}
 void prof_end(tt_ctx* c, int stage) {
   if (!c->prof || !c->ev_open[stage]) return;
   cudaEvent_t e = ev_get(c);
@@ -568,6 +574,8 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaMalloc((void**)&c->d_pos_count, sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_pos_fast_count, sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_status, 2 * sizeof(int)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_ticket, 4 * sizeof(unsigned)))) return TT_E_CUDA;  // VerifyFinish::sync
+  if (bad(cudaMemset(c->d_ticket, 0, 4 * sizeof(unsigned)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_sublist_count, sizeof(int)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->d_sublist_count, 0, sizeof(int)))) return TT_E_CUDA;
   if (bad(cudaDeviceSynchronize())) return TT_E_CUDA;
@@ -588,7 +596,8 @@ void tt_ctx_destroy(tt_ctx* c) {
                   c->d_sublist, c->d_sublist_count, c->d_pos, c->d_pos_count, c->d_pos_fast,
                   c->d_pos_fast_count, c->d_status, c->d_record, c->d_params, c->d_packed, c->d_xs, c->d_xb,
                   c->d_tiles, c->d_ex, c->d_mix, c->tr.slots, c->tr.work, c->tr.grads, c->tr.dscore,
-                  c->tr.scores, c->tr.rank, c->tr.lat, c->tr.loss, c->tr.list, c->tr.bad, c->d_gather};
+                  c->tr.scores, c->tr.rank, c->tr.lat, c->tr.loss, c->tr.list, c->tr.bad, c->d_gather,
+                  c->d_ticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int r = 0; r < tt_ctx::kRing; ++r) {
@@ -908,6 +917,34 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
 int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg,
                       CandRef ref) {
   const bool by_id = ref.id != nullptr;
+  if (cfg->precision == TT_PREC_FP64 && ctx->h == 64 && n_stmt_of(S) <= 8 && n_block_of(S) <= 8 &&
+      verify64_finish_ok(cfg->k, cfg->b)) {
+    // the tuner geometry: features, PaCM and the finish in ONE kernel
+    // (k_verify64; its last CTA runs select_top + the record once the
+    // side-stream identities of the drafted set have landed)
+    if (!by_id) {
+      TT_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+      TT_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      if (launch_drafted_identity(S, ref.soa, ref.ld, ref.s0, ref.seeded ? cfg->first : ref.index_base,
+                                  ref.seeded != 0, ctx->d_idx, ctx->d_count, cfg->k, ctx->d_id, ctx->side,
+                                  ctx->d_ticket))
+        return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
+      TT_LAUNCHED(ctx);
+      TT_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+    }
+    const VerifyFinish vf{ctx->d_cost, ctx->d_idx,    ctx->d_id,      ctx->sel.state,
+                          cfg->b,      ctx->d_record, ctx->d_ticket,  by_id ? 0 : 1};
+    prof_begin(ctx, 1);
+    prof_begin(ctx, 5);
+    if (launch_verify64(S, D, ref, ctx->d_count, cfg->k, ctx->d_params, ctx->h, ctx->d_score, ctx->stream, &vf))
+      return fail(ctx, TT_E_VALIDATE, "fused verify: unsupported op shape");
+    prof_end(ctx, 5);
+    prof_end(ctx, 1);
+    TT_LAUNCHED(ctx);
+    // join (the identity kernel is long done: the finish waited for it)
+    if (!by_id) TT_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+    return TT_OK;
+  }
   if (!by_id) {  // fork: identities of the drafted set on the side stream
     TT_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
     TT_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));

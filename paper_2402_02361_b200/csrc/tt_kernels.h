@@ -125,7 +125,7 @@ int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, in
 // identities of the drafted set (side stream)
 int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, uint64_t s0, int64_t first,
                             bool seeded, const int64_t* idx, const int64_t* count_dev, int64_t k_max, uint64_t* out,
-                            cudaStream_t st);
+                            cudaStream_t st, unsigned* sync = nullptr);
 // How a kernel finds drafted candidate `pos`. Candidates are addressed by identity (population-independent) or by
 // (soa, ld, local index). `list`/`count` optionally restrict scoring to a
 // device-side sublist of positions (count read on device).
@@ -157,8 +157,28 @@ int launch_rank_loss(const double* scores, const double* lat, const int32_t* lis
                      double* loss, int accumulate, double* dscore, cudaStream_t st);
 // k_verify.cu: features + fp64 PaCM of the drafted set in one kernel (h = 64,
 // <= 8 statement rows and dataflow blocks, attention on); -1 = not applicable
+// vf (optional): the round's finish fused in — identities written to
+// id_write (if set), then the last CTA runs select_top + the record gather
+// (k_max <= 512, b <= 32; -1 otherwise).
+// sync: [0] the verify CTAs' ticket, [1] the identity kernel's block ticket,
+// [2] identity kernels completed, [3] fused finishes started (epochs; all zero
+// at context creation). With wait_ids the last CTA waits for the side-stream
+// identity kernel (k_drafted_identity launched with the same sync) before the
+// finish, computing the identities itself if that takes longer than 2 ms.
+inline bool verify64_finish_ok(int64_t k, int64_t b) { return k <= 512 && b <= 32 && b <= k; }
+struct VerifyFinish {
+  const double* drafts;
+  const int64_t* idx;
+  uint64_t* ids;
+  const SelState* sel;
+  int64_t b;
+  int64_t* record;
+  unsigned* sync;
+  int wait_ids;
+};
 int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
-                    const double* params, int h, double* score_out, cudaStream_t st);
+                    const double* params, int h, double* score_out, cudaStream_t st,
+                    const VerifyFinish* vf = nullptr);
 int launch_pacm64(const double* stmt, const double* block, int n_stmt, int n_block, const int64_t* count_dev,
                   int64_t k_max, const int32_t* sublist, const int* sublist_count, const double* params, int h,
                   int attention_identity, double* score_out, cudaStream_t st);

@@ -20,7 +20,7 @@ m = tt.PaCM(ctx, tt.init_params(64, derive_seed(42, TAG_INIT)), 64)
 ids = tt.random_init(ctx, sk, 512, 3, with_identity=True)[1]
 pop = tt.random_init(ctx, sk, 65536, 7)
 L = C.CDLL(_capi.LIB_PATH)
-span = (C.c_ulonglong * 4)()
+span = (C.c_ulonglong * 7)()
 for _ in range(3):
     torch.cuda.synchronize()
     (L.ttdbg_verify64_span if fused else L.ttdbg_pacm64_h64_span)(span, 1)
@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 (L.ttdbg_verify64_span if fused else L.ttdbg_pacm64_h64_span)(span, 0)
 sp = list(span)
 print(f"span (ns): first start -> first past pdl_wait {sp[1]-sp[0]}, -> last past wait {sp[2]-sp[0]}, "
-      f"-> last CTA done {sp[3]-sp[0]}")
+      f"-> last CTA done {sp[3]-sp[0]}" + (f", finish {sp[4]-sp[0]} (ids ready {sp[6]-sp[0]}) -> {sp[5]-sp[0]}" if fused else ""))
 clk = (C.c_longlong * 24)()
 (L.ttdbg_verify64_clocks if fused else L.ttdbg_pacm64_h64_clocks)(clk, 24)
 c = np.array(clk[:24], dtype=np.int64)
@@ -45,3 +45,9 @@ print(f"wait WA {d(4, 5)} | phase 2: S2 {d(5, 6)} Q {d(5, 16)} K {d(5, 17)} V {d
 print(f"phase 3: head1a wait Hw1 {d(8, 9)} chain {d(9, 10)} | logits+softmax {d(8, 11)} PV+pool {d(11, 12)} | sync {d(8, 13)}")
 print(f"phase 5: head1b {d(13, 14)} head2 {d(14, 15)}")
 print(f"total {d(0, 15)} cycles")
+
+if fused:
+    fc = (C.c_longlong * 8)()
+    L.ttdbg_verify64_finish_clocks(fc)
+    f = list(fc)
+    print(f"finish_block: loads+init {f[0]-f[4]} | warp sort {f[1]-f[0]} | cand {f[2]-f[1]} | rank {f[3]-f[2]} cycles")
