@@ -143,7 +143,7 @@ def run_ours(args, rank, world, local_rank):
 
     # rounds pipelined through the context's record ring: round r is enqueued, then
     # round r-1's selection is read back while r runs (at most two in flight)
-    inflight = {"n": 0}
+    inflight = {"n": 0, "retries": 0, "rounds": 0}
 
     def collect_lagged(c=None, keep=1):
         c = c or ctx
@@ -151,6 +151,8 @@ def run_ours(args, rank, world, local_rank):
             out_ = tt.round_collect(c, b)
             assert out_.selected == b and (out_.status & 0xff) == 0, out_
             inflight["n"] -= 1
+            inflight["retries"] += out_.retries
+            inflight["rounds"] += 1
 
     def step_value():
         for sk, soa in zip(sketches, pops):
@@ -375,6 +377,9 @@ def run_ours(args, rank, world, local_rank):
             "bert_1m": b1m,
             "parity": parity,
             "gpu_launches": launches,
+            "selector_retries": {"retries": inflight["retries"], "rounds": inflight["rounds"],
+                                 "note": "device-side threshold retries (re-thresholding the costs already in "
+                                         "HBM, never K1) + host re-runs, summed over every collected round"},
             "stage_ms_per_round": stage_ms,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -508,7 +513,7 @@ FLOP_PER_CAND = 320640  # PaCM forward at h = 64, S = 6, B = 8
 
 def _traffic():
     """dram read+write bytes per launch from the committed ncu capture (profiles/), or {}."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f)
@@ -529,9 +534,9 @@ def roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec):
         byts = args.n * sum(per) / len(per)
         ms = stage_ms["draft_cost"]
         ach = byts / (ms * 1e-3) / 1e9
-        out["draft_cost"] = {"bound": "hbm", "kernel": "k_fsel_cost (K1 SA draft cost + sample threshold)",
+        out["draft_cost"] = {"bound": "hbm", "kernel": "k_fsel (K1 SA draft cost inside the fused selector)",
                              "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                             "frac": ach / peaks["hbm_gbs"], "traffic": traffic.get("k_fsel_cost"),
+                             "frac": ach / peaks["hbm_gbs"], "traffic": traffic.get("k_fsel"),
                              "algorithmic_bytes": byts, "ms": ms, "peak_source": peaks_kind}
     if "pacm_kernel" in stage_ms:
         ms = stage_ms["pacm_kernel"]
@@ -546,9 +551,11 @@ def roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec):
             # CUDA-core fp64, no FMA contraction (bit-exact sums): 64 DMUL/DADD lanes/clk/SM measured
             # (tools/fp64_bench.cu) -> each multiply-add costs 2 lane-ops
             peak = 64 * 148 * sm_mhz * 1e6 / 1e12
-            out["pacm_kernel"] = {"bound": "fp64", "kernel": "k_pacm64 (fp64 CUDA cores, reference order)",
+            out["pacm_kernel"] = {"bound": "fp64",
+                                  "kernel": "k_verify64 (drafted-set features + fp64 PaCM on CUDA cores in the "
+                                            "reference's order + the round's finish; PaCM FLOPs counted)",
                                   "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                                  "traffic": traffic.get("k_pacm64"), "flop_per_candidate": FLOP_PER_CAND,
+                                  "traffic": traffic.get("k_verify64"), "flop_per_candidate": FLOP_PER_CAND,
                                   "ms": ms, "peak_source": "measured fp64 lane rate x 148 SMs x max SM clock"}
     if not out:
         return None

@@ -5,4 +5,5 @@ ncu -i /tmp/$TAG.ncu-rep --page raw --csv > gpurun_out/${TAG}_raw.csv 2>>gpurun_
 ncu -i /tmp/$TAG.ncu-rep --page details --csv > gpurun_out/${TAG}_details.csv 2>>gpurun_out/ncu_$TAG.log
 ncu -i /tmp/$TAG.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_source.csv 2>>gpurun_out/ncu_$TAG.log
 ncu -i /tmp/$TAG.ncu-rep --page source --csv --print-source cuda > gpurun_out/${TAG}_cuda.csv 2>>gpurun_out/ncu_$TAG.log
-cp /tmp/$TAG.ncu-rep gpurun_out/ 2>/dev/null
+[ -n "$KEEP_REP" ] && cp /tmp/$TAG.ncu-rep gpurun_out/ 2>/dev/null
+rm -f gpurun_out/${TAG}_cuda.csv  # large; the SASS page carries the stalls
