@@ -18,8 +18,9 @@
 // loads the weights once and walks tiles with a stride of the grid, the
 // next tile's features in flight while the current tile computes (double
 // buffer). Epilogues (tanh.approx, masked row sums, the per-candidate 8x8
-// softmax attention, mean pooling, the 2h -> h -> 1 head) run in fp32 on
-// the CUDA cores, one thread per TMEM lane (= row).
+// softmax attention, mean pooling) run in fp32 on the CUDA cores, one
+// thread per TMEM lane (= row); the head's 2h -> h layer is a third MMA over
+// the tile's 16 concat vectors (M = 128, the first 16 rows live).
 //
 // Scores carry bf16 operand rounding (|score error| vs fp64 typically
 // 1e-3..3e-2, bounded in tests at 6e-2); the round certifies its selection
@@ -44,8 +45,8 @@ constexpr uint32_t kOffWe = kOffW1 + 64 * 32 * 2;     // bf16 [64][32]
 constexpr uint32_t kOffW2 = kOffWe + 64 * 32 * 2;     // bf16 [64][64]
 constexpr uint32_t kOffWqkv = kOffW2 + 64 * 64 * 2;   // bf16 [192][64]
 constexpr uint32_t kOffBias = kOffWqkv + 192 * 64 * 2;  // f32 b1, be, b2, bq, bk, bv (6 x 64)
-constexpr uint32_t kOffHw1 = kOffBias + 6 * 64 * 4;   // f32 [128 m][64 j]
-constexpr uint32_t kOffHb1 = kOffHw1 + 128 * 64 * 4;  // f32 [64]
+constexpr uint32_t kOffHw1 = kOffBias + 6 * 64 * 4;   // bf16 [64 n][128 k]: the head's B operand
+constexpr uint32_t kOffHb1 = kOffHw1 + 64 * 128 * 2;  // f32 [64]
 constexpr uint32_t kOffHw2 = kOffHb1 + 64 * 4;        // f32 [64]
 constexpr uint32_t kOffHb2 = kOffHw2 + 64 * 4;        // f32 [4]
 constexpr uint32_t kPackBytes = kOffHb2 + 16;
@@ -87,7 +88,11 @@ __global__ void k_tc_pack(const double* __restrict__ p, uint8_t* __restrict__ ou
     ((float*)(out + kOffHb1))[e] = (float)hb1[e];
     ((float*)(out + kOffHw2))[e] = (float)hw2[e];
   }
-  for (int e = tid; e < 128 * 64; e += nth) ((float*)(out + kOffHw1))[e] = (float)hw1[e];
+  __nv_bfloat16* Hw1 = (__nv_bfloat16*)(out + kOffHw1);
+  for (int e = tid; e < 64 * 128; e += nth) {  // head layer 1: row = output j, K = concat index m
+    const int n = e / 128, k = e % 128;
+    Hw1[tc::kmaj_off(n, k, 64) / 2] = __float2bfloat16_rn((float)hw1[k * h + n]);
+  }
   if (tid == 0) ((float*)(out + kOffHb2))[0] = (float)hb2[0];
 }
 
@@ -269,47 +274,79 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
       __syncthreads();
     }
     TC_MARK(4);
-    // ---- epilogue 2b: Q half (registers), K and V halves (shared) with biases ----
-    float qv[32];
+    // ---- epilogue 2b: Q and K as split bf16 operands (hi + lo) for the logits MMA, V (f32, shared) ----
+    uint8_t* qh = a2;                 // Q hi | lo: bf16 [128 x 64] K-major each (A2 | A3, free after MMA 2)
+    uint8_t* ql = a3;
+    uint8_t* kh = (uint8_t*)kb;       // K hi | lo: bf16 [128 x 64] each, in the K staging region
+    uint8_t* kl = kh + kTcRows * 64 * 2;
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
       const int ch = 2 * hf + cc;
-      float v[16];
+      float v[16], hi[16], lo[16];
       tc::tmem_ld16(trow + 192 + 16 * ch, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) qv[16 * cc + q] = v[q] + bias[192 + 16 * ch + q];
+      for (int q = 0; q < 16; ++q) {
+        const float x = v[q] + bias[192 + 16 * ch + q];
+        hi[q] = __bfloat162float(__float2bfloat16_rn(x));
+        lo[q] = x - hi[q];
+      }
+      st_bf16x8(qh, tc::kmaj_off(row, 16 * ch, kTcRows), hi);
+      st_bf16x8(qh, tc::kmaj_off(row, 16 * ch + 8, kTcRows), hi + 8);
+      st_bf16x8(ql, tc::kmaj_off(row, 16 * ch, kTcRows), lo);
+      st_bf16x8(ql, tc::kmaj_off(row, 16 * ch + 8, kTcRows), lo + 8);
       tc::tmem_ld16(trow + 256 + 16 * ch, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) kb[row * kLd + 16 * ch + q] = v[q] + bias[256 + 16 * ch + q];
+      for (int q = 0; q < 16; ++q) {
+        const float x = v[q] + bias[256 + 16 * ch + q];
+        hi[q] = __bfloat162float(__float2bfloat16_rn(x));
+        lo[q] = x - hi[q];
+      }
+      st_bf16x8(kh, tc::kmaj_off(row, 16 * ch, kTcRows), hi);
+      st_bf16x8(kh, tc::kmaj_off(row, 16 * ch + 8, kTcRows), hi + 8);
+      st_bf16x8(kl, tc::kmaj_off(row, 16 * ch, kTcRows), lo);
+      st_bf16x8(kl, tc::kmaj_off(row, 16 * ch + 8, kTcRows), lo + 8);
       tc::tmem_ld16(trow + 320 + 16 * ch, v);
 #pragma unroll
       for (int q = 0; q < 16; ++q) vb[row * kLd + 16 * ch + q] = v[q] + bias[320 + 16 * ch + q];
     }
-    tc::tc_fence_before();  // TMEM reads of this tile done before the next tile's MMAs
+    tc::fence_async_smem();
+    tc::tc_fence_before();  // TMEM reads of D3 / D4 done before the logits MMA overwrites columns 64..191
     __syncthreads();
+    tc::tc_fence_after();
     TC_MARK(5);
+    // ---- logits of every row pair on the tensor cores: L[128 x 128] = Q K^T in three bf16 MMAs
+    // (hi.hi + hi.lo + lo.hi: ~16-bit operands); only each candidate's 8 x 8 diagonal block is read
+    if (t == 0) {
+      const uint32_t id128 = tc::idesc_bf16_f32(128, 128);
+      const uint32_t sqh = tc::smem_u32(qh), sql = tc::smem_u32(ql), skh = tc::smem_u32(kh), skl = tc::smem_u32(kl);
+      const uint32_t A[3] = {sqh, sqh, sql}, B[3] = {skh, skl, skh};
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int s = 0; s < 4; ++s)  // K = 64 = 4 x 16
+          tc::mma_bf16(tmem + 64, tc::desc_k_none(A[p] + 2 * s * LBO_A, LBO_A, 128),
+                       tc::desc_k_none(B[p] + 2 * s * LBO_A, LBO_A, 128), id128, (p | s) > 0);
+      tc::mma_commit(&bars[1]);
+    }
+    tc::mbar_wait(&bars[1], mma_phase & 1u);
+    ++mma_phase;
+    tc::tc_fence_after();
     // ---- attention within the candidate (rows 8c .. 8c+B-1) ----
     {
       const float scale = 0.125f;  // 1 / sqrt(64)
+      // this warp's 32 rows are candidates c0 .. c0 + 3: logit columns 8 c0 .. 8 c0 + 31
+      const int c0 = (row >> 5) * 4;
+      float wa[16], wb[16];
+      tc::tmem_ld16(trow + 64 + 8 * c0, wa);
+      tc::tmem_ld16(trow + 64 + 8 * c0 + 16, wb);
       float lg[8];
+      const int g = c - c0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) lg[u] = 0.f;
-      // partial logits over this half's 32 dimensions, 8 independent chains
-#pragma unroll 4
-      for (int q = 0; q < 32; ++q) {
-        const float x = qv[q];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) lg[u] = fmaf(x, kb[(8 * c + u) * kLd + 32 * hf + q], lg[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) part[t * 9 + u] = lg[u];
-      __syncthreads();
-      const int pt = t ^ 128;  // the partner thread: same row, other half
+      for (int u = 0; u < 8; ++u) lg[u] = g == 0 ? wa[u] : g == 1 ? wa[8 + u] : g == 2 ? wb[u] : wb[8 + u];
       float mx = -3.0e38f;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float d = hf == 0 ? lg[u] + part[pt * 9 + u] : part[pt * 9 + u] + lg[u];
-        lg[u] = u < n_block ? d * scale : -3.0e38f;
+        lg[u] = u < n_block ? lg[u] * scale : -3.0e38f;
         mx = fmaxf(mx, lg[u]);
       }
       float sum = 0.f;
@@ -338,35 +375,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pacm_tc(const uint8_t* __rest
         cat[c * 128 + 64 + j] = acc;
       }
     }
+    tc::tc_fence_before();
     __syncthreads();
     TC_MARK(6);
-    // ---- head: tanh([s|d] W1h + b1h) . w2h + b2h; thread (c, i, hf) owns columns 8i + 4hf .. +3 ----
+    // ---- head layer 1 on the tensor cores: D[16 x 64] = [s|d] (bf16, rows 16..127 zero) . W1h,
+    // M = 128 with only the first 16 rows live (the pipe has ample slack); A in the A2|A3
+    // region (dead after the second MMA), D in TMEM columns 0..63 (D1, consumed by epilogue 1)
     {
-      const float* hw1 = (const float*)(wp + kOffHw1);
-      const float* hb1 = (const float*)(wp + kOffHb1);
-      const float* hw2 = (const float*)(wp + kOffHw2);
-      const int j0 = 8 * i + 4 * hf;
-      float g[4];
+      uint8_t* ah = a2;  // bf16 [128 x 128] K-major, 32 KB = A2 | A3
+      for (int e = t; e < kTcRows * 128 / 8; e += kTcThreads) {  // 8 values per store
+        const int r = e / 16, k8 = (e % 16) * 8;
+        float v[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) g[q] = hb1[j0 + q];
-      const float* cr = cat + c * 128;
-#pragma unroll 8
-      for (int m = 0; m < 128; ++m) {
-        const float x = cr[m];
-        const float4 w0 = *(const float4*)(hw1 + m * 64 + j0);
-        g[0] = fmaf(x, w0.x, g[0]), g[1] = fmaf(x, w0.y, g[1]), g[2] = fmaf(x, w0.z, g[2]), g[3] = fmaf(x, w0.w, g[3]);
+        for (int q = 0; q < 8; ++q) v[q] = r < kTcCand ? cat[r * 128 + k8 + q] : 0.f;
+        st_bf16x8(ah, tc::kmaj_off(r, k8, kTcRows), v);
       }
-      float pp = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) pp = fmaf(tanh_fast(g[q]), hw2[j0 + q], pp);
-      pp += __shfl_xor_sync(0xffffffffu, pp, 1);
-      pp += __shfl_xor_sync(0xffffffffu, pp, 2);
-      pp += __shfl_xor_sync(0xffffffffu, pp, 4);
-      if (hf == 1 && i == 0) part[t * 9] = pp;
+      tc::fence_async_smem();
+      tc::tc_fence_before();
       __syncthreads();
-      const int64_t pos = tile * kTcCand + c;
-      if (hf == 0 && i == 0 && pos < count)
-        score_out[pos] = (double)((pp + part[(t ^ 128) * 9]) + *(const float*)(wp + kOffHb2));
+      tc::tc_fence_after();
+      if (t == 0) {
+        const uint32_t id64 = tc::idesc_bf16_f32(128, 64);
+#pragma unroll
+        for (int s = 0; s < 8; ++s)  // K = 128 = 8 x 16
+          tc::mma_bf16(tmem + 0, tc::desc_k_none(sa2 + 2 * s * LBO_A, LBO_A, 128),
+                       tc::desc_k_none(sw + kOffHw1 + 2 * s * 1024, 1024, 128), id64, s > 0);
+        tc::mma_commit(&bars[1]);
+      }
+      tc::mbar_wait(&bars[1], mma_phase & 1u);
+      ++mma_phase;
+      tc::tc_fence_after();
+      if (warp == 0) {  // lane r = candidate r of the tile: tanh(g + b1h) . w2h + b2h
+        const float* hb1 = (const float*)(wp + kOffHb1);
+        const float* hw2 = (const float*)(wp + kOffHw2);
+        float pp = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          float v[16];
+          tc::tmem_ld16(trow + 16 * ch, v);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pp = fmaf(tanh_fast(v[q] + hb1[16 * ch + q]), hw2[16 * ch + q], pp);
+        }
+        const int64_t pos = tile * kTcCand + t;
+        if (t < kTcCand && pos < count) score_out[pos] = (double)(pp + *(const float*)(wp + kOffHb2));
+      }
+      tc::tc_fence_before();
       TC_MARK(7);
     }
     __syncthreads();  // cat / kb / vb / part reused by the next tile
