@@ -260,7 +260,7 @@ def run_ours(args, rank, world, local_rank):
         assert out_e.selected == b
     etimes, elaunch, _ = timed(step_e2e)
     h2d = sum(x.numel() * 8 for x in ids_host) + params_host.numel() * 8
-    d2h = len(sketches) * 8 * (4 + 4 * b)
+    d2h = len(sketches) * 8 * (7 + 4 * b)  # each round record, written by its finishing kernel into mapped pinned memory
 
     # ---- e2e, seeded API (explore(seed) semantics: population drawn inside the call)
     def step_seeded():

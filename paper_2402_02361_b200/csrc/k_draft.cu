@@ -460,6 +460,9 @@ constexpr int kMaxAttempts = 8;
 // [9 + 2b] the latest arrival (first attempt)
 
 __device__ unsigned long long g_sel_ns[24];
+// timeline ring of the last 64 selector launches: [start, emit end]
+__device__ unsigned long long g_tl[64][2];
+__device__ unsigned g_tl_n[1];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -598,6 +601,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
   if (blockIdx.x == 0 && t == 0) {
     g_sel_ns[0] = gtimer();
     for (int q = 9; q < 16; q += 2) g_sel_ns[q] = 0;
+    const unsigned r = atomicAdd(&g_tl_n[0], 1u) & 63u;  // timeline ring (tools/probe_round_timeline.py)
+    g_tl[r][0] = g_sel_ns[0];
   }
   // n / 256 samples, clamped to [4096, 32768]: each sample stands for <= 512
   // candidates, so the rank-r threshold keeps ~(r + 1) * stride survivors
@@ -722,6 +727,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     }
     return;
   }
+  // the dependent verify kernel may launch now (its weight copies overlap the emit)
+  pdl_trigger();
   // ---- E: emit. Position of a unique survivor = its rank minus the
   // duplicates ranked below it (a bitmap over ranks, prefix popcounts).
   if (blockIdx.x > 0 && (int64_t)blockIdx.x * blockDim.x >= m) return;
@@ -759,6 +766,7 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     st->all = all ? 1 : 0;
     st->need = need;
     g_sel_ns[5] = gtimer(), g_sel_ns[6] = m, g_sel_ns[7] = attempt + 1;
+    g_tl[(g_tl_n[0] - 1u) & 63u][1] = g_sel_ns[5];
   }
 }
 
@@ -1176,11 +1184,11 @@ int launch_drafted_identity(const DevSketch& S, const int32_t* soa, int64_t ld, 
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, (tt::note_launch(), k_drafted_identity<NSP, NRED, false><<<g, 128, 0, st>>>(S, src, idx, count_dev, k_max, out, sync)));
 }
 
-__global__ void k_mark_invalid(const int* __restrict__ invalid, int64_t* __restrict__ out_idx) {
-  if (*invalid) out_idx[0] = kRankInvalid;
+__global__ void k_mark_invalid(int* __restrict__ invalid, int64_t* __restrict__ out_idx) {
+  if (*invalid) out_idx[0] = kRankInvalid, *invalid = 0;  // the flag is zero between calls
 }
 
-int launch_mark_invalid(const int* invalid, int64_t* out_idx, cudaStream_t st) {
+int launch_mark_invalid(int* invalid, int64_t* out_idx, cudaStream_t st) {
   k_mark_invalid<<<1, 1, 0, st>>>(invalid, out_idx);
   return cudaGetLastError() != cudaSuccess;
 }
@@ -1216,6 +1224,10 @@ int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, in
 
 }  // namespace tt
 
+extern "C" int ttdbg_select_timeline(unsigned long long* out, unsigned* n) {
+  int rc = (int)cudaMemcpyFromSymbol(out, tt::g_tl, sizeof(unsigned long long) * 128);
+  return rc ? rc : (int)cudaMemcpyFromSymbol(n, tt::g_tl_n, sizeof(unsigned));
+}
 extern "C" int ttdbg_select_clocks(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 24 ? n : 24));
 }

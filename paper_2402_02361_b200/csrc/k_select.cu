@@ -276,9 +276,10 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ scor
                                                  const int64_t* __restrict__ n_dev, int64_t b,
                                                  const int64_t* __restrict__ idx, const uint64_t* __restrict__ id,
                                                  const SelState* __restrict__ sel, const int* __restrict__ rescored,
-                                                 const double* __restrict__ fast, int64_t* __restrict__ out) {
+                                                 const double* __restrict__ fast, RecRing out,
+                                                 int* __restrict__ invalid) {
   __shared__ FinishSmem fs;
-  finish_block(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, fast, out, fs);
+  finish_block(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, fast, out, invalid, fs);
 }
 
 // Certification band for the tensor-core path, one CTA (n <= 1024,
@@ -349,11 +350,11 @@ int launch_cert_band(const double* fast, const double* drafts, int64_t n_max, co
 
 int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
                   const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
-                  const int* rescored, const double* fast, int64_t* out, cudaStream_t st) {
+                  const int* rescored, const double* fast, RecRing out, int* invalid, cudaStream_t st) {
   if (n_max > 1024 || b > 32 || b > n_max) return -1;
   const int nt = (int)((n_max + 31) / 32 * 32);
   tt::note_launch();
-  k_finish<<<1, nt, 0, st>>>(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, fast, out);
+  k_finish<<<1, nt, 0, st>>>(scores, drafts, excluded, n_max, n_dev, b, idx, id, sel, rescored, fast, out, invalid);
   return 0;
 }
 
@@ -368,8 +369,10 @@ __global__ void k_gather(const int64_t* __restrict__ pos, const int64_t* __restr
                          const int64_t* __restrict__ idx, const double* __restrict__ cost,
                          const uint64_t* __restrict__ id, const double* __restrict__ scores,
                          const double* __restrict__ fast, const uint8_t* __restrict__ excluded, int64_t n_max,
-                         int64_t b, int64_t* __restrict__ out) {
+                         int64_t b, RecRing ring, int* __restrict__ invalid) {
   __shared__ unsigned long long band_err;
+  __shared__ int s_slot;
+  int64_t* __restrict__ out = ring_slot(ring, &s_slot);
   const int64_t cnt = *pos_count;
   const int t = threadIdx.x;
   if (t == 0) band_err = 0ull;
@@ -389,6 +392,8 @@ __global__ void k_gather(const int64_t* __restrict__ pos, const int64_t* __restr
     out[3] = rescored ? *rescored : 0;
     out[4] = 0;
     out[5] = (int64_t)band_err;
+    if (invalid) out[6] = *(volatile int*)invalid, *invalid = 0;
+    else out[6] = 0;
   }
   int64_t* ix = out + kRecHead;
   double* sc = (double*)(ix + b);
@@ -411,9 +416,9 @@ __global__ void k_gather(const int64_t* __restrict__ pos, const int64_t* __restr
 int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
                   const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
                   const uint64_t* id, const double* scores, const double* fast, const uint8_t* excluded,
-                  int64_t n_max, int64_t b, int64_t* out, cudaStream_t st) {
+                  int64_t n_max, int64_t b, RecRing out, int* invalid, cudaStream_t st) {
   tt::note_launch(), k_gather<<<1, 128, 0, st>>>(pos, pos_count, drafted_count, sel, status_b, rescored, idx, cost, id,
-                                                 scores, fast, excluded, n_max, b, out);
+                                                 scores, fast, excluded, n_max, b, out, invalid);
   return 0;
 }
 

@@ -26,6 +26,9 @@ namespace tt {
 // last CTA to finish (ticket) runs select_top + the record gather
 // (tt_finish.cuh) over the whole drafted set in shared memory the PaCM
 // passes are done with.
+// timeline ring of the last 64 fused verify launches: [first CTA start, finish end]
+__device__ unsigned long long g_vtl[64][2];
+__device__ unsigned g_vtl_n[1];
 __device__ unsigned long long g_fin_ns[3];  // the last CTA's finish: start, end, identities ready (%globaltimer)
 
 struct FinishArgs {
@@ -34,9 +37,10 @@ struct FinishArgs {
   uint64_t* ids;            // identities (from the side stream, or known)
   const SelState* sel;      // selector status
   int64_t b;
-  int64_t* record;          // the round record (null: no finish)
+  RecRing record;           // the round records (record.base null: no finish)
   unsigned* sync;           // see VerifyFinish
   int wait_ids;
+  int* invalid;             // K1's population flag (copied into the record, reset)
 };
 
 template <int NSP, int NRED>
@@ -49,6 +53,7 @@ __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice 
   __shared__ bool last;
   const int S = 2 * SK.n_in + 2;
   const int B = SK.kind == TT_OP_ELEMENTWISE ? 1 : 3 * SK.n_in + 2;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && fin.record.base) g_vtl[g_vtl_n[0] & 63u][0] = gtimer64();
   pacm_h64_body(S, B, count_dev, k_max, params, score_out, [&](int64_t e0, int64_t count, double* MISC) {
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     for (int v = t; v < G * kMisc; v += T) MISC[v] = 0.0;  // padding rows, xb^T row 23, idle slots
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice 
       }
     }
   });
-  if (!fin.record) return;
+  if (!fin.record.base) return;
   // ---- finish: the last CTA done runs select_top + the record over all scores
   __threadfence();  // this CTA's scores / identities before its ticket
   __syncthreads();
@@ -123,8 +128,8 @@ __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice 
   }
   extern __shared__ __align__(128) double smf[];
   finish_block(score_out, fin.drafts, nullptr, k_max, count_dev, fin.b, fin.idx, fin.ids, fin.sel, nullptr, nullptr,
-               fin.record, *reinterpret_cast<FinishSmem*>(smf));
-  if (threadIdx.x == 0) g_fin_ns[1] = gtimer64();
+               fin.record, fin.invalid, *reinterpret_cast<FinishSmem*>(smf));
+  if (threadIdx.x == 0) g_fin_ns[1] = gtimer64(), g_vtl[atomicAdd(&g_vtl_n[0], 1u) & 63u][1] = g_fin_ns[1];
 }
 
 int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
@@ -133,7 +138,8 @@ int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const i
   if (h != f64::H || ns > 8 || nb > 8 || k_max <= 0) return -1;
   if (vf && !verify64_finish_ok(k_max, vf->b)) return -1;  // finish_block: one key per thread
   FinishArgs fin{};
-  if (vf) fin = FinishArgs{vf->drafts, vf->idx, vf->ids, vf->sel, vf->b, vf->record, vf->sync, vf->wait_ids};
+  if (vf)
+    fin = FinishArgs{vf->drafts, vf->idx, vf->ids, vf->sel, vf->b, vf->record, vf->sync, vf->wait_ids, vf->invalid};
   const int64_t ctas = (k_max + f64::G - 1) / f64::G;
   const dim3 grid((unsigned)(ctas < 148 ? ctas : 148));
   return TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
@@ -164,4 +170,9 @@ extern "C" int ttdbg_verify64_span(unsigned long long* out, int reset) {
 
 extern "C" int ttdbg_verify64_finish_clocks(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, tt::g_fin_clk, sizeof(long long) * 8);
+}
+
+extern "C" int ttdbg_verify64_timeline(unsigned long long* out, unsigned* n) {
+  int rc = (int)cudaMemcpyFromSymbol(out, tt::g_vtl, sizeof(unsigned long long) * 128);
+  return rc ? rc : (int)cudaMemcpyFromSymbol(n, tt::g_vtl_n, sizeof(unsigned));
 }

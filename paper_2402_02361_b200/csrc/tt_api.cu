@@ -109,8 +109,13 @@ struct tt_ctx {
   };
   std::deque<Pending> pend;
   int ring_next = 0;
-  int64_t* h_rec[kRing] = {};
-  int* h_inv[kRing] = {};
+  // the record ring: one mapped pinned buffer of kRing slots; the finishing
+  // kernel of a round writes its record into slot (d_seq++ % kRing), the host
+  // hands out the same sequence (ring_next), so no device->host copy is queued
+  int64_t* h_ring = nullptr;
+  int64_t* d_ring = nullptr;  // its device address
+  int64_t* h_rec[kRing] = {};  // h_ring + r * stride
+  unsigned* d_seq = nullptr;
   cudaEvent_t ev_rec[kRing] = {};
   // CUDA graphs of whole rounds, keyed by every argument that shapes the
   // enqueued work (sketch, device, config, population pointer, seed, need);
@@ -409,15 +414,15 @@ int ensure_b(tt_ctx* ctx, int64_t b) {
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos, sizeof(int64_t) * b));
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_pos_fast, sizeof(int64_t) * b));
   TT_CUDA(ctx, cudaMalloc((void**)&ctx->d_record, sizeof(int64_t) * record_words(b)));
+  int64_t* nh = nullptr;
+  TT_CUDA(ctx, cudaHostAlloc((void**)&nh, sizeof(int64_t) * record_words(b) * tt_ctx::kRing, cudaHostAllocMapped));
   for (int r = 0; r < tt_ctx::kRing; ++r) {
-    int64_t* nh = nullptr;
-    TT_CUDA(ctx, cudaMallocHost((void**)&nh, sizeof(int64_t) * record_words(b)));
-    if (ctx->h_rec[r]) {
-      std::memcpy(nh, ctx->h_rec[r], sizeof(int64_t) * record_words(ctx->b_cap));
-      cudaFreeHost(ctx->h_rec[r]);
-    }
-    ctx->h_rec[r] = nh;
+    if (ctx->h_ring) std::memcpy(nh + r * record_words(b), ctx->h_rec[r], sizeof(int64_t) * record_words(ctx->b_cap));
+    ctx->h_rec[r] = nh + r * record_words(b);
   }
+  if (ctx->h_ring) cudaFreeHost(ctx->h_ring);
+  ctx->h_ring = nh;
+  TT_CUDA(ctx, cudaHostGetDevicePointer((void**)&ctx->d_ring, nh, 0));
   ctx->b_cap = b;
   return TT_OK;
 }
@@ -548,8 +553,6 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming))) return TT_E_CUDA;
   for (int r = 0; r < tt_ctx::kRing; ++r) {
     if (bad(cudaEventCreateWithFlags(&c->ev_rec[r], cudaEventDisableTiming))) return TT_E_CUDA;
-    if (bad(cudaMallocHost((void**)&c->h_inv[r], sizeof(int)))) return TT_E_CUDA;
-    *c->h_inv[r] = 0;
   }
   c->stream = c->own;
   if (const char* g = getenv("TT_GRAPHS")) c->graphs = g[0] != '0';
@@ -574,8 +577,9 @@ int tt_ctx_create(int device, tt_ctx** out) {
   if (bad(cudaMalloc((void**)&c->d_pos_count, sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_pos_fast_count, sizeof(int64_t)))) return TT_E_CUDA;
   if (bad(cudaMalloc((void**)&c->d_status, 2 * sizeof(int)))) return TT_E_CUDA;
-  if (bad(cudaMalloc((void**)&c->d_ticket, 4 * sizeof(unsigned)))) return TT_E_CUDA;  // VerifyFinish::sync
-  if (bad(cudaMemset(c->d_ticket, 0, 4 * sizeof(unsigned)))) return TT_E_CUDA;
+  if (bad(cudaMalloc((void**)&c->d_ticket, 8 * sizeof(unsigned)))) return TT_E_CUDA;  // VerifyFinish::sync | ring seq
+  if (bad(cudaMemset(c->d_ticket, 0, 8 * sizeof(unsigned)))) return TT_E_CUDA;
+  c->d_seq = c->d_ticket + 4;
   if (bad(cudaMalloc((void**)&c->d_sublist_count, sizeof(int)))) return TT_E_CUDA;
   if (bad(cudaMemset(c->d_sublist_count, 0, sizeof(int)))) return TT_E_CUDA;
   if (bad(cudaDeviceSynchronize())) return TT_E_CUDA;
@@ -601,11 +605,10 @@ void tt_ctx_destroy(tt_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int r = 0; r < tt_ctx::kRing; ++r) {
-    if (c->h_rec[r]) cudaFreeHost(c->h_rec[r]);
-    if (c->h_inv[r]) cudaFreeHost(c->h_inv[r]);
     if (c->ev_rec[r]) cudaEventDestroy(c->ev_rec[r]);
   }
   if (c->h_ex) cudaFreeHost(c->h_ex);
+  if (c->h_ring) cudaFreeHost(c->h_ring);
   if (c->h_loss) cudaFreeHost(c->h_loss);
   for (cudaEvent_t e : c->ex_ev) cudaEventDestroy(e);
   graphs_clear(c);
@@ -718,7 +721,10 @@ int tt_draft_cost(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   int invalid = 0;
   TT_CUDA(ctx, cudaMemcpyAsync(&invalid, ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   if ((rc = sync_check(ctx))) return rc;
-  if (invalid) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule (factor products / unroll)");
+  if (invalid) {  // the flag is zero between calls
+    TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+    return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule (factor products / unroll)");
+  }
   return TT_OK;
 }
 
@@ -915,7 +921,9 @@ int score_drafted(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, CandRef r
 // identities). Identities of the b selections come from d_id for merged
 // rounds, otherwise they are computed for those b only.
 int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg,
-                      CandRef ref) {
+                      CandRef ref, int slot) {
+  (void)slot;  // the finishing kernel takes the ring's next slot = slot (same sequence)
+  const RecRing record{ctx->d_ring, record_words(ctx->b_cap), ctx->d_seq};
   const bool by_id = ref.id != nullptr;
   if (cfg->precision == TT_PREC_FP64 && ctx->h == 64 && n_stmt_of(S) <= 8 && n_block_of(S) <= 8 &&
       verify64_finish_ok(cfg->k, cfg->b)) {
@@ -932,8 +940,8 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
       TT_LAUNCHED(ctx);
       TT_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
     }
-    const VerifyFinish vf{ctx->d_cost, ctx->d_idx,    ctx->d_id,      ctx->sel.state,
-                          cfg->b,      ctx->d_record, ctx->d_ticket,  by_id ? 0 : 1};
+    const VerifyFinish vf{ctx->d_cost, ctx->d_idx, ctx->d_id,     ctx->sel.state,   cfg->b,
+                          record,      ctx->d_ticket, by_id ? 0 : 1, ctx->sel.invalid};
     prof_begin(ctx, 1);
     prof_begin(ctx, 5);
     if (launch_verify64(S, D, ref, ctx->d_count, cfg->k, ctx->d_params, ctx->h, ctx->d_score, ctx->stream, &vf))
@@ -963,14 +971,14 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
   const uint8_t* excl = certified ? ctx->d_excluded : nullptr;
   const double* fast = certified ? ctx->d_score_fast : nullptr;
   if (launch_finish(ctx->d_score, ctx->d_cost, excl, cfg->k, ctx->d_count, cfg->b, ctx->d_idx, ctx->d_id,
-                    ctx->sel.state, ctx->d_sublist_count, fast, ctx->d_record, ctx->stream)) {
+                    ctx->sel.state, ctx->d_sublist_count, fast, record, ctx->sel.invalid, ctx->stream)) {
     // large draft sets / batches: tiled select_top, then the record gather
     if (launch_select_top(ctx->d_score, ctx->d_cost, excl, cfg->k, ctx->d_count, cfg->b, ctx->d_pos,
                           ctx->d_pos_count, ctx->d_status, ctx->stream))
       return fail(ctx, TT_E_CONFIG, "select_top: draft_size too large for the batch");
     launch_gather(ctx->d_pos, ctx->d_pos_count, ctx->d_count, ctx->sel.state, nullptr, ctx->d_sublist_count,
-                  ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, fast, excl, cfg->k, cfg->b, ctx->d_record,
-                  ctx->stream);
+                  ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_score, fast, excl, cfg->k, cfg->b, record,
+                  ctx->sel.invalid, ctx->stream);
   }
   prof_end(ctx, 3);
   TT_LAUNCHED(ctx);
@@ -979,10 +987,9 @@ int verify_and_select(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const
 
 // The round's record and validity flag into its ring slot, then its event.
 // Outside any graph (the slot changes every round; the graphs do not).
-int record_copy(tt_ctx* ctx, int slot, int64_t b) {
-  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_rec[slot], ctx->d_record, sizeof(int64_t) * record_words(b), cudaMemcpyDeviceToHost,
-                               ctx->stream));
-  TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_inv[slot], ctx->sel.invalid, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+int record_copy(tt_ctx* ctx, int slot, int64_t) {
+  // the record is already in its mapped slot (written by the finishing
+  // kernel): the slot's event marks when it is complete
   TT_CUDA(ctx, cudaEventRecord(ctx->ev_rec[slot], ctx->stream));
   return TT_OK;
 }
@@ -1003,9 +1010,9 @@ int check_round_cfg(tt_ctx* ctx, const tt_round_config* cfg) {
 // enqueued on ctx->stream. Scratch must already be sized (no allocation
 // here), so the sequence can be captured into a CUDA graph.
 int round_body(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_round_config* cfg, const int32_t* soa,
-               int64_t ld, uint64_t seed, int64_t need, bool hash) {
+               int64_t ld, uint64_t seed, int64_t need, bool hash, int slot) {
   const bool seeded = soa == nullptr;
-  if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
+  // sel.invalid is zero between calls (every reader resets it): no memset node
   prof_begin(ctx, 0);
   prof_k1_arm(ctx);
   if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k, need, cfg->toggles,
@@ -1018,14 +1025,14 @@ int round_body(tt_ctx* ctx, const DevSketch& S, const DevDevice& D, const tt_rou
   // index: a SoA gather, or a counter-based regeneration
   CandRef ref = seeded ? CandRef{nullptr, 0, ctx->d_idx, 0, nullptr, seed_state(seed), 1, 0}
                        : CandRef{soa, ld, ctx->d_idx, cfg->first, nullptr, 0, 0, 0};
-  return verify_and_select(ctx, S, D, cfg, ref);
+  return verify_and_select(ctx, S, D, cfg, ref, slot);
 }
 
 // retry_slot >= 0: a synchronous re-run of a collected round into its own
 // (already popped) ring slot; nothing is pushed
 int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
                   const int32_t* soa, int64_t ld, uint64_t seed, int64_t need, bool hash = false,
-                  int retry_slot = -1) {
+                  int* retry_slot = nullptr) {
   DevSketch S;
   DevDevice D;
   int rc = compile_sketch(ctx, sk, S);
@@ -1038,10 +1045,12 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   if ((rc = ensure_feat(ctx, cfg->k))) return rc;
   if (cfg->n > kSmallSelectMax && (rc = ensure_cost(ctx, cfg->n))) return rc;
   if (cfg->precision == TT_PREC_BF16 && (rc = ensure_packed(ctx))) return rc;
-  int slot = retry_slot;
-  if (slot < 0 && (rc = ring_claim(ctx, &slot))) return rc;
+  // the ring's next slot (a synchronous re-run of a collected round takes it
+  // too: the device hands out slots in launch order)
+  int slot = -1;
+  if ((rc = ring_claim(ctx, &slot))) return rc;
   if (!ctx->graphs || ctx->prof) {
-    if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash))) return rc;
+    if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash, slot))) return rc;
   } else {
     // graph cache: the key is every byte that shapes the enqueued work
     std::string key;
@@ -1054,13 +1063,13 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
     if (ctx->graph_seen.size() > 4096) ctx->graph_seen.clear();  // bounded memory over long tuning runs
     const bool repeat = it != ctx->graph_cache.end() || !ctx->graph_seen.insert(key).second;
     if (!repeat) {
-      if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash))) return rc;
+      if ((rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash, slot))) return rc;
     } else if (it == ctx->graph_cache.end()) {
       cudaStream_t launch = ctx->stream;
       const uint64_t l0 = tt_kernel_launches();
       TT_CUDA(ctx, cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeRelaxed));
       ctx->stream = ctx->own;
-      rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash);
+      rc = round_body(ctx, S, D, cfg, soa, ld, seed, need, hash, slot);
       ctx->stream = launch;
       cudaGraph_t g = nullptr;
       const cudaError_t ec = cudaStreamEndCapture(ctx->own, &g);
@@ -1081,14 +1090,16 @@ int round_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, c
   }
   // outside any capture: the record into this round's ring slot, then its event
   if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
-  if (retry_slot < 0)
+  if (!retry_slot)
     ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, need, ld, hash, false, *cfg, *sk, *dev, soa, seed,
                                    nullptr, nullptr, nullptr, 0});
+  else
+    *retry_slot = slot, ctx->ring_next = (slot + 1) % tt_ctx::kRing;
   return TT_OK;
 }
 
 int merged_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
-                   const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int retry_slot = -1);
+                   const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int* retry_slot = nullptr);
 
 // The oldest round in flight into the caller's buffers (capacity entries
 // each). A round whose selector ran out of margin (NEED_MORE: duplicates;
@@ -1104,9 +1115,10 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
     return fail(ctx, TT_E_CONFIG, "round_collect: the oldest round selects " + std::to_string(p.b) +
                                       " candidates, the buffers hold " + std::to_string(capacity));
   ctx->pend.pop_front();
+  int slot = p.slot;  // a re-run lands in the ring's next slot
   // wait for this round only (the stream may already hold later rounds)
   auto wait_slot = [&]() -> int {
-    const cudaError_t e1 = cudaEventSynchronize(ctx->ev_rec[p.slot]);
+    const cudaError_t e1 = cudaEventSynchronize(ctx->ev_rec[slot]);
     const cudaError_t e2 = cudaGetLastError();
     if (e1 != cudaSuccess || e2 != cudaSuccess)
       return fail(ctx, TT_E_CUDA, std::string("round: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
@@ -1115,8 +1127,7 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
   int rc = wait_slot();
   if (rc) return rc;
   const int64_t b = p.b;
-  const int64_t* rec = ctx->h_rec[p.slot];
-  const int* inv = ctx->h_inv[p.slot];
+  const int64_t* rec = ctx->h_rec[slot];  // mapped: complete once the slot's event fired
   int retries = 0, extra = 0;
   const int retry_mask = TT_SEL_NEED_MORE | TT_SEL_OVERFLOW;
   if (((int)rec[2] & retry_mask) && allow_retry && !p.merged) {
@@ -1132,8 +1143,9 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
         need *= 2;
       }
       tt_round_config cfg = p.cfg;
-      if ((rc = round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, need, hash, p.slot))) return rc;
+      if ((rc = round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, need, hash, &slot))) return rc;
       if ((rc = wait_slot())) return rc;
+      rec = ctx->h_rec[slot];
       ++retries;
       ok = !((int)rec[2] & retry_mask);
     }
@@ -1145,7 +1157,7 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
   if ((int)rec[2] & TT_SEL_OVERFLOW)
     return fail(ctx, TT_E_STATE, p.merged ? "draft selector overflow on a rank: re-run the draft half with tt_round_local"
                                           : "draft selector overflow: more than 4096 unique schedules tie at the threshold");
-  if (p.soa && *inv) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
+  if (p.soa && rec[6]) return fail(ctx, TT_E_VALIDATE, "schedule does not satisfy validate_schedule");
   double band_err;
   std::memcpy(&band_err, rec + 5, sizeof(double));
   if (p.cfg.precision != TT_PREC_FP64 && band_err > p.cfg.band && allow_retry) {
@@ -1153,10 +1165,11 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
     // the exclusions are not certified, so the round is re-run in fp64
     tt_round_config cfg = p.cfg;
     cfg.precision = TT_PREC_FP64;
-    rc = p.merged ? merged_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.m_cost, p.m_gidx, p.m_id, p.m, p.slot)
-                  : round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, p.need, p.hash, p.slot);
+    rc = p.merged ? merged_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.m_cost, p.m_gidx, p.m_id, p.m, &slot)
+                  : round_enqueue(ctx, &p.sketch, &p.dev, &cfg, p.soa, p.ld, p.seed, p.need, p.hash, &slot);
     if (rc) return rc;
     if ((rc = wait_slot())) return rc;
+    rec = ctx->h_rec[slot];
     extra |= TT_ROUND_BAND_RERUN;
     if ((int)rec[2] & retry_mask) return fail(ctx, TT_E_STATE, "draft selector: fp64 re-run did not converge");
   }
@@ -1184,7 +1197,7 @@ int round_collect(tt_ctx* ctx, int64_t capacity, int64_t* sel_index, double* sel
 }
 
 int merged_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, const tt_round_config* cfg,
-                   const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int retry_slot) {
+                   const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int* retry_slot) {
   DevSketch S;
   DevDevice D;
   int rc = compile_sketch(ctx, sk, S);
@@ -1198,8 +1211,8 @@ int merged_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, 
   if ((rc = ensure_k(ctx, cfg->k))) return rc;
   if ((rc = ensure_b(ctx, cfg->b))) return rc;
   if (cfg->precision == TT_PREC_BF16 && (rc = ensure_packed(ctx))) return rc;
-  int slot = retry_slot;
-  if (slot < 0 && (rc = ring_claim(ctx, &slot))) return rc;
+  int slot = -1;
+  if ((rc = ring_claim(ctx, &slot))) return rc;
   prof_begin(ctx, 4);
   if (launch_merge(cost, gidx, id, m, cfg->k, ctx->d_idx, ctx->d_cost, ctx->d_id, ctx->d_count, ctx->sel.state,
                    ctx->sel.mscratch, ctx->stream))
@@ -1207,13 +1220,15 @@ int merged_enqueue(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, 
   prof_end(ctx, 4);
   TT_LAUNCHED(ctx);
   CandRef ref{nullptr, 0, nullptr, 0, ctx->d_id};
-  if ((rc = verify_and_select(ctx, S, D, cfg, ref))) return rc;
+  if ((rc = verify_and_select(ctx, S, D, cfg, ref, slot))) return rc;
   if ((rc = record_copy(ctx, slot, cfg->b))) return rc;
   // no selector retry: the local lists are the ranks' own (a rank that could
   // not certify its list marks it, and the merge reports OVERFLOW)
-  if (retry_slot < 0)
+  if (!retry_slot)
     ring_push(ctx, tt_ctx::Pending{slot, cfg->b, cfg->k, -1, 0, false, true, *cfg, *sk, *dev, nullptr, 0, cost, gidx,
                                    id, m});
+  else
+    *retry_slot = slot, ctx->ring_next = (slot + 1) % tt_ctx::kRing;
   return TT_OK;
 }
 
@@ -1584,8 +1599,7 @@ int tt_round_local_async(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec*
     return select_sync(ctx, S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k, cfg->toggles,
                        cfg->first, gidx_out, cost_out, id_out, &cnt);
   }
-  if (!seeded) TT_CUDA(ctx, cudaMemsetAsync(ctx->sel.invalid, 0, sizeof(int), ctx->stream));
-  prof_begin(ctx, 0);
+  prof_begin(ctx, 0);  // sel.invalid is zero between calls; k_mark_invalid resets it
   if (launch_select(S, D, soa, ld, seed_state(seed), cfg->first, seeded, cfg->n, cfg->k,
                     cfg->k + cfg->k / 8 + 16, cfg->toggles, cfg->first, ctx->sel, gidx_out, cost_out, id_out,
                     ctx->d_count, ctx->stream))

@@ -46,7 +46,15 @@ __device__ __forceinline__ void warp_sort32(Key3& k) {
 // passed in (FinishSmem), so a kernel can run it in memory it is done with.
 static __device__ long long g_fin_clk[8];  // finish_block phase marks (thread 0; probe)
 
+// this round's slot of the record ring (one thread takes it, all get it)
+__device__ __forceinline__ int64_t* ring_slot(const RecRing& r, int* s_slot) {
+  if (threadIdx.x == 0) *s_slot = (int)(atomicAdd(r.seq, 1u) % (unsigned)kRingSlots);
+  __syncthreads();
+  return r.base + (int64_t)(*s_slot) * r.stride;
+}
+
 struct FinishSmem {
+  int slot;
   Key3 lists[32][33];
   int16_t rank_of[1024];  // output position of each selected candidate, -1 otherwise
   int cnt[1024];          // candidates' ranks among the warps' b best
@@ -59,12 +67,13 @@ __device__ __forceinline__ void finish_block(const double* __restrict__ scores, 
                                              const int64_t* __restrict__ n_dev, int64_t b,
                                              const int64_t* __restrict__ idx, const uint64_t* __restrict__ id,
                                              const SelState* __restrict__ sel, const int* __restrict__ rescored,
-                                             const double* __restrict__ fast, int64_t* __restrict__ out,
-                                             FinishSmem& fs) {
+                                             const double* __restrict__ fast, RecRing ring,
+                                             int* __restrict__ invalid, FinishSmem& fs) {
   auto& lists = fs.lists;
   auto& avail = fs.avail;
   auto& band_err = fs.band_err;
   auto& rank_of = fs.rank_of;
+  int64_t* __restrict__ out = ring_slot(ring, &fs.slot);
   if (threadIdx.x == 0) g_fin_clk[4] = clock64();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
   // every global read issued up front, independent of each other (one
@@ -145,6 +154,8 @@ __device__ __forceinline__ void finish_block(const double* __restrict__ scores, 
     out[3] = rs;
     out[4] = 0;
     out[5] = (int64_t)band_err;
+    if (invalid) out[6] = *(volatile int*)invalid, *invalid = 0;  // K1 set it earlier in this round
+    else out[6] = 0;
   }
 }
 

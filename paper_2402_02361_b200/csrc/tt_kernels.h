@@ -36,11 +36,23 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 constexpr int64_t kSmallSelectMax = 1024;
 
-// Round record (the one device->host copy of a round), 8-byte words:
+// Round record, 8-byte words, written by the round's finishing kernel straight
+// into the context's mapped pinned ring slot (no device->host copy):
 // [0] selected, [1] drafted, [2] status, [3] rescored, [4] selector retries
-// (host), [5] band error bits (max |fast - fp64| over the rescored set), then
-// b population indices, b scores, b draft costs, b identities.
-constexpr int64_t kRecHead = 6;
+// (host), [5] band error bits (max |fast - fp64| over the rescored set), [6]
+// the explicit population failed validate_schedule (K1's flag, which the
+// finisher resets for the next round), then b population indices, b scores,
+// b draft costs, b identities.
+constexpr int64_t kRecHead = 7;
+// The ring of round records in mapped pinned memory: the finishing kernel of
+// a round takes slot (*seq)++ % kRingSlots, so rounds land in enqueue order;
+// the host hands out the same sequence (tt_ctx ring_next).
+constexpr int kRingSlots = 16;
+struct RecRing {
+  int64_t* base;    // kRingSlots slots of `stride` words (device address of the mapped buffer)
+  int64_t stride;
+  unsigned* seq;    // device counter of finished rounds
+};
 inline int64_t record_words(int64_t b) { return kRecHead + 4 * b; }
 
 enum : int { TT_SEL_OVERFLOW = 1, TT_SEL_NEED_MORE = 2, TT_SEL_INVALID = 4 };
@@ -118,7 +130,7 @@ constexpr int64_t kMergeSortMax = 4096;  // one-CTA sort path (any order)
 constexpr int64_t kRankFailed = -2;      // index word of a rank whose selector failed
 constexpr int64_t kRankInvalid = -3;     // index word of a rank whose population failed validate_schedule
 // sharded draft half, explicit population: slot 0's index <- kRankInvalid when K1 flagged a schedule
-int launch_mark_invalid(const int* invalid, int64_t* out_idx, cudaStream_t st);
+int launch_mark_invalid(int* invalid, int64_t* out_idx, cudaStream_t st);
 int launch_merge(const double* cost, const int64_t* gidx, const uint64_t* id, int64_t m, int64_t k, int64_t* out_idx,
                  double* out_cost, uint64_t* out_id, int64_t* out_count, SelState* state, int32_t* scratch,
                  cudaStream_t st);
@@ -172,9 +184,10 @@ struct VerifyFinish {
   uint64_t* ids;
   const SelState* sel;
   int64_t b;
-  int64_t* record;
+  RecRing record;
   unsigned* sync;
   int wait_ids;
+  int* invalid;  // K1's population flag: copied into the record, then reset
 };
 int launch_verify64(const DevSketch& S, const DevDevice& D, CandRef ref, const int64_t* count_dev, int64_t k_max,
                     const double* params, int h, double* score_out, cudaStream_t st,
@@ -226,13 +239,13 @@ int launch_momentum(double* phi, const double* target, int64_t n, double m, cuda
 // the candidates not excluded (the fp64-rescored set)
 int launch_finish(const double* scores, const double* drafts, const uint8_t* excluded, int64_t n_max,
                   const int64_t* n_dev, int64_t b, const int64_t* idx, const uint64_t* id, const SelState* sel,
-                  const int* rescored, const double* fast, int64_t* out, cudaStream_t st);
+                  const int* rescored, const double* fast, RecRing out, int* invalid, cudaStream_t st);
 // fast top-b + certification band in one CTA (n <= 1024, b <= 32); -1 otherwise
 int launch_cert_band(const double* fast, const double* drafts, int64_t n_max, const int64_t* n_dev, int64_t b,
                      double band, int32_t* sublist, int* sublist_count, uint8_t* excluded, cudaStream_t st);
 int launch_gather(const int64_t* pos, const int64_t* pos_count, const int64_t* drafted_count, const SelState* sel,
                   const int* status_b, const int* rescored, const int64_t* idx, const double* cost,
                   const uint64_t* id, const double* scores, const double* fast, const uint8_t* excluded,
-                  int64_t n_max, int64_t b, int64_t* out, cudaStream_t st);
+                  int64_t n_max, int64_t b, RecRing out, int* invalid, cudaStream_t st);
 
 }  // namespace tt

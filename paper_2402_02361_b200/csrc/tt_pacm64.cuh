@@ -263,8 +263,6 @@ __device__ __forceinline__ void pacm_h64_body(int S, int B, const int64_t* __res
                                               Stage stage) {
   using namespace f64;
   if (threadIdx.x == 0) atomicMin(&g_h64_ns[0], gtimer64());
-  pdl_wait();  // inputs come from the preceding kernel
-  if (threadIdx.x == 0) atomicMin(&g_h64_ns[1], gtimer64()), atomicMax(&g_h64_ns[2], gtimer64());
   extern __shared__ __align__(128) double smf[];
   __shared__ __align__(8) uint64_t mb[3];
   __shared__ double etab[32];
@@ -275,9 +273,6 @@ __device__ __forceinline__ void pacm_h64_body(int S, int B, const int64_t* __res
   double* MISC = QKV + G * kQKV;     // [G][kMisc]
   const int t = threadIdx.x;
   const Params64 P = split_params(params, H);
-  int64_t count = k_max;
-  if (count_dev) count = *count_dev < k_max ? *count_dev : k_max;
-  if ((int64_t)blockIdx.x * G >= count) return;
   auto load_w1e = [&]() {  // QKV region <- W1 | We
     tc::fence_async_smem();
     tc::mbar_expect_tx(&mb[0], (24 + 23) * H * 8);
@@ -292,12 +287,23 @@ __device__ __forceinline__ void pacm_h64_body(int S, int B, const int64_t* __res
     tc::bulk_g2s(WA + 2 * H * H, P.wk, H * H * 8, &mb[1]);
     tc::bulk_g2s(WA + 3 * H * H, P.wv, H * H * 8, &mb[1]);
   };
+  // the weights do not depend on the preceding kernel (they were loaded before
+  // it ran): their bulk copies start before the grid-dependency wait, so
+  // under programmatic dependent launch they overlap the selector's tail
   if (t == 0) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) tc::mbar_init(&mb[i], 1);
     tc::fence_mbar_init();
     load_w1e();
     load_wa();
+  }
+  pdl_wait();  // the drafted set and its count come from the preceding kernel
+  if (threadIdx.x == 0) atomicMin(&g_h64_ns[1], gtimer64()), atomicMax(&g_h64_ns[2], gtimer64());
+  int64_t count = k_max;
+  if (count_dev) count = *count_dev < k_max ? *count_dev : k_max;
+  if ((int64_t)blockIdx.x * G >= count) {  // no candidates: the weight copies must land before exit
+    if (t == 0) tc::mbar_wait(&mb[0], 0), tc::mbar_wait(&mb[1], 0);
+    return;
   }
   const double scale = __ddiv_rn(1.0, sqrt((double)H));  // ranker.cpp:179
   const double inv_n = __ddiv_rn(1.0, (double)B);        // ranker.cpp:198
