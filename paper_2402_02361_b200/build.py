@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 # bit are built without FMA contraction
 EXACT = {"k_draft.cu", "k_verify.cu", "k_rank.cu", "k_explore.cu", "k_feat.cu", "k_oracle.cu", "k_pacm64.cu", "k_select.cu", "k_train.cu", "tt_api.cu"}
 SOURCES = ["k_draft.cu", "k_verify.cu", "k_rank.cu", "k_explore.cu", "k_feat.cu", "k_oracle.cu", "k_pacm64.cu", "k_select.cu", "k_pacm_tc.cu", "k_train.cu", "tt_api.cu"]
-HEADERS = ["tt_device.cuh", "tt_pacm64.cuh", "tt_features.cuh", "tt_block.cuh", "tt_kernels.h", "tt_tc.cuh"]
+HEADERS = ["tt_device.cuh", "tt_pacm64.cuh", "tt_finish.cuh", "tt_features.cuh", "tt_block.cuh", "tt_kernels.h", "tt_tc.cuh"]
 
 
 def _mtime(p):

@@ -25,9 +25,9 @@ __device__ __forceinline__ uint64_t ordered(double x) {
 // position asc; excluded never chosen) fused with the record gather for the
 // single device->host copy: [0] selected, [1] drafted, [2] status, [3]
 // rescored, then b population indices, b scores, b draft costs, b
-// identities. n <= 1024, b <= 32: every warp sorts its 32 keys with
-// shuffles (15 exchange steps, no shared-memory network); the warps' b best
-// are then ranked among each other by counting.
+// identities. n <= 1024, b <= 32: the keys no larger than the b-th smallest
+// warp minimum (a bound on the b-th best) are the only candidates; they are
+// ranked among each other by counting.
 __device__ __forceinline__ void warp_sort32(Key3& k) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -106,37 +106,47 @@ __device__ __forceinline__ void finish_block(const double* __restrict__ scores, 
   k.c = ok ? (uint32_t)t : 0xffffffffu;
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   if (lane == 0 && bal) atomicAdd(&avail, __popc(bal));
-  warp_sort32(k);
+  // filter: M = the b-th smallest of the warps' minima (select_top's order is
+  // ascending Key3). At least b keys are <= M (those b warp minima), so the
+  // b best are all <= M; when fewer than b warps hold a key, every key is a
+  // candidate. Only the candidates are ranked, by counting.
+  Key3 mn = k;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const Key3 o = mn.shfl_xor(off);
+    if (o.lt(mn)) mn = o;
+  }
+  Key3* wmin = &lists[0][0];   // [nw <= 32] warp minima
+  Key3* cand = &lists[0][32];  // the candidates: <= 32 b <= 1024 (the keys of the <= b warps whose minimum is <= M)
+  if (lane == 0) wmin[warp] = mn;
+  if (t == 0) fs.cnt[0] = 0;  // candidate count
+  __syncthreads();
   if (threadIdx.x == 0) g_fin_clk[1] = clock64();
-  // each warp's b best (sorted ascending in its lanes) are the only
-  // candidates for the global b best: rank them among the nw * b by counting
-  // (independent comparisons, no serial tournament)
-  Key3* cand = &lists[0][0];
-  if (lane < b) cand[warp * b + lane] = k;
+  if (warp == 0) {  // lane w: rank of warp w's minimum among the minima
+    Key3 me;
+    me.a = kAll, me.b = kAll, me.c = 0xffffffffu;
+    if (lane < nw) me = wmin[lane];
+    int r = 0;
+    for (int q = 0; q < nw; ++q) r += wmin[q].lt(me) ? 1 : 0;
+    const unsigned hit = __ballot_sync(0xffffffffu, me.c != 0xffffffffu && r == (int)b - 1);
+    if (lane == 0) fs.cnt[1] = hit ? (int)(__ffs(hit) - 1) : -1;  // the warp whose minimum is M, or none
+  }
+  __syncthreads();
+  const int mw = fs.cnt[1];
+  Key3 M;
+  M.a = kAll, M.b = kAll, M.c = 0xffffffffu;
+  if (mw >= 0) M = wmin[mw];
+  if (k.c != 0xffffffffu && !M.lt(k)) cand[atomicAdd(&fs.cnt[0], 1)] = k;  // k <= M
   __syncthreads();
   if (threadIdx.x == 0) g_fin_clk[2] = clock64();
   const int64_t keep = b < avail ? b : avail;
-  __syncthreads();
-  const int m = nw * (int)b;
-  // rank of candidate i = number of candidates below it; the j range is
-  // split over the block's threads (parts of 32 comparisons, integer adds
-  // in shared memory: order-independent, exact)
-  int* cnt = fs.cnt;
-  for (int i = t; i < m; i += blockDim.x) cnt[i] = 0;
-  __syncthreads();
-  const int parts = (m + 31) / 32;
-  for (int w = t; w < m * parts; w += blockDim.x) {
-    const int i = w % m, j0 = (w / m) * 32, j1 = j0 + 32 < m ? j0 + 32 : m;
+  const int m = fs.cnt[0];
+  if (threadIdx.x == 0) g_fin_clk[5] = m, g_fin_clk[6] = mw;
+  for (int i = t; i < m; i += blockDim.x) {  // rank among the candidates (a strict total order)
     const Key3 me = cand[i];
     int r = 0;
-#pragma unroll 8
-    for (int j = j0; j < j1; ++j) r += cand[j].lt(me);
-    if (r) atomicAdd(&cnt[i], r);
-  }
-  __syncthreads();
-  for (int i = t; i < m; i += blockDim.x) {
-    const Key3 me = cand[i];
-    if (me.c != 0xffffffffu && cnt[i] < keep) rank_of[me.c] = (int16_t)cnt[i];  // absent keys rank past every real one
+    for (int q = 0; q < m; ++q) r += cand[q].lt(me) ? 1 : 0;
+    if (r < keep) rank_of[me.c] = (int16_t)r;
   }
   __syncthreads();
   if (threadIdx.x == 0) g_fin_clk[3] = clock64();

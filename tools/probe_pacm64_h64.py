@@ -50,4 +50,5 @@ if fused:
     fc = (C.c_longlong * 8)()
     L.ttdbg_verify64_finish_clocks(fc)
     f = list(fc)
-    print(f"finish_block: loads+init {f[0]-f[4]} | warp sort {f[1]-f[0]} | cand {f[2]-f[1]} | rank {f[3]-f[2]} cycles")
+    print(f"finish_block: loads+init {f[0]-f[4]} | warp minima {f[1]-f[0]} | candidates {f[2]-f[1]} | rank {f[3]-f[2]} "
+          f"cycles; {f[5]} candidates, bound from warp {f[6]}")
