@@ -262,6 +262,33 @@ def run_ours(args, rank, world, local_rank):
     h2d = sum(x.numel() * 8 for x in ids_host) + params_host.numel() * 8
     d2h = len(sketches) * 8 * (7 + 4 * b)  # each round record, written by its finishing kernel into mapped pinned memory
 
+    # ---- e2e with the candidates uploaded in the SoA factor layout itself (int32 columns,
+    # 4 B per factor: 76 B per conv candidate) instead of 8-byte identities: no decode step
+    pops_host = [p_.cpu().pin_memory() for p_ in pops]
+    ev_soa = [torch.cuda.Event() for _ in sketches]
+
+    def prep_soa(r):
+        with torch.cuda.stream(copy_stream):
+            pops[r].copy_(pops_host[r], non_blocking=True)
+            ev_soa[r].record(copy_stream)
+
+    def step_e2e_soa():
+        ev_start = torch.cuda.Event()
+        ev_start.record(stream)
+        copy_stream.wait_event(ev_start)
+        prep_soa(0)
+        model.load(params_host)
+        for r, sk in enumerate(sketches):
+            if r + 1 < len(sketches):
+                prep_soa(r + 1)
+            stream.wait_event(ev_soa[r])
+            one_round(sk, pops[r])
+            if r > 0:
+                assert tt.round_collect(ctx, b).selected == b
+        assert tt.round_collect(ctx, b).selected == b
+    sotimes, _, _ = timed(step_e2e_soa)
+    h2d_soa = sum(x.numel() * 4 for x in pops_host) + params_host.numel() * 8
+
     # ---- e2e, seeded API (explore(seed) semantics: population drawn inside the call)
     def step_seeded():
         model.load(params_host)
@@ -333,7 +360,7 @@ def run_ours(args, rank, world, local_rank):
             c_.close()
 
     b1m = None if args.no_bert else bert_1m(args, ctx, dev, params_host, rank, world, stream, flush)
-    tot, etot, stot, atot = agg(times), agg(etimes), agg(stimes), agg(atimes)
+    tot, etot, stot, atot, sotot = agg(times), agg(etimes), agg(stimes), agg(atimes), agg(sotimes)
     cands = n * world * len(sketches) * args.steps
     result = None
     if rank == 0:
@@ -360,6 +387,11 @@ def run_ours(args, rank, world, local_rank):
                            "from pinned host memory, the next subgraph's upload overlapped on a copy stream, "
                            "every round's selection read back (round r-1's while round r runs); identities "
                            "decoded on a second context's stream, overlapping the previous round"},
+            "e2e_soa": {"value": cands / sotot, "unit": UNIT, "h2d_bytes_per_step": h2d_soa,
+                        "d2h_bytes_per_step": d2h,
+                        "api": "tt_round_async / tt_round_collect with the population uploaded every round in the "
+                               "SoA factor layout (int32 columns, 4 B per factor) from pinned host memory, the next "
+                               "subgraph's upload overlapped on a copy stream; no identity decode"},
             "e2e_seeded": {"value": cands / stot, "unit": UNIT,
                            "h2d_bytes_per_step": params_host.numel() * 8, "d2h_bytes_per_step": d2h,
                            "api": "explore(seed) semantics: population drawn on device inside the call"},
