@@ -631,23 +631,18 @@ def explore_ga(args, ctx, dev, sketches, names, reps=5):
 
 def tuner_round(R, ctx, sk, dev, threads, reps):
     """The tuner's whole real round at TunerConfig defaults (tuner.cpp:294-384: GA draft set with
-    random_mix 0.2 -> features -> PaCM fp64 -> select_top(10)) through the public API (tt_draft_set,
-    tt_pacm_score, tt_select_top; host in, host out), beside the reference's own functions composed
-    the same way (oracle/_ref ref_tuner_round)."""
+    random_mix 0.2 -> features -> PaCM fp64 -> select_top(10)) through the public API (tt_tuner_round:
+    host in, host out, one call), beside the reference's own functions composed the same way
+    (oracle/_ref ref_tuner_round)."""
     import ctypes as C
-
-    import torch
 
     from paper_2402_02361_b200 import tiletune as tt
     from paper_2402_02361_b200.types import TAG_INIT, derive_seed
     params = tt.init_params(64, derive_seed(5, TAG_INIT))
-    model = tt.PaCM(ctx, params, 64)
+    tt.PaCM(ctx, params, 64)
 
     def ours(seed):
-        ids, dc, _ = tt.draft_set(ctx, sk, dev, 32, 512, 512, 0.2, seed, seed + 1)
-        ids_d = torch.from_numpy(ids.view(np.int64)).cuda()
-        sc = model.score(sk, dev, ids_d, tt.TT_PREC_FP64)
-        return tt.select_top(ctx, sc, torch.from_numpy(dc).cuda(), None, 10)
+        return tt.tuner_round(ctx, sk, dev, 32, 512, 512, 0.2, seed, seed + 1, 10, tt.TT_PREC_FP64)[0]
     ours(7)
     t0 = time.perf_counter()
     for r in range(reps):

@@ -34,15 +34,32 @@ namespace tt {
 namespace {
 
 constexpr int kMutThreads = 512;
-constexpr int kSegs = 128;  // offset-chain segments (stitched by one thread)
+constexpr int kWork = kMutThreads - 32;  // warps 0..14 work; warp 15 publishes generations to the host
+constexpr int kMain = 224;               // warps 0..6: this generation's wheel and children
+constexpr int kPrep = kWork - kMain;     // warps 7..14: the next generation's offset chain and draws
+constexpr int kSegs = 128;               // offset-chain segments
+// CTAs of the explore cluster and the children slice of each (rounded up to
+// even so the arrays after it stay 8-byte aligned)
+__host__ __device__ constexpr int cluster_of(int64_t n) { return n > 448 ? 8 : (int)((n + 63) / 64); }
+__host__ __device__ constexpr int explore_per_cap(int64_t n) {
+  return (int)(((n + cluster_of(n) - 1) / cluster_of(n) + 1) & ~1LL);
+}
 constexpr int kMaxCols = 4 * 4 + 3 * 3 + 1;  // 4 spatial x 4 + 3 reduction x 3 + unroll
 
 // clock64 marks of thread 0 at the phase boundaries (ttdbg_mutate_clocks)
-__device__ long long g_clk_mut[8];
-#define MUT_MARK(i)                          \
-  do {                                       \
-    if (tid == 0 && blockIdx.x == 0) g_clk_mut[i] = clock64(); \
+// of generation g_mut_gen (ttdbg_mutate_probe)
+__device__ long long g_clk_mut[26];
+__device__ int g_mut_gen = 1;
+__device__ unsigned long long g_mut_ns[4];  // globaltimer at kernel start / generation 1 start / loop end; clock64 span
+#define MUT_MARK_T(i, t)                                            \
+  do {                                                              \
+    if (tid == (t)) {                                               \
+      long long c_;                                                 \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)::"memory"); \
+      s_clk[i] = c_;                                                \
+    }                                                               \
   } while (0)
+#define MUT_MARK(i) MUT_MARK_T(i, 0)
 
 __device__ __forceinline__ int upper_bound_d(const double* cum, int n, double r) {
   int lo = 0, hi = n;
@@ -146,17 +163,6 @@ struct GenOut {  // pinned host slots: generation g at base + g * stride
   size_t stride, cost_off;
 };
 
-// every thread's host writes, then one system-scope flag per generation:
-// the CTA barrier orders the block's writes before thread 0's fence, and the
-// (cumulative) fence orders them before the flag, as in a grid barrier
-__device__ __forceinline__ void publish(volatile uint32_t* flags, int g) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    flags[g] = 1u;
-  }
-}
-
 // generation g's device slot
 __device__ __forceinline__ GenDev gen_dev(const GenOut& d, int g, int n) {
   char* b = d.base + (size_t)g * d.stride;
@@ -168,58 +174,119 @@ __device__ __forceinline__ GenDev gen_dev(const GenOut& d, int g, int n) {
 }
 
 // Writes generation g's member j: factors, cost and identity to its device
-// slot (every generation keeps its own), cost and identity to the pinned
-// host mirror the pool is built from.
+// slot (every generation keeps its own). The pinned host mirror is written
+// by the publishing warp (publish_slice), so no working thread has a
+// system-memory write in flight at a cluster barrier.
 template <int NSP, int NRED>
-__device__ __forceinline__ void emit(const GenOut& h, int g, int n, const GenDev& d, int j, const Factors<NSP, NRED>& F,
-                                     double c, uint64_t id, bool write_dev_soa) {
+__device__ __forceinline__ void emit(int n, const GenDev& d, int j, const Factors<NSP, NRED>& F, double c, uint64_t id,
+                                     bool write_dev_soa) {
   constexpr int kN = Factors<NSP, NRED>::kN;
-  char* hb = h.base + (size_t)g * h.stride;
-  double* hc = (double*)(hb + h.cost_off);
-  uint64_t* hi = (uint64_t*)(hc + n);
   if (write_dev_soa) {
 #pragma unroll
     for (int q = 0; q < kN; ++q) d.soa[(size_t)q * n + j] = F.f[q];
     d.soa[(size_t)kN * n + j] = F.unroll;
   }
   d.cost[j] = c, d.id[j] = id;
-  hc[j] = c, hi[j] = id;
 }
 
+// One warp: this CTA's slice [jlo, jhi) of generation g (device slot d,
+// written by this CTA before a barrier the warp has passed) copied to the
+// pinned host slot, then the slice's system-scope flag. Lane 0's release
+// fence is cumulative over the lanes' writes it observed through the
+// warp barrier.
+__device__ __forceinline__ void publish_slice(const GenOut& h, const GenDev& d, int g, int n, int jlo, int jhi,
+                                              volatile uint32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  char* hb = h.base + (size_t)g * h.stride;
+  double* hc = (double*)(hb + h.cost_off);
+  uint64_t* hi = (uint64_t*)(hc + n);
+  for (int j = jlo + lane; j < jhi; j += 32) hc[j] = d.cost[j], hi[j] = d.id[j];
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    *flag = 1u;
+  }
+}
+
+// Segment maps of the offset chain: entry e in [0, 4) (offset lo + e) ->
+// (exit relative to the next segment's lo, children started inside), four
+// 16-bit fields (exit << 14 | count). Composition is associative, so the
+// chain's entry into every segment is a scan.
+__device__ __forceinline__ uint64_t seg_map(const int32_t* seg_exit, const int32_t* seg_cnt, int s, int W) {
+  uint64_t m = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t x = (uint32_t)(seg_exit[4 * s + e] - (s + 1) * W) & 3u;
+    m |= (uint64_t)(x << 14 | (uint32_t)seg_cnt[4 * s + e]) << (16 * e);
+  }
+  return m;
+}
+__device__ __forceinline__ uint64_t map_compose(uint64_t a, uint64_t b) {  // a, then b
+  uint64_t r = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t fa = (uint32_t)(a >> (16 * e)) & 0xffffu;
+    const uint32_t fb = (uint32_t)(b >> (16 * (fa >> 14))) & 0xffffu;
+    r |= (uint64_t)((fb & 0xc000u) | ((fa & 0x3fffu) + (fb & 0x3fffu))) << (16 * e);
+  }
+  return r;
+}
+constexpr uint64_t kMapIdentity = (uint64_t)1 << 30 | (uint64_t)2 << 46 | (uint64_t)3 << 62;
+
 // All generations of one explore in one thread-block cluster (<= 8 CTAs):
-// generation 0 is the random_init
-// population already in slot 0 (k_generate); generation g >= 1 is
-// mutate(generation g-1) written into slot g & 1. Every member's draft cost
-// and identity are computed by the thread that produced it, and each CTA's
-// slice of a generation is published to pinned host memory followed by a
-// system-scope flag (flags[g * clusters + rank]), so the host folds the
-// generation into the pool while the device moves on.
+// generation 0 is the random_init population already in device slot 0
+// (k_generate); generation g >= 1 is mutate(generation g-1) in slot g. Every
+// member's draft cost and identity are computed by the thread that produced
+// it, and each CTA's slice of a generation is published to pinned host
+// memory followed by a system-scope flag (flags[g * clusters + rank]), so the
+// host folds the generation into the pool while the device moves on.
+//
+// Warp roles (the generation chain is latency bound, so the work that does
+// not depend on the costs is taken off it):
+//   main  (warps 0..6)   weights, the DADD running total (warp 0) while
+//                        warps 1..6 stage the parents in shared memory, then
+//                        the children of this CTA's slice;
+//   prep  (warps 7..14)  the NEXT generation's parent-independent part: the
+//                        draw count at every stream offset, the offset chain
+//                        (segment walks per entry, a warp scan of the
+//                        segment maps, re-walks) and every child's draws;
+//   publish (warp 15)    the previous generation's host copy and flag.
 template <int NSP, int NRED>
 __global__ void __launch_bounds__(kMutThreads, 1)
-    k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenOut dv, uint64_t s_init,
-                   GenOut h, volatile uint32_t* flags, int staged) {
+    k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenOut dv, uint64_t s_init, GenOut h,
+                   volatile uint32_t* flags, int staged) {
   constexpr int kN = Factors<NSP, NRED>::kN;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* cum = (double*)smem;        // [n] weights, then their running sums
-  int32_t* off = (int32_t*)(cum + n);  // [n] stream offset of child j
-  uint8_t* len = (uint8_t*)(off + n);  // [4n] draws a child starting at offset o consumes
-  int32_t* seg_exit = (int32_t*)(len + 4 * (size_t)n);  // [kSegs][4]
+  const int per_cap = explore_per_cap(n);
+  double* cum = (double*)smem;                          // [n] weights, then their running sums
+  double* ch_u = cum + n;                               // [2][per_cap] roulette uniform of child jlo + c
+  int32_t* ch_p = (int32_t*)(ch_u + 2 * per_cap);       // [2][per_cap] slot + 1 | move / unroll draws
+  int32_t* off = ch_p + 2 * per_cap;                    // [n] stream offset of child j
+  int32_t* seg_exit = off + n;                          // [kSegs][4]
   int32_t* seg_cnt = seg_exit + 4 * kSegs;              // [kSegs][4]
   int32_t* seg_entry = seg_cnt + 4 * kSegs;             // [kSegs]
   int32_t* seg_base = seg_entry + kSegs;                // [kSegs]
+  uint8_t* len = (uint8_t*)(seg_base + kSegs);          // [4n] draws a child starting at offset o consumes
   // staged copy of the previous generation (when it fits): parents are read
   // at random by the apply pass, so they come from shared memory
-  uint64_t* id_s = (uint64_t*)(seg_base + kSegs);  // [n]
-  int32_t* pop_s = (int32_t*)(id_s + n);            // [cols][n]
+  uint64_t* id_s = (uint64_t*)(len + 4 * (size_t)n);    // [n] (4n is a multiple of 8)
+  int32_t* pop_s = (int32_t*)(id_s + n);                // [cols][n]
   __shared__ double s_total;
-  __shared__ uint64_t s_state;
   __shared__ int s_t0[TT_MAX_AXES], s_np[TT_MAX_AXES], s_omega[TT_MAX_AXES];
   __shared__ uint64_t s_w[TT_MAX_PRIMES];  // identity weight of each (axis, prime) digit
   __shared__ PrimeTab tab;
-  __shared__ double s_bc[kMutThreads / 32];
-  __shared__ int s_bi[kMutThreads / 32];
+  __shared__ double s_bc[kMain / 32];
+  __shared__ int s_bi[kMain / 32];
+  __shared__ long long s_clk[26];  // phase marks of generation probe_g, written out at the end
   const int tid = threadIdx.x;
   const int n_axes = S.n_axes;
+  const int probe_g = g_mut_gen;
+  unsigned long long ns0 = 0;
+  long long ck0 = 0;
+  if (tid == 0 && blockIdx.x == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns0)::"memory");
+    ck0 = clock64();
+  }
   // the grid is one thread-block cluster: every CTA derives the generation's
   // wheel and offset chain itself (identical, deterministic) and produces its
   // own slice of the children; generations are separated by cluster barriers
@@ -244,204 +311,260 @@ __global__ void __launch_bounds__(kMutThreads, 1)
     uint64_t w = (uint64_t)S.n_unroll;
     for (int t = S.n_prime - 1; t >= 0; --t) s_w[t] = w, w *= S.pr_count[t];
   }
-  // generation 0: cost the random_init population
-  for (int j = jlo + tid; j < jhi; j += kMutThreads) {
-    Factors<NSP, NRED> F;
-    const GenDev d0 = gen_dev(dv, 0, n);
-    load_factors_cg<NSP, NRED>(d0.soa, n, j, F);
-    emit<NSP, NRED>(h, 0, n, d0, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), d0.id[j], false);
-  }
-  publish(flags, cr);
-  cluster.sync();
-  uint64_t s0 = s_init;
-  const int n_off = 4 * (n - 1);  // child n-1 starts at offset <= 4(n-2)
-  for (int g = 1; g < n_steps; ++g) {
-  const GenDev prev = gen_dev(dv, g - 1, n);
-  const GenDev cur = gen_dev(dv, g, n);
-  const double* cost = prev.cost;
-  if (g == 1) MUT_MARK(0);
-  if (staged) {
-    for (int i = tid; i < (kN + 1) * n; i += kMutThreads) pop_s[i] = prev.soa[i];
-    for (int i = tid; i < n; i += kMutThreads) id_s[i] = prev.id[i];
-  }
-  const int32_t* pop = staged ? pop_s : prev.soa;
-  const uint64_t* pid = staged ? id_s : prev.id;
-  // A. weights 1 / (cost + eps) (schedule.cpp:347-351), the elite (first
-  // argmin, :360-362) and the draw count of a child starting at every offset.
-  // A child consumes parent + slot draws, then 1 (unroll) or, for an axis
-  // slot, 2 more iff it has a movable prime — and the slot's factors multiply
-  // to the axis extent, so that is "extent > 1", independent of the parent.
-  double bc = __longlong_as_double(0x7ff0000000000000LL);
-  int bi = n;
-  for (int i = tid; i < n; i += kMutThreads) {
-    const double c = cost[i];
-    cum[i] = 1.0 / __dadd_rn(c, 1e-12);
-    if (c < bc) bc = c, bi = i;
-  }
-  for (int o = tid; o < n_off; o += kMutThreads) {
-    const int slot = (int)uniform_index(draw(s0, (uint64_t)o + 1), (uint64_t)n_axes + 1);
-    len[o] = (uint8_t)tab.len[slot];
-  }
-  for (int o = 16; o; o >>= 1) {
-    const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
-  }
-  if ((tid & 31) == 0) s_bc[tid >> 5] = bc, s_bi[tid >> 5] = bi;
   __syncthreads();
-  if (g == 1) MUT_MARK(1);
-  // B. warp 0: the elite, then the running total in the reference's order
-  // (one dependent DADD chain, operands staged through registers).
-  // Meanwhile the other warps build the chain of child start offsets
-  // o_1 = 0, o_{j+1} = o_j + len[o_j]: segment s covers offsets
-  // [s*W, (s+1)*W) and the chain enters it at one of its first 4 offsets
-  // (len <= 4), so each segment is walked from all 4 entries (exit, child
-  // count), one thread stitches the true entries, and every segment is
-  // re-walked from its entry to write the offsets.
-  // segment count balancing the walks (~5W/3 steps) against the stitch (segs steps)
+
+  const int n_off = 4 * (n - 1);  // child n-1 starts at offset <= 4(n-2)
+  // segment count balancing the walks (~W/2.5 steps) against the scan
   const int segs = min(kSegs, max(1, (int)sqrtf(1.67f * (float)n_off)));
   const int W = (n_off + segs - 1) / segs;
-  if (tid < 32) {
-    bc = tid < kMutThreads / 32 ? s_bc[tid] : __longlong_as_double(0x7ff0000000000000LL);
-    bi = tid < kMutThreads / 32 ? s_bi[tid] : n;
-    for (int o = 16; o; o >>= 1) {
-      const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
+  // The prep team's pass for the generation whose mutate() starts at RNG
+  // state sp: its children's draws into ch_*[buf]; returns the state after it.
+  auto prep = [&](uint64_t sp, int buf, bool mark) -> uint64_t {
+    const int p = tid - kMain;
+    if (mark) MUT_MARK_T(15, kMain);
+    // A child consumes parent + slot draws, then 1 (unroll) or, for an axis
+    // slot, 2 more iff it has a movable prime — and the slot's factors
+    // multiply to the axis extent, so that is "extent > 1", independent of
+    // the parent. So the draw count at every offset is known up front.
+    for (int o = p; o < n_off; o += kPrep)
+      len[o] = (uint8_t)tab.len[(int)uniform_index(draw(sp, (uint64_t)o + 1), (uint64_t)n_axes + 1)];
+    named_barrier(3, kPrep);
+    if (mark) MUT_MARK_T(16, kMain);
+    // the chain o_1 = 0, o_{j+1} = o_j + len[o_j]: segment s covers offsets
+    // [s W, (s + 1) W) and the chain enters it at one of its first 4 offsets
+    // (len <= 4): each (segment, entry) walked by its own thread
+    for (int q = p; q < 4 * segs; q += kPrep) {
+      const int sg = q >> 2, hi = min(sg * W + W, n_off);
+      int o = sg * W + (q & 3), c = 0;
+      while (o < hi) o += len[o], ++c;
+      seg_exit[q] = o, seg_cnt[q] = c;
     }
-    if (tid == 0) {
-      s_bi[0] = bi;
-      double t = 0.0;
-      int i = 0;
-      for (; i + 16 <= n; i += 16) {
-        double w[16];
+    named_barrier(3, kPrep);
+    if (mark) MUT_MARK_T(17, kMain);
+    if (p < 32) {  // scan of the segment maps: entry offset and first child of every segment
+      const int qn = (segs + 31) >> 5, s_lo = min(segs, p * qn), s_hi = min(segs, s_lo + qn);
+      uint64_t m = kMapIdentity;
+      for (int sg = s_lo; sg < s_hi; ++sg) m = map_compose(m, seg_map(seg_exit, seg_cnt, sg, W));
 #pragma unroll
-        for (int q = 0; q < 16; ++q) w[q] = cum[i + q];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) t = __dadd_rn(t, w[q]), w[q] = t;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) cum[i + q] = w[q];
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, m, d);
+        if (p >= d) m = map_compose(o, m);
       }
-      for (; i < n; ++i) t = __dadd_rn(t, cum[i]), cum[i] = t;
-      s_total = t;
-    }
-  } else {
-    // warps 1..: the offset chain, synchronised among themselves only, so
-    // it runs under warp 0's DADD chain
-    const int sg = tid - 32;
-    if (sg < segs) {
-      const int lo = sg * W, hi = min(lo + W, n_off);
-      for (int e = 0; e < 4; ++e) {
-        int o = lo + e, c = 0;
-        while (o < hi) o += len[o], ++c;
-        seg_exit[sg * 4 + e] = o, seg_cnt[sg * 4 + e] = c;
-      }
-    }
-    named_barrier(1, kMutThreads - 32);
-    // stitch: the true entry offset and first child of every segment
-    if (sg == 0) {
-      int o = 0, j = 1;
-      for (int g = 0; g < segs; ++g) {
-        seg_entry[g] = o, seg_base[g] = j;
-        const int lo = g * W;
-        if (o < lo + W && lo < n_off) {
-          const int e = o - lo;
-          j += seg_cnt[g * 4 + e];
-          o = seg_exit[g * 4 + e];
-        }
+      uint64_t pre = __shfl_up_sync(0xffffffffu, m, 1);
+      if (p == 0) pre = kMapIdentity;
+      int e = (int)(pre >> 14) & 3, j = 1 + (int)(pre & 0x3fffu);  // the chain starts at offset 0, child 1
+      for (int sg = s_lo; sg < s_hi; ++sg) {
+        seg_entry[sg] = sg * W + e, seg_base[sg] = j;
+        const uint32_t f = (uint32_t)(seg_map(seg_exit, seg_cnt, sg, W) >> (16 * e)) & 0xffffu;
+        e = (int)(f >> 14), j += (int)(f & 0x3fffu);
       }
     }
-    named_barrier(1, kMutThreads - 32);
+    named_barrier(3, kPrep);
+    if (mark) MUT_MARK_T(18, kMain);
     // every segment re-walked from its entry to place its children's offsets
-    if (sg < segs) {
+    for (int sg = p; sg < segs; sg += kPrep) {
       const int hi = min(sg * W + W, n_off);
       int o = seg_entry[sg], j = seg_base[sg];
       while (o < hi && j < n) off[j] = o, o += len[o], ++j;
     }
-  }
-  __syncthreads();
-  if (g == 1) MUT_MARK(2);
-  if (g == 1) MUT_MARK(3);
-  if (tid == 0) {
-    const int last = off[n - 1];
-    s_state = s0 + (uint64_t)(last + len[last]) * kGolden;  // RngStream state after mutate()
-  }
-  // D. children: elite at 0 (schedule.cpp:368), the rest from their draws
-  const double total = s_total;
-  const int best = s_bi[0];
-  for (int j = jlo + tid; j < jhi; j += kMutThreads) {
-    int par = best;
-    int slot = -1, from = 0, to = 0, c0 = 0, tsel = 0, uidx = 0;
-    int32_t prime = 1, unroll = 0;
-    uint32_t f[4] = {1u, 1u, 1u, 1u};
-    if (j > 0) {
+    named_barrier(3, kPrep);
+    if (mark) MUT_MARK_T(19, kMain);
+    // the parent-independent draws of this CTA's children: the roulette
+    // uniform, the slot and the move / unroll draws
+    for (int j = jlo + p; j < jhi; j += kPrep) {
+      if (j == 0) continue;
       const uint64_t o = (uint64_t)off[j];
-      const double r = __dmul_rn((double)(draw(s0, o) >> 11) * 0x1.0p-53, total);
-      par = upper_bound_d(cum, n, r);
-      slot = (int)uniform_index(draw(s0, o + 1), (uint64_t)n_axes + 1);
+      ch_u[buf * per_cap + j - jlo] = (double)(draw(sp, o) >> 11) * 0x1.0p-53;
+      const int slot = (int)uniform_index(draw(sp, o + 1), (uint64_t)n_axes + 1);
+      int pk = 0;  // slot + 1, 0 = nothing movable (the child is the parent)
       if (slot == n_axes) {
-        uidx = (int)uniform_index(draw(s0, o + 2), (uint64_t)S.n_unroll);
-        unroll = tab.unroll[uidx];
-      } else {
-        c0 = slot_col0(S, slot);
-        const int arity = tab.arity[slot];
-        const int nm = s_omega[slot];
-        if (nm > 0 && arity > 1) {
-          load_slot(pop, n, c0, arity, par, f);
-          const int m = (int)uniform_index(draw(s0, o + 2), (uint64_t)nm);
-          pick_move(tab, s_t0[slot], s_np[slot], f, arity, m, &from, &prime, &tsel);
-          to = (int)uniform_index(draw(s0, o + 3), (uint64_t)arity - 1);
-          if (to >= from) ++to;
-        } else {
-          slot = -1;  // nothing movable: the child is the parent
-        }
+        pk = (slot + 1) | (int)uniform_index(draw(sp, o + 2), (uint64_t)S.n_unroll) << 8;
+      } else if (s_omega[slot] > 0 && tab.arity[slot] > 1) {
+        const int m = (int)uniform_index(draw(sp, o + 2), (uint64_t)s_omega[slot]);
+        const int to = (int)uniform_index(draw(sp, o + 3), (uint64_t)tab.arity[slot] - 1);
+        pk = (slot + 1) | m << 8 | to << 24;
       }
+      ch_p[buf * per_cap + j - jlo] = pk;
     }
-    const bool mv = slot >= 0 && slot < n_axes;
-    const int c_from = mv ? c0 + from : -1, c_to = mv ? c0 + to : -1, c_un = slot == n_axes ? kN : -1;
-    // all columns loaded before any store: one L2 round trip per child
-    Factors<NSP, NRED> F;
-    load_factors_cg<NSP, NRED>(pop, n, par, F);
-    // the child's identity from its parent's: one digit changes (the moved
-    // prime's exponent composition, or the unroll index)
-    uint64_t id_j = pid[par];
-    if (c_un == kN) {
-      int uold = 0;
-      for (int u = 0; u < S.n_unroll; ++u)
-        if (tab.unroll[u] == F.unroll) uold = u;
-      id_j += (uint64_t)uidx - (uint64_t)uold;
-    } else if (mv) {
-      const int arity = tab.arity[slot];
-      int e[4];
-      exps_of(tab, tsel, f, arity, e);
-      const uint64_t d_old = rank_composition(tab.e[tsel], arity, e);
-      e[from] -= 1, e[to] += 1;
-      const uint64_t d_new = rank_composition(tab.e[tsel], arity, e);
-      id_j += (d_new - d_old) * s_w[tsel];
+    const int last = off[n - 1];
+    const uint64_t nx = sp + (uint64_t)(last + len[last]) * kGolden;  // RngStream state after mutate()
+    named_barrier(3, kPrep);  // off / len read before the next pass rewrites them
+    if (mark) MUT_MARK_T(20, kMain);
+    return nx;
+  };
+
+  // generation 0: cost the random_init population; the prep team prepares
+  // generation 1 meanwhile
+  uint64_t s_prep = s_init;
+  if (tid < kMain) {
+    const GenDev d0 = gen_dev(dv, 0, n);
+    for (int j = jlo + tid; j < jhi; j += kMain) {
+      Factors<NSP, NRED> F;
+      load_factors_cg<NSP, NRED>(d0.soa, n, j, F);
+      emit<NSP, NRED>(n, d0, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), d0.id[j], false);
     }
-    if (c_un == kN) F.unroll = unroll;
-#pragma unroll
-    for (int q = 0; q < kN; ++q) {
-      if (q == c_from) F.f[q] /= prime;
-      if (q == c_to) F.f[q] *= prime;
-    }
-    if (g == 1) MUT_MARK(5);
-    const double c_j = draft_cost_of<NSP, NRED>(S, D, F, toggles);
-    if (g == 1 && c_j > 0) MUT_MARK(6);
-    if (g == 1 && id_j != 1) MUT_MARK(7);
-    emit<NSP, NRED>(h, g, n, cur, j, F, c_j, id_j, true);
+  } else if (tid < kWork && n_steps > 1) {
+    s_prep = prep(s_prep, 1, false);
   }
-  if (g == 1) MUT_MARK(4);
-  publish(flags, g * nc + cr);
-  cluster.sync();  // generation g complete in every CTA before anyone reads it
-  s0 = s_state;
+  cluster.sync();
+  if (tid == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    g_mut_ns[1] = t - ns0;
+  }
+  for (int g = 1; g < n_steps; ++g) {
+    const GenDev prev = gen_dev(dv, g - 1, n);
+    if (g == probe_g) MUT_MARK(0);
+    if (tid >= kWork) {
+      // warp 15 publishes the previous generation (this CTA's slice) to the
+      // host while the others build this one: the system fence waits for the
+      // host writes' PCIe completions, so no working warp carries them
+      publish_slice(h, prev, g - 1, n, jlo, jhi, flags + (g - 1) * nc + cr);
+    } else if (tid >= kMain) {
+      if (g + 1 < n_steps) s_prep = prep(s_prep, (g + 1) & 1, g == probe_g);
+    } else {
+      const GenDev cur = gen_dev(dv, g, n);
+      const int32_t* pop = staged ? pop_s : prev.soa;
+      const uint64_t* pid = staged ? id_s : prev.id;
+      // A. weights 1 / (cost + eps) (schedule.cpp:347-351) and the elite
+      // (first argmin, :360-362)
+      double bc = __longlong_as_double(0x7ff0000000000000LL);
+      int bi = n;
+      for (int i = tid; i < n; i += kMain) {
+        const double c = prev.cost[i];
+        cum[i] = 1.0 / __dadd_rn(c, 1e-12);
+        if (c < bc) bc = c, bi = i;
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
+      }
+      if ((tid & 31) == 0) s_bc[tid >> 5] = bc, s_bi[tid >> 5] = bi;
+      if (g == probe_g) MUT_MARK(14);
+      named_barrier(2, kMain);
+      // B. warp 0: the elite, then the running total in the reference's
+      // order (one dependent DADD chain, operands staged through registers);
+      // warps 1..6 stage the parents into shared memory meanwhile
+      if (tid < 32) {
+        bc = tid < kMain / 32 ? s_bc[tid] : __longlong_as_double(0x7ff0000000000000LL);
+        bi = tid < kMain / 32 ? s_bi[tid] : n;
+        for (int o = 16; o; o >>= 1) {
+          const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
+        }
+        if (tid == 0) {
+          s_bi[0] = bi;
+          double t = 0.0;
+          int i = 0;
+          for (; i + 16 <= n; i += 16) {
+            double w[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) w[q] = cum[i + q];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) t = __dadd_rn(t, w[q]), w[q] = t;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) cum[i + q] = w[q];
+          }
+          for (; i < n; ++i) t = __dadd_rn(t, cum[i]), cum[i] = t;
+          s_total = t;
+          if (g == probe_g) MUT_MARK(22);
+        }
+      } else if (staged) {
+        // async copies, all in flight at once, no register staging; every
+        // generation has its own device slot, so no stale L1 line can hit
+        const int nt = kMain - 32, t = tid - 32;
+        const uint32_t sp = (uint32_t)__cvta_generic_to_shared(pop_s);
+        const uint32_t si = (uint32_t)__cvta_generic_to_shared(id_s);
+        for (int i = t; i < (kN + 1) * n; i += nt)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sp + 4u * i), "l"(prev.soa + i) : "memory");
+        for (int i = t; i < n; i += nt)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(si + 8u * i), "l"(prev.id + i) : "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        if (g == probe_g) MUT_MARK_T(21, 32);
+      }
+      named_barrier(2, kMain);
+      if (g == probe_g) MUT_MARK(3);
+      // D. children: elite at 0 (schedule.cpp:368), the rest from their draws
+      const double total = s_total;
+      const int best = s_bi[0];
+      const double* cu = ch_u + (g & 1) * per_cap;
+      const int32_t* cp = ch_p + (g & 1) * per_cap;
+      for (int j = jlo + tid; j < jhi; j += kMain) {
+        int par = best, pk = 0;
+        if (j > 0) {
+          par = upper_bound_d(cum, n, __dmul_rn(cu[j - jlo], total));
+          pk = cp[j - jlo];
+        }
+        if (g == probe_g) MUT_MARK(12);
+        const int slot = (pk & 0xff) - 1;
+        // all columns loaded before any store: one round trip per child
+        Factors<NSP, NRED> F;
+        load_factors_cg<NSP, NRED>(pop, n, par, F);
+        uint64_t id_j = pid[par];
+        int c_from = -1, c_to = -1;
+        uint32_t v_from = 0, v_to = 0;
+        if (slot == n_axes) {  // the unroll digit
+          const int uidx = pk >> 8;
+          int uold = 0;
+          for (int u = 0; u < S.n_unroll; ++u)
+            if (tab.unroll[u] == F.unroll) uold = u;
+          id_j += (uint64_t)uidx - (uint64_t)uold;
+          F.unroll = tab.unroll[uidx];
+        } else if (slot >= 0) {  // a prime moved between two positions of the slot
+          const int c0 = slot_col0(S, slot), arity = tab.arity[slot];
+          uint32_t f[4] = {1u, 1u, 1u, 1u};
+          load_slot(pop, n, c0, arity, par, f);
+          int from = 0, tsel = 0;
+          int32_t prime = 1;
+          pick_move(tab, s_t0[slot], s_np[slot], f, arity, (pk >> 8) & 0xffff, &from, &prime, &tsel);
+          int to = pk >> 24;
+          if (to >= from) ++to;
+          int e[4];
+          exps_of(tab, tsel, f, arity, e);
+          const int d_old = rank_composition_cf(tab.e[tsel], arity, e);
+          e[from] -= 1, e[to] += 1;
+          const int d_new = rank_composition_cf(tab.e[tsel], arity, e);
+          id_j += (uint64_t)(int64_t)(d_new - d_old) * s_w[tsel];
+          c_from = c0 + from, c_to = c0 + to;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q == from) v_from = f[q];
+            if (q == to) v_to = f[q];
+          }
+          v_from /= (uint32_t)prime, v_to *= (uint32_t)prime;
+        }
+        if (g == probe_g) MUT_MARK(8);
+#pragma unroll
+        for (int q = 0; q < kN; ++q) F.f[q] = q == c_from ? (int32_t)v_from : q == c_to ? (int32_t)v_to : F.f[q];
+        if (g == probe_g) MUT_MARK(5);
+        const double c_j = draft_cost_of<NSP, NRED>(S, D, F, toggles);
+        if (g == probe_g && c_j > 0) MUT_MARK(6);
+        emit<NSP, NRED>(n, cur, j, F, c_j, id_j, true);
+      }
+      if (g == probe_g) MUT_MARK(4);
+    }
+    if (g == probe_g) MUT_MARK(10);
+    cluster.sync();  // generation g complete in every CTA before anyone reads it
+    if (g == probe_g) MUT_MARK(11);
+  }
+  // the last generation (every earlier one was published by warp 15)
+  __syncthreads();
+  if (tid >= kWork) publish_slice(h, gen_dev(dv, n_steps - 1, n), n_steps - 1, n, jlo, jhi, flags + (n_steps - 1) * nc + cr);
+  if (cr == 0 && tid < 26 && probe_g < n_steps) g_clk_mut[tid] = s_clk[tid];
+  if (tid == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    g_mut_ns[2] = t - ns0, g_mut_ns[3] = (unsigned long long)(clock64() - ck0);
   }
 }
 
 }  // namespace
 
 size_t mutate_smem_bytes(int64_t n, int cols, bool staged) {
-  return (size_t)n * 16 + (size_t)kSegs * 10 * 4 + (staged ? (size_t)n * (8 + 4 * (size_t)cols) : 0) + 16;
+  return (size_t)n * 16 + (size_t)kSegs * 10 * 4 + (size_t)explore_per_cap(n) * 24 +
+         (staged ? (size_t)n * (8 + 4 * (size_t)cols) : 0) + 16;
 }
 constexpr size_t kSmemCap = 220 * 1024;
 
@@ -476,10 +599,14 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
   return rc ? rc : (err != cudaSuccess ? 2 : 0);
 }
 
-int explore_cluster_size(int64_t n) { return (int)std::min<int64_t>(8, std::max<int64_t>(1, (n + 63) / 64)); }
+int explore_cluster_size(int64_t n) { return cluster_of(n); }
 
 }  // namespace tt
 
 extern "C" int ttdbg_mutate_clocks(long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, tt::g_clk_mut, sizeof(long long) * (n < 8 ? n : 8));
+  return (int)cudaMemcpyFromSymbol(out, tt::g_clk_mut, sizeof(long long) * (n < 26 ? n : 26));
 }
+extern "C" int ttdbg_mutate_ns(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, tt::g_mut_ns, sizeof(unsigned long long) * 4);
+}
+extern "C" int ttdbg_mutate_probe(int g) { return (int)cudaMemcpyToSymbol(tt::g_mut_gen, &g, sizeof(int)); }

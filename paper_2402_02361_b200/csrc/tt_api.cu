@@ -5,6 +5,8 @@
 #include <nccl.h>  // types only: the library is dlopen()ed by tt_comm_init
 
 #include <algorithm>
+#include <chrono>
+#include <limits>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -87,6 +89,13 @@ struct tt_ctx {
   std::vector<cudaEvent_t> ex_ev;  // one per generation in flight
   void* d_mix = nullptr;           // random-mix schedules of a draft set: soa | cost | identity
   size_t mix_cap = 0;
+  void* h_mix = nullptr;  // pinned: the mix's costs | identities
+  size_t h_mix_cap = 0;
+  // tt_tuner_round: the draft set on the device (identities | costs | scores)
+  // and its pinned host image (identities | costs | picks | pick scores)
+  void* d_tr = nullptr;
+  void* h_tr = nullptr;
+  int64_t tr_cap = 0;
   // rounds in flight: each enqueued round copies its record into its own
   // pinned ring slot and records its own event, so a caller can keep up to
   // kRing rounds in flight and collect them in order (a 17th enqueue fails
@@ -610,6 +619,9 @@ void tt_ctx_destroy(tt_ctx* c) {
   if (c->h_ex) cudaFreeHost(c->h_ex);
   if (c->h_ring) cudaFreeHost(c->h_ring);
   if (c->h_loss) cudaFreeHost(c->h_loss);
+  if (c->h_mix) cudaFreeHost(c->h_mix);
+  if (c->h_tr) cudaFreeHost(c->h_tr);
+  if (c->d_tr) cudaFree(c->d_tr);
   for (cudaEvent_t e : c->ex_ev) cudaEventDestroy(e);
   graphs_clear(c);
   if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
@@ -1802,9 +1814,21 @@ void mutate_h(const DevSketch& S, const tt_sketch* sk, const int32_t* pop, const
 
 }  // namespace
 
+namespace {
+double g_ex_stamp[8];  // host timeline of the last tt_explore (ttdbg_explore_stamps), microseconds
+inline double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+extern "C" int ttdbg_explore_stamps(double* out) {
+  for (int i = 0; i < 8; ++i) out[i] = g_ex_stamp[i] - g_ex_stamp[0];
+  return 0;
+}
+
 int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t k, int64_t n,
                uint64_t seed, int toggles, int32_t* soa_host, double* cost_host, uint64_t* id_host,
                int64_t* count_host, uint64_t* evaluations) {
+  g_ex_stamp[0] = now_us();
   if (!ctx) return TT_E_STATE;
   if (n_steps < 1) return fail(ctx, TT_E_STATE, "explore: n_steps must be >= 1");
   if (k < 1) return fail(ctx, TT_E_STATE, "explore: draft_size must be >= 1");
@@ -1880,8 +1904,14 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   auto by_cost = [](const PE& a, const PE& b) { return a.cost != b.cost ? a.cost < b.cost : a.disc < b.disc; };
   // pool insertion in population order (first discovery wins,
   // draft.cpp:198-204) + trim to the k smallest (cost, discovery) (:174-191)
+  // Once the pool is full, an entry whose cost is >= the worst kept cost
+  // can never survive a trim (k kept entries precede it in (cost, discovery)
+  // order: its discovery is later), so it is skipped before the membership
+  // probe. Discovery numbers then have gaps, which keeps their order.
+  double bar = std::numeric_limits<double>::infinity();
   auto consume = [&](const GenSlot& g, int gen) {
     for (int64_t i = 0; i < n; ++i) {
+      if (!(g.cost[i] < bar)) continue;
       if (!h_insert(g.id[i])) continue;
       PE e{g.cost[i], discovery++, g.id[i], 0};
       if (on_device) {
@@ -1905,6 +1935,10 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
       }
       if (!on_device) std::copy(rows_t.begin(), rows_t.begin() + (size_t)k * cols, rows.begin());
     }
+    if ((int64_t)pool.size() == k) {
+      bar = pool[0].cost;
+      for (const PE& e : pool) bar = e.cost > bar ? e.cost : bar;
+    }
   };
 
   if (on_device) {
@@ -1912,6 +1946,7 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
     // cost) and publishes each to its pinned slot + flag; the host folds
     // generation g into the pool as soon as its flag is up
     for (int g = 0; g < n_steps * nflag; ++g) h_flags[g] = 0u;
+    g_ex_stamp[1] = now_us();
     const size_t cost_off = (size_t)((char*)hgen(0).cost - (char*)ctx->h_ex);
     const int lrc = launch_explore_gens(S, D, toggles, n, n_steps, ctx->d_ex, gen_bytes(n, cols), cost_off, s_init,
                                         ctx->h_ex, gen_bytes(n, cols), cost_off, h_flags, st);
@@ -1919,7 +1954,10 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
                                                   cudaGetErrorString(cudaGetLastError()));
     if (lrc) return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
+    g_ex_stamp[2] = now_us();
     for (int g = 0; g < n_steps; ++g) {
+      if (g == 1) g_ex_stamp[3] = now_us();
+      if (g == n_steps - 1) g_ex_stamp[4] = now_us();
       for (int f = g * nflag; f < (g + 1) * nflag; ++f)
       for (uint64_t spin = 0; h_flags[f] == 0u; ++spin) {
         if ((spin & 1023) == 1023) {  // a faulted or finished kernel never raises the flag
@@ -1931,9 +1969,11 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
         }
       }
       std::atomic_thread_fence(std::memory_order_acquire);
+      if (g == n_steps - 1) g_ex_stamp[5] = now_us();
       consume(hgen(g), g);
     }
     if ((rc = sync_check(ctx))) return rc;
+    g_ex_stamp[6] = now_us();
     // factor columns stay in the device slots; fetched only when asked for
     if (soa_host) {
       TT_CUDA(ctx, cudaMemcpyAsync(ctx->h_ex, ctx->d_ex, (size_t)n_steps * gen_bytes(n, cols), cudaMemcpyDeviceToHost,
@@ -1983,6 +2023,7 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
   }
   *count_host = cnt;
   if (evaluations) *evaluations = (uint64_t)n_steps * (uint64_t)n;
+  g_ex_stamp[7] = now_us();
   return TT_OK;
 }
 
@@ -2000,9 +2041,11 @@ int tt_draft_set(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, in
   const int64_t n_spec = std::max<int64_t>(1, std::llround((1.0 - random_mix) * (double)draft_size));
   const int64_t n_random = draft_size - n_spec;
   int64_t cnt = 0;
-  int rc = tt_explore(ctx, sk, dev, n_steps, n_spec, pop_size, explore_seed, toggles, nullptr, cost_host, id_host,
-                      &cnt, evaluations);
-  if (rc) return rc;
+  int rc = TT_OK;
+  // the random mix does not depend on the explore: it is generated and costed
+  // on the side stream while the GA cluster kernel runs (8 SMs of 148)
+  double* mc = nullptr;
+  uint64_t* mi = nullptr;
   if (n_random > 0) {
     DevSketch S;
     DevDevice D;
@@ -2015,26 +2058,102 @@ int tt_draft_set(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, in
       TT_CUDA(ctx, cudaMalloc(&ctx->d_mix, want));
       ctx->mix_cap = want;
     }
+    const size_t hwant = (size_t)n_random * 16;
+    if (hwant > ctx->h_mix_cap) {
+      cudaFreeHost(ctx->h_mix);
+      ctx->h_mix = nullptr, ctx->h_mix_cap = 0;
+      TT_CUDA(ctx, cudaHostAlloc(&ctx->h_mix, hwant, cudaHostAllocDefault));
+      ctx->h_mix_cap = hwant;
+    }
+    mc = (double*)ctx->h_mix, mi = (uint64_t*)(mc + n_random);
     GenSlot m = gen_slot(ctx->d_mix, n_random, S.cols, 0);
-    if (launch_generate(S, seed_state(mix_seed), 0, n_random, m.soa, n_random, m.id, ctx->stream))
+    TT_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+    TT_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    if (launch_generate(S, seed_state(mix_seed), 0, n_random, m.soa, n_random, m.id, ctx->side))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
     if (launch_draft_cost(S, D, m.soa, n_random, 0, 0, false, n_random, toggles, m.cost, nullptr, ctx->sel.invalid,
-                          ctx->stream))
+                          ctx->side))
       return fail(ctx, TT_E_VALIDATE, "unsupported op shape");
     TT_LAUNCHED(ctx);
-    std::vector<double> mc((size_t)n_random);
-    std::vector<uint64_t> mi((size_t)n_random);
-    TT_CUDA(ctx, cudaMemcpyAsync(mc.data(), m.cost, sizeof(double) * n_random, cudaMemcpyDeviceToHost, ctx->stream));
-    TT_CUDA(ctx, cudaMemcpyAsync(mi.data(), m.id, sizeof(uint64_t) * n_random, cudaMemcpyDeviceToHost, ctx->stream));
-    if ((rc = sync_check(ctx))) return rc;
-    std::unordered_map<uint64_t, int> seen;
-    seen.reserve((size_t)(cnt + n_random) * 2);
-    for (int64_t i = 0; i < cnt; ++i) seen.emplace(id_host[i], 0);
-    for (int64_t i = 0; i < n_random; ++i)
-      if (seen.emplace(mi[(size_t)i], 0).second) id_host[cnt] = mi[(size_t)i], cost_host[cnt++] = mc[(size_t)i];
+    TT_CUDA(ctx, cudaMemcpyAsync(mc, m.cost, sizeof(double) * n_random, cudaMemcpyDeviceToHost, ctx->side));
+    TT_CUDA(ctx, cudaMemcpyAsync(mi, m.id, sizeof(uint64_t) * n_random, cudaMemcpyDeviceToHost, ctx->side));
   }
+  rc = tt_explore(ctx, sk, dev, n_steps, n_spec, pop_size, explore_seed, toggles, nullptr, cost_host, id_host, &cnt,
+                  evaluations);
+  if (n_random > 0) {
+    const cudaError_t e = cudaStreamSynchronize(ctx->side);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(ctx, TT_E_CUDA, cudaGetErrorString(e));
+    // membership: open addressing over the identities (insertion order kept)
+    int hb = 4;
+    while (((int64_t)1 << hb) < 2 * (cnt + n_random)) ++hb;
+    const uint64_t hm = ((uint64_t)1 << hb) - 1;
+    std::vector<uint64_t> key((size_t)hm + 1);
+    std::vector<uint8_t> used((size_t)hm + 1, 0);
+    auto insert = [&](uint64_t id) {
+      for (uint64_t q = scramble64(id) & hm;; q = (q + 1) & hm) {
+        if (!used[q]) return used[q] = 1, key[q] = id, true;
+        if (key[q] == id) return false;
+      }
+    };
+    for (int64_t i = 0; i < cnt; ++i) insert(id_host[i]);
+    for (int64_t i = 0; i < n_random; ++i)
+      if (insert(mi[i])) id_host[cnt] = mi[i], cost_host[cnt++] = mc[i];
+  }
+  if (rc) return rc;
   *count_host = cnt;
+  return TT_OK;
+}
+
+int tt_tuner_round(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t draft_size,
+                   int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int64_t b,
+                   int precision, int64_t* sel_idx, double* sel_scores, int64_t* n_candidates) {
+  if (!ctx) return TT_E_STATE;
+  if (!sel_idx || !n_candidates) return fail(ctx, TT_E_STATE, "tuner_round: null output");
+  if (b < 1) return fail(ctx, TT_E_STATE, "select_top: b must be >= 1");
+  if (draft_size < 1) return fail(ctx, TT_E_CONFIG, "draft_size must be >= 1");
+  if (!ctx->d_params) return fail(ctx, TT_E_STATE, "score: tt_pacm_load first");
+  int rc = TT_OK;
+  if (draft_size > ctx->tr_cap) {
+    cudaFree(ctx->d_tr), cudaFreeHost(ctx->h_tr);
+    ctx->d_tr = ctx->h_tr = nullptr, ctx->tr_cap = 0;
+    TT_CUDA(ctx, cudaMalloc(&ctx->d_tr, (size_t)draft_size * 24));
+    TT_CUDA(ctx, cudaHostAlloc(&ctx->h_tr, (size_t)draft_size * 32 + 64, cudaHostAllocDefault));
+    ctx->tr_cap = draft_size;
+  }
+  if ((rc = ensure_b(ctx, b))) return rc;
+  uint64_t* d_id = (uint64_t*)ctx->d_tr;
+  double* d_cost = (double*)(d_id + draft_size);
+  double* d_score = d_cost + draft_size;
+  uint64_t* h_id = (uint64_t*)ctx->h_tr;
+  double* h_cost = (double*)(h_id + draft_size);
+  double* h_score = h_cost + draft_size;  // the whole set's scores (sel_scores is gathered from it)
+  int64_t* h_pos = (int64_t*)(h_score + draft_size);
+  int* h_status = (int*)(h_pos + b);
+  int64_t cnt = 0;
+  if ((rc = tt_draft_set(ctx, sk, dev, n_steps, draft_size, pop_size, random_mix, explore_seed, mix_seed,
+                         TT_TOGGLES_ALL, h_id, h_cost, &cnt, nullptr)))
+    return rc;
+  cudaStream_t st = ctx->stream;
+  TT_CUDA(ctx, cudaMemcpyAsync(d_id, h_id, sizeof(uint64_t) * cnt, cudaMemcpyHostToDevice, st));
+  TT_CUDA(ctx, cudaMemcpyAsync(d_cost, h_cost, sizeof(double) * cnt, cudaMemcpyHostToDevice, st));
+  if ((rc = tt_pacm_score(ctx, sk, dev, d_id, cnt, precision, d_score))) return rc;
+  if (launch_select_top(d_score, d_cost, nullptr, cnt, nullptr, b, ctx->d_pos, ctx->d_pos_count, ctx->d_status, st))
+    return fail(ctx, TT_E_STATE, "select_top: n too large for b (tiles * b must be <= 4096)");
+  TT_LAUNCHED(ctx);
+  TT_CUDA(ctx, cudaMemcpyAsync(h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TT_CUDA(ctx, cudaMemcpyAsync(h_pos, ctx->d_pos, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
+  if (sel_scores) TT_CUDA(ctx, cudaMemcpyAsync(h_score, d_score, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+  if ((rc = sync_check(ctx))) return rc;
+  *n_candidates = cnt;
+  if (*h_status)
+    return fail(ctx, TT_E_STATE, "select_top: requested " + std::to_string(b) + " but only " + std::to_string(cnt) +
+                                     " candidates in the draft set");
+  for (int64_t i = 0; i < b; ++i) {
+    sel_idx[i] = h_pos[i];
+    if (sel_scores) sel_scores[i] = h_score[h_pos[i]];
+  }
   return TT_OK;
 }
 

@@ -30,7 +30,7 @@ from ._capi import TTError, RoundConfig, RoundResult, TT_BF16_BAND, TT_PREC_BF16
 from .types import DeviceSpec, OpSpec, OracleSpec, Sketch, TT_TOGGLES_ALL
 
 __all__ = ["Context", "TTError", "TT_PREC_FP64", "TT_PREC_BF16", "random_init", "draft_cost", "draft_topk",
-           "explore1", "topk_merge", "schedule_identity", "schedule_from_identity", "extract_features",
+           "explore1", "explore", "draft_set", "tuner_round", "topk_merge", "schedule_identity", "schedule_from_identity", "extract_features",
            "extract_features_soa", "PaCM", "select_top", "gd_step", "momentum_update", "draft_verify_round",
            "init_params", "param_count", "generate_sketch", "forward_calls", "reset_forward_calls",
            "oracle_latency", "oracle_measure", "oracle_best", "train", "momentum_adapt"]
@@ -194,6 +194,21 @@ def draft_set(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft
                                  cost.ctypes.data, C.byref(cnt), C.byref(ev)))
     m = cnt.value
     return ids[:m], cost[:m], ev.value
+
+
+def tuner_round(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, draft_size: int, pop_size: int,
+                random_mix: float, explore_seed: int, mix_seed: int, b: int, precision: int = TT_PREC_FP64):
+    """One tuner round (tuner.cpp:294-396): the draft set, features + PaCM
+    scores on the device, select_top(b). Needs a loaded PaCM (PaCM(ctx, ...)).
+    Returns (picked indices into the draft set int64 [b], their scores
+    float64 [b], draft-set size)."""
+    sel = np.zeros(b, np.int64)
+    sc = np.zeros(b, np.float64)
+    cnt = C.c_int64(0)
+    ctx.check(lib().tt_tuner_round(ctx.h, C.byref(sketch), C.byref(dev), n_steps, draft_size, pop_size, random_mix,
+                                   explore_seed & (2**64 - 1), mix_seed & (2**64 - 1), b, precision,
+                                   sel.ctypes.data, sc.ctypes.data, C.byref(cnt)))
+    return sel, sc, cnt.value
 
 
 def topk_merge(ctx: Context, cost: torch.Tensor, gidx: torch.Tensor, ids: torch.Tensor, k: int):
