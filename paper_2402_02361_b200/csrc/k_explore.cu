@@ -50,6 +50,13 @@ constexpr int kMaxCols = 4 * 4 + 3 * 3 + 1;  // 4 spatial x 4 + 3 reduction x 3 
 // of generation g_mut_gen (ttdbg_mutate_probe)
 __device__ long long g_clk_mut[26];
 __device__ int g_mut_gen = 1;
+// debugging: when set (ttdbg_explore_watch), lane 0 of every warp writes
+// (generation << 8 | phase) to its word of this mapped host array as it goes
+__device__ unsigned* g_mut_prog = nullptr;
+#define MUT_PROG(ph)                                                          \
+  do {                                                                        \
+    if (prog && (tid & 31) == 0) *(volatile unsigned*)(prog + cr * 16 + (tid >> 5)) = (unsigned)(g << 8 | (ph)); \
+  } while (0)
 __device__ unsigned long long g_mut_ns[4];  // globaltimer at kernel start / generation 1 start / loop end; clock64 span
 #define MUT_MARK_T(i, t)                                            \
   do {                                                              \
@@ -89,13 +96,17 @@ struct PrimeTab {
   int32_t len[TT_MAX_AXES + 1];  // draws a child consumes by slot
 };
 
+// f[q] without a dynamic register index (the loops over positions stay loops)
+__device__ __forceinline__ uint32_t sel4(const uint32_t (&f)[4], int q) {
+  return q == 0 ? f[0] : q == 1 ? f[1] : q == 2 ? f[2] : f[3];
+}
+
 __device__ __forceinline__ void pick_move(const PrimeTab& S, int t0, int np, const uint32_t (&f)[4], int arity,
                                           int m, int* pos, int32_t* prime, int* tsel) {
   int cnt = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (q >= arity) break;
-    uint32_t v = f[q];
+#pragma unroll 1
+  for (int q = 0; q < arity; ++q) {
+    uint32_t v = sel4(f, q);
     for (int t = t0; t < t0 + np && v > 1; ++t) {
       int e = 0;
       if (S.p[t] == 2) {
@@ -115,6 +126,14 @@ __device__ __forceinline__ void pick_move(const PrimeTab& S, int t0, int np, con
 
 __device__ __forceinline__ void named_barrier(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void named_barrier_arrive(int id, int threads) {
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// the non-.aligned form: lanes of one warp may reach it from different code
+// (a child loop whose trip count differs across the warp's lanes)
+__device__ __forceinline__ void named_barrier_divergent(int id, int threads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // the arity factors of `slot` of population member `par` (SoA, ld n)
@@ -138,16 +157,15 @@ __device__ __forceinline__ void load_factors_cg(const int32_t* soa, int n, int i
 
 // exponents of prime table entry t in the arity factors f
 __device__ __forceinline__ void exps_of(const PrimeTab& S, int t, const uint32_t (&f)[4], int arity, int (&e)[4]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t v = f[q];
+  e[0] = e[1] = e[2] = e[3] = 0;
+#pragma unroll 1
+  for (int q = 0; q < arity; ++q) {
+    uint32_t v = sel4(f, q);
     int x = 0;
-    if (q < arity) {
-      if (S.p[t] == 2) {
-        x = __ffs(v) - 1;
-      } else {
-        for (uint32_t qv = v * S.inv[t]; qv <= S.lim[t]; qv = v * S.inv[t]) v = qv, ++x;
-      }
+    if (S.p[t] == 2) {
+      x = __ffs(v) - 1;
+    } else {
+      for (uint32_t qv = v * S.inv[t]; qv <= S.lim[t]; qv = v * S.inv[t]) v = qv, ++x;
     }
     e[q] = x;
   }
@@ -254,12 +272,15 @@ constexpr uint64_t kMapIdentity = (uint64_t)1 << 30 | (uint64_t)2 << 46 | (uint6
 template <int NSP, int NRED>
 __global__ void __launch_bounds__(kMutThreads, 1)
     k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenOut dv, uint64_t s_init, GenOut h,
-                   volatile uint32_t* flags, int staged) {
+                   volatile uint32_t* flags, int mode) {
   constexpr int kN = Factors<NSP, NRED>::kN;
   extern __shared__ __align__(16) unsigned char smem[];
   const int per_cap = explore_per_cap(n);
-  double* cum = (double*)smem;                          // [n] weights, then their running sums
-  double* ch_u = cum + n;                               // [2][per_cap] roulette uniform of child jlo + c
+  const bool staged = (mode & 1) != 0, spec = (mode & 2) != 0;
+  double* cum = (double*)smem;                          // [n] the wheel: running sums in the reference's order
+  double* wts = spec ? cum + n : cum;                   // [n] weights (in place without speculation)
+  double* cum_sp = spec ? wts + n : nullptr;            // [n] the approximate wheel (parallel scan)
+  double* ch_u = cum + (spec ? 3 : 1) * (size_t)n;      // [2][per_cap] roulette uniform of child jlo + c
   int32_t* ch_p = (int32_t*)(ch_u + 2 * per_cap);       // [2][per_cap] slot + 1 | move / unroll draws
   int32_t* off = ch_p + 2 * per_cap;                    // [n] stream offset of child j
   int32_t* seg_exit = off + n;                          // [kSegs][4]
@@ -271,7 +292,8 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   // at random by the apply pass, so they come from shared memory
   uint64_t* id_s = (uint64_t*)(len + 4 * (size_t)n);    // [n] (4n is a multiple of 8)
   int32_t* pop_s = (int32_t*)(id_s + n);                // [cols][n]
-  __shared__ double s_total;
+  __shared__ double s_total, s_total_sp;
+  __shared__ int s_best;
   __shared__ int s_t0[TT_MAX_AXES], s_np[TT_MAX_AXES], s_omega[TT_MAX_AXES];
   __shared__ uint64_t s_w[TT_MAX_PRIMES];  // identity weight of each (axis, prime) digit
   __shared__ PrimeTab tab;
@@ -281,6 +303,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   const int tid = threadIdx.x;
   const int n_axes = S.n_axes;
   const int probe_g = g_mut_gen;
+  unsigned* const prog = g_mut_prog;
   unsigned long long ns0 = 0;
   long long ck0 = 0;
   if (tid == 0 && blockIdx.x == 0) {
@@ -415,6 +438,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
   for (int g = 1; g < n_steps; ++g) {
     const GenDev prev = gen_dev(dv, g - 1, n);
     if (g == probe_g) MUT_MARK(0);
+    MUT_PROG(1);
     if (tid >= kWork) {
       // warp 15 publishes the previous generation (this CTA's slice) to the
       // host while the others build this one: the system fence waits for the
@@ -432,7 +456,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
       int bi = n;
       for (int i = tid; i < n; i += kMain) {
         const double c = prev.cost[i];
-        cum[i] = 1.0 / __dadd_rn(c, 1e-12);
+        wts[i] = 1.0 / __dadd_rn(c, 1e-12);
         if (c < bc) bc = c, bi = i;
       }
       for (int o = 16; o; o >>= 1) {
@@ -442,110 +466,161 @@ __global__ void __launch_bounds__(kMutThreads, 1)
       }
       if ((tid & 31) == 0) s_bc[tid >> 5] = bc, s_bi[tid >> 5] = bi;
       if (g == probe_g) MUT_MARK(14);
+      MUT_PROG(2);
       named_barrier(2, kMain);
-      // B. warp 0: the elite, then the running total in the reference's
-      // order (one dependent DADD chain, operands staged through registers);
-      // warps 1..6 stage the parents into shared memory meanwhile
+      MUT_PROG(3);
+      // B. warp 0: the running total in the reference's order — one
+      // dependent DADD chain (~12 cycles a step) — then it releases barrier 4.
+      // The children do not wait for it: warp 6 builds an approximate wheel
+      // (a parallel scan: the same sums in another order, a few ulps off),
+      // warps 1..5 stage the parents, and warps 1..6 build every child from
+      // the parent the approximate wheel picks. Once the exact wheel is out
+      // each child checks its draw against it and is rebuilt in the rare
+      // case the draw fell between the two wheels' bounds.
       if (tid < 32) {
-        bc = tid < kMain / 32 ? s_bc[tid] : __longlong_as_double(0x7ff0000000000000LL);
-        bi = tid < kMain / 32 ? s_bi[tid] : n;
-        for (int o = 16; o; o >>= 1) {
-          const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
-        }
         if (tid == 0) {
-          s_bi[0] = bi;
           double t = 0.0;
           int i = 0;
           for (; i + 16 <= n; i += 16) {
             double w[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) w[q] = cum[i + q];
+            for (int q = 0; q < 16; ++q) w[q] = wts[i + q];
 #pragma unroll
             for (int q = 0; q < 16; ++q) t = __dadd_rn(t, w[q]), w[q] = t;
 #pragma unroll
             for (int q = 0; q < 16; ++q) cum[i + q] = w[q];
           }
-          for (; i < n; ++i) t = __dadd_rn(t, cum[i]), cum[i] = t;
+          for (; i < n; ++i) t = __dadd_rn(t, wts[i]), cum[i] = t;
           s_total = t;
           if (g == probe_g) MUT_MARK(22);
         }
-      } else if (staged) {
-        // async copies, all in flight at once, no register staging; every
-        // generation has its own device slot, so no stale L1 line can hit
-        const int nt = kMain - 32, t = tid - 32;
-        const uint32_t sp = (uint32_t)__cvta_generic_to_shared(pop_s);
-        const uint32_t si = (uint32_t)__cvta_generic_to_shared(id_s);
-        for (int i = t; i < (kN + 1) * n; i += nt)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sp + 4u * i), "l"(prev.soa + i) : "memory");
-        for (int i = t; i < n; i += nt)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(si + 8u * i), "l"(prev.id + i) : "memory");
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        if (g == probe_g) MUT_MARK_T(21, 32);
-      }
-      named_barrier(2, kMain);
-      if (g == probe_g) MUT_MARK(3);
-      // D. children: elite at 0 (schedule.cpp:368), the rest from their draws
-      const double total = s_total;
-      const int best = s_bi[0];
-      const double* cu = ch_u + (g & 1) * per_cap;
-      const int32_t* cp = ch_p + (g & 1) * per_cap;
-      for (int j = jlo + tid; j < jhi; j += kMain) {
-        int par = best, pk = 0;
-        if (j > 0) {
-          par = upper_bound_d(cum, n, __dmul_rn(cu[j - jlo], total));
-          pk = cp[j - jlo];
-        }
-        if (g == probe_g) MUT_MARK(12);
-        const int slot = (pk & 0xff) - 1;
-        // all columns loaded before any store: one round trip per child
-        Factors<NSP, NRED> F;
-        load_factors_cg<NSP, NRED>(pop, n, par, F);
-        uint64_t id_j = pid[par];
-        int c_from = -1, c_to = -1;
-        uint32_t v_from = 0, v_to = 0;
-        if (slot == n_axes) {  // the unroll digit
-          const int uidx = pk >> 8;
-          int uold = 0;
-          for (int u = 0; u < S.n_unroll; ++u)
-            if (tab.unroll[u] == F.unroll) uold = u;
-          id_j += (uint64_t)uidx - (uint64_t)uold;
-          F.unroll = tab.unroll[uidx];
-        } else if (slot >= 0) {  // a prime moved between two positions of the slot
-          const int c0 = slot_col0(S, slot), arity = tab.arity[slot];
-          uint32_t f[4] = {1u, 1u, 1u, 1u};
-          load_slot(pop, n, c0, arity, par, f);
-          int from = 0, tsel = 0;
-          int32_t prime = 1;
-          pick_move(tab, s_t0[slot], s_np[slot], f, arity, (pk >> 8) & 0xffff, &from, &prime, &tsel);
-          int to = pk >> 24;
-          if (to >= from) ++to;
-          int e[4];
-          exps_of(tab, tsel, f, arity, e);
-          const int d_old = rank_composition_cf(tab.e[tsel], arity, e);
-          e[from] -= 1, e[to] += 1;
-          const int d_new = rank_composition_cf(tab.e[tsel], arity, e);
-          id_j += (uint64_t)(int64_t)(d_new - d_old) * s_w[tsel];
-          c_from = c0 + from, c_to = c0 + to;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q == from) v_from = f[q];
-            if (q == to) v_to = f[q];
+        __syncwarp();
+        named_barrier_arrive(4, kMain);
+      } else {
+        if (tid >= kMain - 32) {  // warp 6: the elite and the approximate wheel
+          const int l = tid & 31;
+          bc = l < kMain / 32 ? s_bc[l] : __longlong_as_double(0x7ff0000000000000LL);
+          bi = l < kMain / 32 ? s_bi[l] : n;
+          for (int o = 16; o; o >>= 1) {
+            const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oc < bc || (oc == bc && oi < bi)) bc = oc, bi = oi;
           }
-          v_from /= (uint32_t)prime, v_to *= (uint32_t)prime;
-        }
-        if (g == probe_g) MUT_MARK(8);
+          if (spec) {
+            const int ch = (n + 31) >> 5, i0 = min(n, l * ch), i1 = min(n, i0 + ch);
+            double t = 0.0;
+            for (int i = i0; i < i1; ++i) t += wts[i];
+            double incl = t;
 #pragma unroll
-        for (int q = 0; q < kN; ++q) F.f[q] = q == c_from ? (int32_t)v_from : q == c_to ? (int32_t)v_to : F.f[q];
-        if (g == probe_g) MUT_MARK(5);
-        const double c_j = draft_cost_of<NSP, NRED>(S, D, F, toggles);
-        if (g == probe_g && c_j > 0) MUT_MARK(6);
-        emit<NSP, NRED>(n, cur, j, F, c_j, id_j, true);
+            for (int d = 1; d < 32; d <<= 1) {
+              const double o = __shfl_up_sync(0xffffffffu, incl, d);
+              if (l >= d) incl += o;
+            }
+            t = incl - t;  // exclusive prefix
+            for (int i = i0; i < i1; ++i) t += wts[i], cum_sp[i] = t;
+            if (l == 31) s_total_sp = incl;
+          }
+          if (l == 0) s_best = bi;
+        } else if (staged) {  // warps 1..5: the parents into shared memory
+          // async copies, all in flight at once, no register staging; every
+          // generation has its own device slot, so no stale L1 line can hit
+          const int nt = kMain - 64, t = tid - 32;
+          const uint32_t sp = (uint32_t)__cvta_generic_to_shared(pop_s);
+          const uint32_t si = (uint32_t)__cvta_generic_to_shared(id_s);
+          for (int i = t; i < (kN + 1) * n; i += nt)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sp + 4u * i), "l"(prev.soa + i) : "memory");
+          for (int i = t; i < n; i += nt)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(si + 8u * i), "l"(prev.id + i) : "memory");
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          if (g == probe_g) MUT_MARK_T(21, 32);
+        }
+        MUT_PROG(4);
+        named_barrier(5, kMain - 32);
+        MUT_PROG(5);
+        if (g == probe_g) MUT_MARK_T(3, 32);
+        // D. children: elite at 0 (schedule.cpp:368), the rest from their draws
+        const double* cu = ch_u + (g & 1) * per_cap;
+        const int32_t* cpk = ch_p + (g & 1) * per_cap;
+        const int best = s_best;
+        // child j from parent par (factors, identity, draft cost)
+        auto build = [&](int j, int par, Factors<NSP, NRED>& F, uint64_t& id_j) -> double {
+          const int pk = j > 0 ? cpk[j - jlo] : 0;
+          const int slot = (pk & 0xff) - 1;
+          // all columns loaded before any store: one round trip per child
+          load_factors_cg<NSP, NRED>(pop, n, par, F);
+          id_j = pid[par];
+          int c_from = -1, c_to = -1;
+          uint32_t v_from = 0, v_to = 0;
+          if (slot == n_axes) {  // the unroll digit
+            const int uidx = pk >> 8;
+            int uold = 0;
+#pragma unroll 1
+            for (int u = 0; u < S.n_unroll; ++u)
+              if (tab.unroll[u] == F.unroll) uold = u;
+            id_j += (uint64_t)uidx - (uint64_t)uold;
+            F.unroll = tab.unroll[uidx];
+          } else if (slot >= 0) {  // a prime moved between two positions of the slot
+            const int c0 = slot_col0(S, slot), arity = tab.arity[slot];
+            uint32_t f[4] = {1u, 1u, 1u, 1u};
+            load_slot(pop, n, c0, arity, par, f);
+            int from = 0, tsel = 0;
+            int32_t prime = 1;
+            pick_move(tab, s_t0[slot], s_np[slot], f, arity, (pk >> 8) & 0xffff, &from, &prime, &tsel);
+            int to = pk >> 24;
+            if (to >= from) ++to;
+            int e[4];
+            exps_of(tab, tsel, f, arity, e);
+            const int d_old = rank_composition_cf(tab.e[tsel], arity, e);
+            e[from] -= 1, e[to] += 1;
+            const int d_new = rank_composition_cf(tab.e[tsel], arity, e);
+            id_j += (uint64_t)(int64_t)(d_new - d_old) * s_w[tsel];
+            c_from = c0 + from, c_to = c0 + to;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q == from) v_from = f[q];
+              if (q == to) v_to = f[q];
+            }
+            v_from /= (uint32_t)prime, v_to *= (uint32_t)prime;
+          }
+#pragma unroll
+          for (int q = 0; q < kN; ++q) F.f[q] = q == c_from ? (int32_t)v_from : q == c_to ? (int32_t)v_to : F.f[q];
+          return draft_cost_of<NSP, NRED, true>(S, D, F, toggles);
+        };
+        bool exact = !spec;  // past barrier 4: the exact wheel is in cum / s_total
+        if (exact) named_barrier(4, kMain);
+        for (int j = jlo + tid - 32; j < jhi; j += kMain - 32) {
+          const double u = j > 0 ? cu[j - jlo] : 0.0;
+          int par = best;
+          if (j > 0) par = exact ? upper_bound_d(cum, n, __dmul_rn(u, s_total))
+                                 : upper_bound_d(cum_sp, n, __dmul_rn(u, s_total_sp));
+          if (g == probe_g) MUT_MARK_T(12, 32);
+          Factors<NSP, NRED> F;
+          uint64_t id_j;
+          double c_j;
+          for (;;) {  // one pass, two when the approximate wheel picked another parent
+            c_j = build(j, par, F, id_j);
+            if (exact) break;
+            if (g == probe_g) MUT_MARK_T(6, 32);
+            MUT_PROG(6);
+            named_barrier_divergent(4, kMain);
+            MUT_PROG(7);
+            exact = true;
+            if (g == probe_g) MUT_MARK_T(8, 32);
+            if (j == 0) break;
+            const double r = __dmul_rn(u, s_total);  // upper_bound_d's answer is par iff
+            if ((par == 0 || cum[par - 1] <= r) && (par == n - 1 || cum[par] > r)) break;
+            par = upper_bound_d(cum, n, r);
+          }
+          emit<NSP, NRED>(n, cur, j, F, c_j, id_j, true);
+        }
+        MUT_PROG(8);
+        if (!exact) named_barrier_divergent(4, kMain);
+        MUT_PROG(9);
+        if (g == probe_g) MUT_MARK_T(4, 32);
       }
-      if (g == probe_g) MUT_MARK(4);
     }
     if (g == probe_g) MUT_MARK(10);
+    MUT_PROG(10);
     cluster.sync();  // generation g complete in every CTA before anyone reads it
     if (g == probe_g) MUT_MARK(11);
   }
@@ -562,8 +637,8 @@ __global__ void __launch_bounds__(kMutThreads, 1)
 
 }  // namespace
 
-size_t mutate_smem_bytes(int64_t n, int cols, bool staged) {
-  return (size_t)n * 16 + (size_t)kSegs * 10 * 4 + (size_t)explore_per_cap(n) * 24 +
+size_t mutate_smem_bytes(int64_t n, int cols, bool staged, bool spec) {
+  return (size_t)n * (spec ? 32 : 16) + (size_t)kSegs * 10 * 4 + (size_t)explore_per_cap(n) * 24 +
          (staged ? (size_t)n * (8 + 4 * (size_t)cols) : 0) + 16;
 }
 constexpr size_t kSmemCap = 220 * 1024;
@@ -574,8 +649,14 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
   if (n < 2 || n > kMutateMaxN) return 1;
   GenOut dv{(char*)dev_base, dev_stride, dev_cost_off};
   GenOut h{(char*)host_base, host_stride, host_cost_off};
-  const bool staged = mutate_smem_bytes(n, S.cols, true) <= kSmemCap;
-  const size_t sm = mutate_smem_bytes(n, S.cols, staged);
+  // staged parents and the speculative wheel when they fit, in that order
+  int mode = 0;
+  for (int m : {3, 1, 2, 0})
+    if (mutate_smem_bytes(n, S.cols, m & 1, m & 2) <= kSmemCap) {
+      mode = m;
+      break;
+    }
+  const size_t sm = mutate_smem_bytes(n, S.cols, mode & 1, mode & 2);
   cudaError_t err = cudaSuccess;
   const int rc = TT_DISPATCH_SHAPE(S.n_sp, S.n_red, ({
     static bool init = false;
@@ -594,7 +675,7 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
     cfg.attrs = at, cfg.numAttrs = 1;
     tt::note_launch();
     err = cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, dv, s_init, h, flags,
-                             (int)staged);
+                             mode);
   }));
   return rc ? rc : (err != cudaSuccess ? 2 : 0);
 }
@@ -608,5 +689,8 @@ extern "C" int ttdbg_mutate_clocks(long long* out, int n) {
 }
 extern "C" int ttdbg_mutate_ns(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, tt::g_mut_ns, sizeof(unsigned long long) * 4);
+}
+extern "C" int ttdbg_mutate_watch(unsigned* mapped) {
+  return (int)cudaMemcpyToSymbol(tt::g_mut_prog, &mapped, sizeof(mapped));
 }
 extern "C" int ttdbg_mutate_probe(int g) { return (int)cudaMemcpyToSymbol(tt::g_mut_gen, &g, sizeof(int)); }

@@ -1816,10 +1816,15 @@ void mutate_h(const DevSketch& S, const tt_sketch* sk, const int32_t* pop, const
 
 namespace {
 double g_ex_stamp[8];  // host timeline of the last tt_explore (ttdbg_explore_stamps), microseconds
+double g_ex_watch_s = 0;  // debugging: give up on a generation flag after this many seconds
 inline double now_us() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 }  // namespace
+extern "C" int ttdbg_explore_watch(double seconds) {
+  g_ex_watch_s = seconds;
+  return 0;
+}
 extern "C" int ttdbg_explore_stamps(double* out) {
   for (int i = 0; i < 8; ++i) out[i] = g_ex_stamp[i] - g_ex_stamp[0];
   return 0;
@@ -1960,6 +1965,9 @@ int tt_explore(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int 
       if (g == n_steps - 1) g_ex_stamp[4] = now_us();
       for (int f = g * nflag; f < (g + 1) * nflag; ++f)
       for (uint64_t spin = 0; h_flags[f] == 0u; ++spin) {
+        if (g_ex_watch_s > 0 && (spin & 0xffff) == 0xffff && now_us() - g_ex_stamp[0] > 1e6 * g_ex_watch_s)
+          return fail(ctx, TT_E_STATE, "explore: generation " + std::to_string(g) + " flag " + std::to_string(f) +
+                                           " not published within the watch limit (kernel stuck)");
         if ((spin & 1023) == 1023) {  // a faulted or finished kernel never raises the flag
           const cudaError_t q = cudaStreamQuery(st);
           if (q != cudaErrorNotReady && h_flags[f] == 0u) {

@@ -28,7 +28,7 @@ for pg in (1, 8, 20, 31):
     c = np.array(clk[:26], dtype=np.int64)
     r = lambda k: int(c[k] - c[0])  # noqa: E731
     print(f"gen {pg}: main: phaseA {r(14)} chain-done {r(22)} staging-done {r(21)} apply {r(3)}..{r(4)} "
-          f"[search {r(12) - r(3)} move {r(8) - r(12)} factors {r(5) - r(8)} draft_cost {r(6) - r(5)}] "
+          f"[search {r(12) - r(3)} build {r(6) - r(12)} wait-exact {r(8) - r(6)}] "
           f"| prep: start {r(15)} len {r(16)} walks {r(17)} scan {r(18)} rewalk {r(19)} draws {r(20)} "
           f"| sync {r(10)}..{r(11)}", flush=True)
 lib.ttdbg_mutate_probe(1)
