@@ -51,17 +51,52 @@ __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice 
   using namespace f64;
   __shared__ CandInfo<NSP, NRED> ci[G];
   __shared__ bool last;
+  // the sketch and device model copied to shared memory before the grid
+  // dependency wait: the staging reads them with per-lane indices, which in
+  // the parameter bank are constant-cache misses on the critical path
+  __shared__ DevSketch sk_s;
+  __shared__ DevDevice dd_s;
+  {
+    const uint32_t* a = reinterpret_cast<const uint32_t*>(&SK);
+    const uint32_t* b = reinterpret_cast<const uint32_t*>(&D);
+    for (int i = threadIdx.x; i < (int)(sizeof(DevSketch) / 4); i += blockDim.x) reinterpret_cast<uint32_t*>(&sk_s)[i] = a[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(DevDevice) / 4); i += blockDim.x) reinterpret_cast<uint32_t*>(&dd_s)[i] = b[i];
+    __syncthreads();
+  }
   const int S = 2 * SK.n_in + 2;
   const int B = SK.kind == TT_OP_ELEMENTWISE ? 1 : 3 * SK.n_in + 2;
   if (blockIdx.x == 0 && threadIdx.x == 0 && fin.record.base) g_vtl[g_vtl_n[0] & 63u][0] = gtimer64();
   pacm_h64_body(S, B, count_dev, k_max, params, score_out, [&](int64_t e0, int64_t count, double* MISC) {
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     for (int v = t; v < G * kMisc; v += T) MISC[v] = 0.0;  // padding rows, xb^T row 23, idle slots
-    if (warp == 0 && lane < G && e0 + lane < count) {
+    if (warp == 0) {  // candidate lane >> 3 of the G = 4, 8 lanes each
+      const int cc = lane >> 3, sub = lane & 7;
+      const bool have = e0 + cc < count;
       Factors<NSP, NRED> F;
-      feat_load<NSP, NRED>(SK, ref, e0 + lane, F);
+      if (ref.seeded) {
+        // a seeded schedule is rebuilt from its draws: each lane takes every
+        // 8th prime of the plan, and the 8 partial factor sets multiply
+        if (have) {
+          const uint64_t j = (uint64_t)ref.idx[e0 + cc];
+          H64_MARK(22, 0);
+          generate_part<NSP, NRED>(sk_s, ref.s0, j, sub, 8, F);
+          H64_MARK(23, 0);
+        } else {
+#pragma unroll
+          for (int q = 0; q < Factors<NSP, NRED>::kN; ++q) F.f[q] = 1;
+          F.unroll = 1;
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+#pragma unroll
+          for (int q = 0; q < Factors<NSP, NRED>::kN; ++q) F.f[q] *= __shfl_xor_sync(0xffffffffu, F.f[q], o);
+          F.unroll *= __shfl_xor_sync(0xffffffffu, F.unroll, o);
+        }
+      } else if (sub == 0 && have) {
+        feat_load<NSP, NRED>(sk_s, ref, e0 + cc, F);
+      }
       H64_MARK(19, 0);
-      cand_info<NSP, NRED>(SK, D, F, ci[lane]);
+      if (sub == 0 && have) cand_info<NSP, NRED>(sk_s, dd_s, F, ci[cc]);
       H64_MARK(20, 0);
     }
     __syncthreads();
@@ -73,7 +108,7 @@ __global__ void __launch_bounds__(f64::T, 1) k_verify64(DevSketch SK, DevDevice 
     if (warp < S + B && e0 + cc < count) {
       double v[TT_STMT_WIDTH];
       uint32_t lm;
-      feature_args<double, NSP, NRED>(SK, D, ci[cc], warp, v, &lm);
+      feature_args<double, NSP, NRED>(sk_s, dd_s, ci[cc], warp, v, &lm);
       double* m = MISC + cc * kMisc + (warp < S ? warp : 24 * 8 + (warp - S));
       const int width = warp < S ? TT_STMT_WIDTH : TT_BLOCK_WIDTH;
 #pragma unroll

@@ -250,7 +250,11 @@ __device__ __forceinline__ unsigned long long gtimer64() {
 }
 #define H64_MARK(i, who)                                                    \
   do {                                                                      \
-    if (blockIdx.x == 0 && t == (who) && e0 == 0) g_clk_h64[i] = clock64(); \
+    if (blockIdx.x == 0 && t == (who) && e0 == 0) {                         \
+      long long c_;                                                         \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)::"memory");          \
+      g_clk_h64[i] = c_;                                                    \
+    }                                                                       \
   } while (0)
 
 // The pass loop of the throughput kernel. Stage(e0, count, misc) fills, for

@@ -40,7 +40,7 @@ clk = (C.c_longlong * 24)()
 (L.ttdbg_verify64_clocks if fused else L.ttdbg_pacm64_h64_clocks)(clk, 24)
 c = np.array(clk[:24], dtype=np.int64)
 d = lambda a, b: int(c[b] - c[a])  # noqa: E731
-print(f"staging {d(0, 1)} (factors {d(0, 19)} cand_info {d(19, 20)} sync {d(0, 21)}) | wait W1|We {d(1, 2)} | phase 1 {d(2, 3)} sync {d(2, 4)}")
+print(f"staging {d(0, 1)} (index load {d(0, 22)} generate {d(22, 23)} combine {d(23, 19)} factors {d(0, 19)} cand_info {d(19, 20)} sync {d(0, 21)}) | wait W1|We {d(1, 2)} | phase 1 {d(2, 3)} sync {d(2, 4)}")
 print(f"wait WA {d(4, 5)} | phase 2: S2 {d(5, 6)} Q {d(5, 16)} K {d(5, 17)} V {d(5, 7)} sync {d(5, 8)}")
 print(f"phase 3: head1a wait Hw1 {d(8, 9)} chain {d(9, 10)} | logits+softmax {d(8, 11)} PV+pool {d(11, 12)} | sync {d(8, 13)}")
 print(f"phase 5: head1b {d(13, 14)} head2 {d(14, 15)}")
