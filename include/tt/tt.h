@@ -141,11 +141,13 @@ int tt_draft_set(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev
  * none excluded, b) — the drafted identities never leave the device between
  * the steps and one device->host read returns the picks. HOST outputs:
  * sel_idx[b] (indices into the draft set, in select_top order), sel_scores[b]
- * (nullable), *n_candidates = draft-set size. E_STATE when the set holds
- * fewer than b candidates (as tt_select_top). Synchronous. */
+ * and sel_identity[b] (nullable; the schedules to measure, decodable with
+ * tt_schedule_from_identity), *n_candidates = draft-set size. E_STATE when
+ * the set holds fewer than b candidates (as tt_select_top). Synchronous. */
 int tt_tuner_round(tt_ctx* ctx, const tt_sketch* sketch, const tt_device_spec* dev, int n_steps, int64_t draft_size,
                    int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int64_t b,
-                   int precision, int64_t* sel_idx, double* sel_scores, int64_t* n_candidates);
+                   int precision, int64_t* sel_idx, double* sel_scores, uint64_t* sel_identity,
+                   int64_t* n_candidates);
 /* Merge R rank-local top-k lists (C1's consumer): m entries of (cost,
  * global index, identity), global index < 0 = empty slot. Same semantics as
  * one explore over the union. Synchronous. */

@@ -87,6 +87,30 @@ std::vector<int64_t> B200Round::run(const TensorOpSpec& op, const DeviceSpec& de
   return idx;
 }
 
+std::vector<int64_t> B200Round::tuner_round(const TensorOpSpec& op, const DeviceSpec& dev,
+                                            const RankerParams& target, int n_steps, int draft_size, int pop_size,
+                                            double random_mix, uint64_t explore_seed, uint64_t mix_seed, int b,
+                                            std::vector<double>* scores, std::vector<uint64_t>* identities,
+                                            int64_t* n_candidates) {
+  tt_op_spec o = to_tt(op);
+  tt_sketch sk;
+  check(ctx_, tt_sketch_from_op(&o, 1, &sk));
+  tt_device_spec d = to_tt(dev);
+  check(ctx_, tt_validate_device(&d));
+  const auto params = flatten(target);
+  check(ctx_, tt_pacm_load(ctx_, params.data(), target.hidden));
+  std::vector<int64_t> idx(b);
+  std::vector<double> sc(b);
+  std::vector<uint64_t> id(b);
+  int64_t cnt = 0;
+  check(ctx_, tt_tuner_round(ctx_, &sk, &d, n_steps, draft_size, pop_size, random_mix, explore_seed, mix_seed, b,
+                             TT_PREC_FP64, idx.data(), sc.data(), id.data(), &cnt));
+  if (scores) *scores = sc;
+  if (identities) *identities = id;
+  if (n_candidates) *n_candidates = cnt;
+  return idx;
+}
+
 std::pair<double, double> B200Round::train(RankerParams& target, const std::vector<double>& stmt,
                                            const std::vector<double>& block, int n_stmt, int n_block,
                                            const std::vector<double>& latencies, const TrainConfig& cfg) {

@@ -40,6 +40,18 @@ class B200Round {
                            int draft_size, int b, uint64_t seed, std::vector<double>* scores = nullptr,
                            std::vector<uint64_t>* identities = nullptr);
 
+  // The tuner's round at its real shape (tuner.cpp:294-396): the draft set
+  // (explore(op, dev, n_steps, n_spec, pop_size, RngStream(explore_seed)) +
+  // the unseen schedules of random_init(., RngStream(mix_seed)), n_spec =
+  // max(1, llround((1 - random_mix) draft_size))), extract_features,
+  // score_batch and select_top(b) in one device call. Returns the indices of
+  // the picks into that draft set; scores / identities / set size optional.
+  std::vector<int64_t> tuner_round(const TensorOpSpec& op, const DeviceSpec& dev, const RankerParams& target,
+                                   int n_steps, int draft_size, int pop_size, double random_mix,
+                                   uint64_t explore_seed, uint64_t mix_seed, int b,
+                                   std::vector<double>* scores = nullptr,
+                                   std::vector<uint64_t>* identities = nullptr, int64_t* n_candidates = nullptr);
+
   // train(target, {task}, cfg) (ranker.cpp:459-512) on the device, in place
   // (features as host rows [n][S][24] / [n][B][23]); returns (initial, final) loss.
   std::pair<double, double> train(RankerParams& target, const std::vector<double>& stmt,

@@ -6,6 +6,8 @@
 // are identical and the trained parameters agree within 1e-11 relative.
 #include <cmath>
 #include <cstdio>
+#include <set>
+#include <string>
 
 #include "b200_shim.hpp"
 #include "tiletune/common.hpp"
@@ -61,6 +63,43 @@ int main() {
     const bool ok = same(pop[idx[e]], ex.drafted[sel[e]]) && std::fabs(sc[e] - scores[sel[e]]) <= 1e-12;
     std::printf("selection %zu: population %lld score %.17g | reference %.17g %s\n", e, (long long)idx[e], sc[e],
                 scores[sel[e]], ok ? "ok" : "MISMATCH");
+    fails += !ok;
+  }
+
+  // ---- the tuner's real round (GA draft set, tuner.cpp:294-323) through the
+  // shim vs the reference's own functions composed the same way
+  {
+    const int steps = 32, dsize = 512, pop = 512, bb = 10;
+    const double mix = 0.2;
+    const uint64_t es = 2000, ms = 2001;
+    int64_t n_spec = std::llround((1.0 - mix) * (double)dsize);
+    if (n_spec < 1) n_spec = 1;
+    RngStream erng(es);
+    ExploreResult gx = explore(op, dev, steps, (int)n_spec, pop, erng, {}, 8);
+    std::vector<Schedule> cands;
+    std::vector<double> drafts;
+    std::set<std::string> seen;
+    for (std::size_t i = 0; i < gx.drafted.size(); ++i)
+      if (seen.insert(schedule_key(gx.sketch, gx.drafted[i])).second)
+        cands.push_back(gx.drafted[i]), drafts.push_back(gx.draft_costs[i]);
+    RngStream mrng(ms);
+    for (auto& s : random_init(gx.sketch, dsize - n_spec, mrng))
+      if (seen.insert(schedule_key(gx.sketch, s)).second)
+        cands.push_back(s), drafts.push_back(draft_cost(gx.sketch, s, dev).total);
+    std::vector<HybridFeature> gf;
+    for (const auto& s : cands) gf.push_back(extract_features(gx.sketch, s, dev));
+    std::vector<double> gs = score_batch(target, gf, {}, 8);
+    std::vector<char> gexcl(gs.size(), 0);
+    auto gsel = select_top(gs, drafts, gexcl, bb);
+    std::vector<double> tsc;
+    int64_t tcnt = 0;
+    std::vector<int64_t> tsel = round.tuner_round(op, dev, target, steps, dsize, pop, mix, es, ms, bb, &tsc, nullptr,
+                                                  &tcnt);
+    bool ok = tcnt == (int64_t)cands.size() && tsel.size() == gsel.size();
+    for (std::size_t e = 0; ok && e < tsel.size(); ++e)
+      ok = tsel[e] == (int64_t)gsel[e] && std::fabs(tsc[e] - gs[gsel[e]]) <= 1e-12 * std::fabs(gs[gsel[e]]) + 1e-300;
+    std::printf("tuner round: %lld candidates (reference %zu), picks %s\n", (long long)tcnt, cands.size(),
+                ok ? "identical" : "MISMATCH");
     fails += !ok;
   }
 

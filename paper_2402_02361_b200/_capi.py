@@ -64,7 +64,7 @@ _SIGS = [
     ("tt_draft_set", C.c_int, [vp, P(Sketch), P(DeviceSpec), C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_uint64,
                                C.c_uint64, C.c_int, vp, vp, i64p, C.POINTER(C.c_uint64)]),
     ("tt_tuner_round", C.c_int, [vp, P(Sketch), P(DeviceSpec), C.c_int, C.c_int64, C.c_int64, C.c_double,
-                                 C.c_uint64, C.c_uint64, C.c_int64, C.c_int, vp, vp, i64p]),
+                                 C.c_uint64, C.c_uint64, C.c_int64, C.c_int, vp, vp, vp, i64p]),
     ("tt_topk_merge", C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int64, vp, vp, vp, i64p]),
     ("tt_features", C.c_int, [vp, P(Sketch), P(DeviceSpec), vp, C.c_int64, vp, vp]),
     ("tt_features_soa", C.c_int, [vp, P(Sketch), P(DeviceSpec), vp, C.c_int64, vp, C.c_int64, vp, vp]),

@@ -2116,7 +2116,8 @@ int tt_draft_set(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, in
 
 int tt_tuner_round(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, int n_steps, int64_t draft_size,
                    int64_t pop_size, double random_mix, uint64_t explore_seed, uint64_t mix_seed, int64_t b,
-                   int precision, int64_t* sel_idx, double* sel_scores, int64_t* n_candidates) {
+                   int precision, int64_t* sel_idx, double* sel_scores, uint64_t* sel_identity,
+                   int64_t* n_candidates) {
   if (!ctx) return TT_E_STATE;
   if (!sel_idx || !n_candidates) return fail(ctx, TT_E_STATE, "tuner_round: null output");
   if (b < 1) return fail(ctx, TT_E_STATE, "select_top: b must be >= 1");
@@ -2161,6 +2162,7 @@ int tt_tuner_round(tt_ctx* ctx, const tt_sketch* sk, const tt_device_spec* dev, 
   for (int64_t i = 0; i < b; ++i) {
     sel_idx[i] = h_pos[i];
     if (sel_scores) sel_scores[i] = h_score[h_pos[i]];
+    if (sel_identity) sel_identity[i] = h_id[h_pos[i]];
   }
   return TT_OK;
 }

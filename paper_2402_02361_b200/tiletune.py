@@ -201,14 +201,15 @@ def tuner_round(ctx: Context, sketch: Sketch, dev: DeviceSpec, n_steps: int, dra
     """One tuner round (tuner.cpp:294-396): the draft set, features + PaCM
     scores on the device, select_top(b). Needs a loaded PaCM (PaCM(ctx, ...)).
     Returns (picked indices into the draft set int64 [b], their scores
-    float64 [b], draft-set size)."""
+    float64 [b], their identities uint64 [b], draft-set size)."""
     sel = np.zeros(b, np.int64)
     sc = np.zeros(b, np.float64)
+    ids = np.zeros(b, np.uint64)
     cnt = C.c_int64(0)
     ctx.check(lib().tt_tuner_round(ctx.h, C.byref(sketch), C.byref(dev), n_steps, draft_size, pop_size, random_mix,
                                    explore_seed & (2**64 - 1), mix_seed & (2**64 - 1), b, precision,
-                                   sel.ctypes.data, sc.ctypes.data, C.byref(cnt)))
-    return sel, sc, cnt.value
+                                   sel.ctypes.data, sc.ctypes.data, ids.ctypes.data, C.byref(cnt)))
+    return sel, sc, ids, cnt.value
 
 
 def topk_merge(ctx: Context, cost: torch.Tensor, gidx: torch.Tensor, ids: torch.Tensor, k: int):
