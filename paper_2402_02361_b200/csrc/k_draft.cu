@@ -630,7 +630,19 @@ __global__ void __launch_bounds__(kFastThreads, 1)
   if (blockIdx.x == 0 && t == 0) g_sel_ns[1] = gtimer();
   // ---- B: the sample, every CTA
   const int ns = (int)((n + stride - 1) / stride);
-  for (int e = t; e < ns; e += blockDim.x) keys[e] = __ldcg(sample + e);
+  for (int e0 = t; e0 < ns; e0 += 8 * blockDim.x) {  // eight loads in flight, then the stores
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      v[u] = e < ns ? __ldcg(sample + e) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      if (e < ns) keys[e] = v[u];
+    }
+  }
   __syncthreads();
   const int lane = t & 31;
   int status = 0, attempt = 0, m = 0, uniq = 0;
@@ -646,16 +658,10 @@ __global__ void __launch_bounds__(kFastThreads, 1)
       for (int e = blockIdx.x * blockDim.x + t; e < kFastCap; e += gridDim.x * blockDim.x) rank_acc[e] = 0, dup[e] = 0;
     // ---- C: compact this CTA's chunk (its costs are still in L2)
     uint32_t* surv = &st->att_surv[attempt];
-    for (int64_t base = i_beg; base < i_end; base += blockDim.x) {
-      const int64_t i = base + t;
-      uint64_t key = 0;
-      bool keep = false;
-      if (i < i_end) {
-        key = cost_key(__ldcg(cost + i));
-        keep = key <= thr;
-      }
+    auto visit = [&](int64_t i, uint64_t key) {  // warp-uniform call
+      const bool keep = i < i_end && key <= thr;
       const unsigned msk = __ballot_sync(0xffffffffu, keep);
-      if (!msk) continue;
+      if (!msk) return;
       uint32_t pos0 = 0;
       if (lane == 0) pos0 = atomicAdd(surv, (uint32_t)__popc(msk));
       pos0 = __shfl_sync(0xffffffffu, pos0, 0);
@@ -667,6 +673,27 @@ __global__ void __launch_bounds__(kFastThreads, 1)
           skey[p] = key, sidx[p] = i;
           sfp[p] = SEED ? id : fingerprint<NSP, NRED>(F);
         }
+      }
+    };
+    if (n <= ((int64_t)6 << 20)) {  // the cost array (<= 48 MB) is still in L2 from K1
+      for (int64_t base = i_beg; base < i_end; base += blockDim.x) {
+        const int64_t i = base + t;
+        visit(i, i < i_end ? cost_key(__ldcg(cost + i)) : 0ull);
+      }
+    } else {
+      // larger cost arrays stream from HBM: kCompactU cost loads in flight per
+      // thread (one load per round trip is latency bound); survivor positions
+      // come from an atomic, so the scan order does not matter
+      constexpr int kCompactU = 8;
+      for (int64_t base = i_beg; base < i_end; base += (int64_t)kCompactU * blockDim.x) {
+        uint64_t kv[kCompactU];
+#pragma unroll
+        for (int u = 0; u < kCompactU; ++u) {
+          const int64_t i = base + (int64_t)u * blockDim.x + t;
+          kv[u] = i < i_end ? cost_key(__ldcg(cost + i)) : 0ull;
+        }
+#pragma unroll 1
+        for (int u = 0; u < kCompactU; ++u) visit(base + (int64_t)u * blockDim.x + t, kv[u]);
       }
     }
     grid_barrier(attempt == 0 ? 1 : -1);
