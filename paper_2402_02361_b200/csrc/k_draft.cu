@@ -46,6 +46,8 @@ constexpr int kFastCap = 8192;               // survivors the fast path ranks
 constexpr int kSampleMin = 4096;             // sampled cost keys (top 32 bits) for the threshold
 constexpr int kSampleMax = 32768;
 constexpr int64_t kFastMaxN = int64_t{16} << 20;  // fast path population limit
+constexpr int kL2TabMax = kSampleMax * 4 / 8;      // p_l2_m table entries (overlays the sample)
+constexpr int64_t kL2TabMinChunk = 4 * 1024;         // candidates per CTA that amortise filling it
 
 static int grid_for(int64_t n, int threads, int max_blocks) {
   int64_t g = (n + threads - 1) / threads;
@@ -615,11 +617,23 @@ __global__ void __launch_bounds__(kFastThreads, 1)
   const int64_t i_beg = blockIdx.x * chunk;
   const int64_t i_end = i_beg + chunk < n ? i_beg + chunk : n;
   bool bad = false;
+  // large chunks: p_l2_m from a table in the (not yet used) sample region
+  // instead of three divisions per GEMM candidate; the sample overwrites it
+  // after the grid barrier
+  double* l2tab = (double*)smem;
+  int n_tab = 0;
+  if (i_end - i_beg >= kL2TabMinChunk) {
+    int64_t mx = 0;
+    for (int a = 0; a < S.n_axes; ++a) mx = S.extent[a] > mx ? S.extent[a] : mx;
+    n_tab = (int)(mx + 1 < kL2TabMax ? mx + 1 : kL2TabMax);
+    l2m_table_fill(l2tab, n_tab, D);
+    __syncthreads();
+  }
   for (int64_t i = i_beg + t; i < i_end; i += blockDim.x) {
     Factors<NSP, NRED> F;
     load_cand<NSP, NRED, SEED>(S, src, i, F, false);
     if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
-    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles);
+    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles, l2tab, n_tab);
     cost[i] = c;
     if ((i & (stride - 1)) == 0) sample[i / stride] = (uint32_t)(cost_key(c) >> 32);
   }

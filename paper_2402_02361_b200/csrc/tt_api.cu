@@ -376,6 +376,8 @@ int compile_device(tt_ctx* ctx, const tt_device_spec* d, DevDevice& D) {
   D.pu_l2 = d->pu_l2, D.n_l2 = d->n_l2, D.t_p = d->t_p, D.t_m = d->t_m;
   D.log2_nl1 = log2i(d->n_l1), D.log2_nl2 = log2i(d->n_l2);
   D.pu_l1_n_l1 = d->pu_l1 * d->n_l1;
+  D.pu_l1_magic = d->pu_l1 > 1 ? UINT64_MAX / (uint64_t)d->pu_l1 + 1 : 0;
+  D.pu_l2_magic = d->pu_l2 > 1 ? UINT64_MAX / (uint64_t)d->pu_l2 + 1 : 0;
   return TT_OK;
 }
 
