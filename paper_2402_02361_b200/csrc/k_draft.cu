@@ -23,6 +23,7 @@
 // a duplicate group; selection is exact for any input.
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -586,7 +587,7 @@ __device__ __forceinline__ bool same_schedule(const DevSketch& S, const Src& src
   return same;
 }
 
-template <int NSP, int NRED, bool SEED, bool WITH_ID>
+template <int NSP, int NRED, bool SEED, bool WITH_ID, bool U32 = false>
 __global__ void __launch_bounds__(kFastThreads, 1)
     k_fsel(DevSketch S, DevDevice D, Src src, int64_t n, int toggles, int64_t k, int64_t need,
            double* __restrict__ cost, uint32_t* __restrict__ sample, SelState* __restrict__ st,
@@ -633,7 +634,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     Factors<NSP, NRED> F;
     load_cand<NSP, NRED, SEED>(S, src, i, F, false);
     if constexpr (!SEED) bad |= !valid_factors<NSP, NRED>(S, F);
-    const double c = draft_cost_of<NSP, NRED>(S, D, F, toggles, l2tab, n_tab);
+    const double c = draft_cost_of<NSP, NRED, false, std::conditional_t<U32, uint32_t, int64_t>>(S, D, F, toggles,
+                                                                                                   l2tab, n_tab);
     cost[i] = c;
     if ((i & (stride - 1)) == 0) sample[i / stride] = (uint32_t)(cost_key(c) >> 32);
   }
@@ -813,6 +815,23 @@ __global__ void __launch_bounds__(kFastThreads, 1)
 
 static int g_num_sms = 0;
 
+// Every product / sum of tile extents draft_cost forms fits in 32 bits:
+// buffer footprints, s2, s5, s4, s6 are each <= the product P of all
+// extents (a factor's tile extents multiply to at most its axis extent), s1
+// and s3 are sums of <= n_in + 1 of them, and the round-ups add < pu / n.
+// Then K1 runs its integer math in uint32 (one IMAD per product instead of
+// three). Invalid explicit schedules (E_VALIDATE) may wrap; they fail anyway.
+static bool fits_u32(const DevSketch& S, const DevDevice& D) {
+  unsigned __int128 p = 1;
+  for (int a = 0; a < S.n_axes; ++a) {
+    p *= (unsigned __int128)(S.extent[a] > 0 ? S.extent[a] : 1);
+    if (p >> 40) return false;
+  }
+  const unsigned __int128 lim = p * (unsigned __int128)(S.n_in + 1) + (unsigned __int128)D.n_l1 +
+                                (unsigned __int128)D.pu_l1 + (unsigned __int128)D.pu_l2 + (unsigned __int128)D.n_l2;
+  return lim < ((unsigned __int128)1 << 32) && (unsigned __int128)S.red_total <= p;
+}
+
 template <int NSP, int NRED, bool SEED>
 static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,
                      int64_t need, SelScratch& w, int64_t* out_idx, double* out_cost, uint64_t* out_id,
@@ -826,6 +845,7 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   static bool init = false;
   if (!init) {
     set_smem(k_fsel<NSP, NRED, SEED, true>, smem), set_smem(k_fsel<NSP, NRED, SEED, false>, smem);
+    set_smem(k_fsel<NSP, NRED, SEED, false, true>, smem);
     init = true;
   }
   // one CTA per SM (co-resident: a cooperative launch), >= 64 candidates each
@@ -841,6 +861,10 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   if (out_id)
     cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, true>, S, D, src, n, toggles, k, need, w.cost, w.sample, w.state,
                        w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id, out_count);
+  else if (fits_u32(S, D))
+    cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, false, true>, S, D, src, n, toggles, k, need, w.cost, w.sample,
+                       w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id,
+                       out_count);
   else
     cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, false>, S, D, src, n, toggles, k, need, w.cost, w.sample,
                        w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id,
