@@ -821,7 +821,11 @@ static int g_num_sms = 0;
 // and s3 are sums of <= n_in + 1 of them, and the round-ups add < pu / n.
 // Then K1 runs its integer math in uint32 (one IMAD per product instead of
 // three). Invalid explicit schedules (E_VALIDATE) may wrap; they fail anyway.
+// The same mode divides with ddiv_inrange, whose range needs t_p and t_m
+// within 2^+-300 (every other operand is then within 2^+-470).
 static bool fits_u32(const DevSketch& S, const DevDevice& D) {
+  const double lo = 0x1p-300, hi = 0x1p300;
+  if (!(D.t_p >= lo && D.t_p <= hi && D.t_m >= lo && D.t_m <= hi)) return false;
   unsigned __int128 p = 1;
   for (int a = 0; a < S.n_axes; ++a) {
     p *= (unsigned __int128)(S.extent[a] > 0 ? S.extent[a] : 1);
@@ -1295,4 +1299,47 @@ extern "C" int ttdbg_select_timeline(unsigned long long* out, unsigned* n) {
 }
 extern "C" int ttdbg_select_clocks(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, tt::g_sel_ns, sizeof(unsigned long long) * (n < 24 ? n : 24));
+}
+
+// ttdbg_div_check (tests/test_gpu_parity.py): ddiv_inrange against
+// __ddiv_rn over n pseudo-random operand pairs per kind — 0: integers in
+// [1, 2^32), 1: an integer over a double in [2^-400, 2^400] (the draft
+// cost's s5 / u_m shape), 2: both doubles in [2^-400, 2^400], 3: integers
+// whose quotient is near 1 (round-up ratios). Returns the mismatch count
+// (0 expected), or -1 on a CUDA error.
+namespace tt {
+__global__ void k_div_check(int64_t n, uint64_t seed, unsigned long long* bad) {
+  unsigned long long my = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = scramble64(seed + 2 * (uint64_t)i * kGolden), y = scramble64(seed + (2 * (uint64_t)i + 1) * kGolden);
+    const auto dbl = [](uint64_t r) {  // exponent in [-400, 400], random mantissa
+      const int e = (int)((r >> 52) % 801) - 400;
+      return __longlong_as_double((long long)(((uint64_t)(e + 1023) << 52) | (r & ((1ull << 52) - 1))));
+    };
+    double a, b;
+    switch (i & 3) {
+      case 0: a = (double)((x >> 32) | 1), b = (double)((y >> 32) | 1); break;
+      case 1: a = (double)((x >> 32) | 1), b = dbl(y); break;
+      case 2: a = dbl(x), b = dbl(y); break;
+      default: {
+        const uint32_t s = (uint32_t)(x >> 33) | 1u, d = (uint32_t)(y % 64) + 1;
+        a = (double)s, b = (double)((s + d - 1) / d * d);
+      }
+    }
+    const double f = ddiv_inrange(a, b), r = __ddiv_rn(a, b);
+    my += __double_as_longlong(f) != __double_as_longlong(r);
+  }
+  if (my) atomicAdd(bad, my);
+}
+}  // namespace tt
+
+extern "C" long long ttdbg_div_check(long long n, unsigned long long seed) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return -1;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  tt::k_div_check<<<148 * 8, 256>>>(n, seed, d);
+  unsigned long long h = 0;
+  const cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? (long long)h : -1;
 }
