@@ -815,26 +815,6 @@ __global__ void __launch_bounds__(kFastThreads, 1)
 
 static int g_num_sms = 0;
 
-// Every product / sum of tile extents draft_cost forms fits in 32 bits:
-// buffer footprints, s2, s5, s4, s6 are each <= the product P of all
-// extents (a factor's tile extents multiply to at most its axis extent), s1
-// and s3 are sums of <= n_in + 1 of them, and the round-ups add < pu / n.
-// Then K1 runs its integer math in uint32 (one IMAD per product instead of
-// three). Invalid explicit schedules (E_VALIDATE) may wrap; they fail anyway.
-// The same mode divides with ddiv_inrange, whose range needs t_p and t_m
-// within 2^+-300 (every other operand is then within 2^+-470).
-static bool fits_u32(const DevSketch& S, const DevDevice& D) {
-  const double lo = 0x1p-300, hi = 0x1p300;
-  if (!(D.t_p >= lo && D.t_p <= hi && D.t_m >= lo && D.t_m <= hi)) return false;
-  unsigned __int128 p = 1;
-  for (int a = 0; a < S.n_axes; ++a) {
-    p *= (unsigned __int128)(S.extent[a] > 0 ? S.extent[a] : 1);
-    if (p >> 40) return false;
-  }
-  const unsigned __int128 lim = p * (unsigned __int128)(S.n_in + 1) + (unsigned __int128)D.n_l1 +
-                                (unsigned __int128)D.pu_l1 + (unsigned __int128)D.pu_l2 + (unsigned __int128)D.n_l2;
-  return lim < ((unsigned __int128)1 << 32) && (unsigned __int128)S.red_total <= p;
-}
 
 template <int NSP, int NRED, bool SEED>
 static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int64_t n, int toggles, int64_t k,

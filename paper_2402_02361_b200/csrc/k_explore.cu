@@ -27,6 +27,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "tt_kernels.h"
 
 namespace tt {
@@ -269,7 +271,7 @@ constexpr uint64_t kMapIdentity = (uint64_t)1 << 30 | (uint64_t)2 << 46 | (uint6
 //                        (segment walks per entry, a warp scan of the
 //                        segment maps, re-walks) and every child's draws;
 //   publish (warp 15)    the previous generation's host copy and flag.
-template <int NSP, int NRED>
+template <int NSP, int NRED, bool U32 = false>
 __global__ void __launch_bounds__(kMutThreads, 1)
     k_explore_gens(DevSketch S, DevDevice D, int toggles, int n, int n_steps, GenOut dv, uint64_t s_init, GenOut h,
                    volatile uint32_t* flags, int mode) {
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
     for (int j = jlo + tid; j < jhi; j += kMain) {
       Factors<NSP, NRED> F;
       load_factors_cg<NSP, NRED>(d0.soa, n, j, F);
-      emit<NSP, NRED>(n, d0, j, F, draft_cost_of<NSP, NRED>(S, D, F, toggles), d0.id[j], false);
+      emit<NSP, NRED>(n, d0, j, F, draft_cost_of<NSP, NRED, false, std::conditional_t<U32, uint32_t, int64_t>>(S, D, F, toggles), d0.id[j], false);
     }
   } else if (tid < kWork && n_steps > 1) {
     s_prep = prep(s_prep, 1, false);
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
           }
 #pragma unroll
           for (int q = 0; q < kN; ++q) F.f[q] = q == c_from ? (int32_t)v_from : q == c_to ? (int32_t)v_to : F.f[q];
-          return draft_cost_of<NSP, NRED, true>(S, D, F, toggles);
+          return draft_cost_of<NSP, NRED, true, std::conditional_t<U32, uint32_t, int64_t>>(S, D, F, toggles);
         };
         bool exact = !spec;  // past barrier 4: the exact wheel is in cum / s_total
         if (exact) named_barrier(4, kMain);
@@ -662,6 +664,7 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
     static bool init = false;
     if (!init) {
       cudaFuncSetAttribute(k_explore_gens<NSP, NRED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+      cudaFuncSetAttribute(k_explore_gens<NSP, NRED, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
       init = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -674,8 +677,14 @@ int launch_explore_gens(const DevSketch& S, const DevDevice& D, int toggles, int
     at[0].val.clusterDim.x = explore_cluster_size(n), at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
     cfg.attrs = at, cfg.numAttrs = 1;
     tt::note_launch();
-    err = cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, dv, s_init, h, flags,
-                             mode);
+    // the 32-bit draft-cost mode (uint32 products, branch-free divisions)
+    // when the sketch and device allow it, as in the round's selector
+    if (fits_u32(S, D))
+      err = cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED, true>, S, D, toggles, (int)n, n_steps, dv, s_init, h,
+                               flags, mode);
+    else
+      err = cudaLaunchKernelEx(&cfg, k_explore_gens<NSP, NRED>, S, D, toggles, (int)n, n_steps, dv, s_init, h, flags,
+                               mode);
   }));
   return rc ? rc : (err != cudaSuccess ? 2 : 0);
 }
