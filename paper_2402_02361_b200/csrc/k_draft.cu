@@ -776,6 +776,13 @@ __global__ void __launch_bounds__(kFastThreads, 1)
   // duplicates ranked below it (a bitmap over ranks, prefix popcounts).
   if (blockIdx.x > 0 && (int64_t)blockIdx.x * blockDim.x >= m) return;
   if (blockIdx.x == 0 && t == 0) g_sel_ns[16] = gtimer();
+  // this thread's survivor, loaded up front (its L2 round trips overlap the
+  // duplicate bitmap and the scan instead of following them)
+  const int e = blockIdx.x * blockDim.x + t;
+  int e_dup = 1, e_rank = 0;
+  int64_t e_idx = 0;
+  uint64_t e_key = 0;
+  if (e < m) e_dup = __ldcg(dup + e), e_rank = __ldcg(rank_acc + e), e_idx = __ldcg(sidx + e), e_key = __ldcg(skey + e);
   for (int w = t; w < kFastCap / 32; w += blockDim.x) dmask[w] = 0;
   __syncthreads();
   for (int e = t; e < m; e += blockDim.x)
@@ -790,14 +797,13 @@ __global__ void __launch_bounds__(kFastThreads, 1)
   block_exclusive_scan(dcnt, dpre, kFastCap / 32, wt);
   __syncthreads();
   if (blockIdx.x == 0 && t == 0) g_sel_ns[18] = gtimer();
-  const int e = blockIdx.x * blockDim.x + t;
-  if (e < m && !__ldcg(dup + e)) {
-    const int r = __ldcg(rank_acc + e);
+  if (e < m && !e_dup) {
+    const int r = e_rank;
     const int o = r - (dpre[r >> 5] + __popc(dmask[r >> 5] & ((1u << (r & 31)) - 1u)));
     if (o < k) {
-      const int64_t i = __ldcg(sidx + e);
+      const int64_t i = e_idx;
       out_idx[o] = i + src.index_base;
-      out_cost[o] = key_cost(__ldcg(skey + e));
+      out_cost[o] = key_cost(e_key);
       if constexpr (WITH_ID) out_id[o] = SEED ? __ldcg(sfp + e) : identity_at<NSP, NRED, SEED>(S, src, i);
     }
   }

@@ -4,7 +4,7 @@ twice, for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
     compute-sanitizer --tool racecheck python tools/sanitize_run.py [part]
 
 parts: round (seeded + explicit, fp64 + bf16-certified, n above and below
-the one-CTA selector), explore (GA cluster kernel + draft set), train (device
+the one-CTA selector), bigchunk (a 700K round: the selector's table path), explore (GA cluster kernel + draft set), train (device
 training + momentum), oracle, sharded (local draft + merge + merged verify),
 select (select_top + features + scoring). Default: all. Sizes are small so a
 racecheck pass finishes in minutes; each part checks its own results against
@@ -20,7 +20,7 @@ from paper_2402_02361_b200 import tiletune as tt  # noqa: E402
 from paper_2402_02361_b200.types import (TAG_INIT, WORKLOADS, derive_seed, make_sketch,  # noqa: E402
                                          make_gemm, oracle_b, reference_device)
 
-parts = sys.argv[1:] or ["round", "explore", "train", "oracle", "sharded", "select"]
+parts = sys.argv[1:] or ["round", "bigchunk", "explore", "train", "oracle", "sharded", "select"]
 ctx = tt.Context(0)
 dev = reference_device()
 params = tt.init_params(64, derive_seed(42, TAG_INIT))
@@ -35,6 +35,18 @@ if "round" in parts:
             b = tt.draft_verify_round(ctx, sk, dev, n, 256, 10, soa=soa, precision=prec)
             assert (a.index == b.index).all(), (name, prec)
         print("round", name, n, a.index.tolist(), flush=True)
+
+if "bigchunk" in parts:
+    # >= 4,096 candidates per CTA: the selector's p_l2_m table (filled in the
+    # sample region, overwritten by the sample after the grid barrier) and
+    # the 32-bit draft-cost mode
+    sk = make_sketch(WORKLOADS["gemm1024"]())
+    n = 700_000
+    soa = tt.random_init(ctx, sk, n, 5)
+    a = tt.draft_verify_round(ctx, sk, dev, n, 512, 10, seed=5)
+    b = tt.draft_verify_round(ctx, sk, dev, n, 512, 10, soa=soa)
+    assert (a.index == b.index).all()
+    print("bigchunk", n, a.index.tolist(), flush=True)
 
 if "explore" in parts:
     sk = make_sketch(WORKLOADS["gemm1024"]())
