@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kMutThreads, 1)
           }
 #pragma unroll
           for (int q = 0; q < kN; ++q) F.f[q] = q == c_from ? (int32_t)v_from : q == c_to ? (int32_t)v_to : F.f[q];
-          return draft_cost_of<NSP, NRED, true, std::conditional_t<U32, uint32_t, int64_t>>(S, D, F, toggles);
+          return draft_cost_of<NSP, NRED, !U32, std::conditional_t<U32, uint32_t, int64_t>>(S, D, F, toggles);
         };
         bool exact = !spec;  // past barrier 4: the exact wheel is in cum / s_total
         if (exact) named_barrier(4, kMain);
