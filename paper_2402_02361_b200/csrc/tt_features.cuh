@@ -35,7 +35,7 @@ template <typename R>
 __device__ __forceinline__ R rdiv(R a, R b);
 template <>
 __device__ __forceinline__ double rdiv<double>(double a, double b) {
-  return __ddiv_rn(a, b);
+  return ddiv_inrange(a, b);  // ratios of counts: integers in [0, 2^63], divisors >= 1
 }
 template <>
 __device__ __forceinline__ float rdiv<float>(float a, float b) {
