@@ -113,3 +113,22 @@ def test_struct_layouts_match_header():
     want = [C.sizeof(DeviceSpec), C.sizeof(make_gemm(1, 1, 1)), C.sizeof(Sketch), C.sizeof(_capi.RoundConfig),
             C.sizeof(_capi.RoundResult)]
     assert got == want
+
+
+def test_magic_round_up_is_exact():
+    """The L1/L2 round-ups of the 32-bit draft-cost mode (tt_device.cuh
+    ceil_div_magic): q = umulhi(floor((2^64 - 1) / b) + 1, a) is floor(a / b)
+    for every a < 2^32 and b < 2^32 (Lemire, Kaser, Kurz 2019), and
+    q + (q * b != a) the round-up draft.cpp:108-127 takes with int64
+    division. Checked here on the formula: every b up to 4,096 and random
+    large b, against exact integer arithmetic at the edges and on random a."""
+    import random
+    rnd = random.Random(7)
+    bs = list(range(2, 4097)) + [rnd.randrange(4097, 1 << 32) for _ in range(2000)] + [(1 << 32) - 1]
+    for b in bs:
+        m = (2 ** 64 - 1) // b + 1
+        for a in [0, 1, b - 1, b, b + 1, (1 << 32) - 1, (1 << 32) - b, ((1 << 32) - 1) // b * b] + \
+                 [rnd.randrange(0, 1 << 32) for _ in range(8)]:
+            q = (m * a) >> 64
+            assert q == a // b
+            assert q + (q * b != a) == -(-a // b)
