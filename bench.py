@@ -580,15 +580,16 @@ def roofline(args, sketches, stage_ms, rounds, peaks, peaks_kind, prec):
                                   "traffic": traffic.get("k_pacm_tc"), "flop_per_candidate": FLOP_PER_CAND,
                                   "ms": ms, "peak_source": peaks_kind + " bf16 dense (burst)"}
         else:
-            # CUDA-core fp64, no FMA contraction (bit-exact sums): 64 DMUL/DADD lanes/clk/SM measured
-            # (tools/fp64_bench.cu) -> each multiply-add costs 2 lane-ops
-            peak = 64 * 148 * sm_mhz * 1e6 / 1e12
+            # CUDA-core fp64: 64 fp64 lanes/clk/SM measured (tools/fp64_bench.cu); the dense layers
+            # use DFMA (2 FLOP per lane-op), so the peak is the FMA rate
+            peak = 2 * 64 * 148 * sm_mhz * 1e6 / 1e12
             out["pacm_kernel"] = {"bound": "fp64",
                                   "kernel": "k_verify64 (drafted-set features + fp64 PaCM on CUDA cores in the "
-                                            "reference's order + the round's finish; PaCM FLOPs counted)",
+                                            "reference's order, DFMA dense layers, + the round's finish; "
+                                            "PaCM FLOPs counted)",
                                   "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                                   "traffic": traffic.get("k_verify64"), "flop_per_candidate": FLOP_PER_CAND,
-                                  "ms": ms, "peak_source": "measured fp64 lane rate x 148 SMs x max SM clock"}
+                                  "ms": ms, "peak_source": "measured fp64 lane rate x 2 (FMA) x 148 SMs x max SM clock"}
     if not out:
         return None
     dom = max(out, key=lambda k: out[k]["ms"])
