@@ -182,20 +182,20 @@ __device__ __forceinline__ void tile8x2(const double* __restrict__ xt, const dou
   store8(a[1], __ldg(b + j + 32), act, rows, yt, j + 32);
 }
 
-// acc + sum_{f<64} x[f * sx] * w[f * sw], f ascending: one dependent DADD
-// chain (the reference's order). The products of each half are formed first
-// (independent multiplies, their loads in flight together), then chained:
-// ~12 cycles per step, against ~25 when each step's operands are loaded in
+// acc + sum_{f<64} x[f * sx] * w[f * sw], f ascending: one dependent DFMA
+// chain (the reference's order, fused like chains8). Each half's operands are
+// loaded first (their loads in flight together), then chained: one pipe
+// step per term, against ~25 cycles when each step's operands are loaded in
 // front of it (tools/chain_bench.cu).
 static __device__ __noinline__ double chain64(double acc, const double* __restrict__ x, int sx,
                                           const double* __restrict__ w, int sw) {
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
-    double p[32];
+    double xv[32], wv[32];
 #pragma unroll
-    for (int v = 0; v < 32; ++v) p[v] = __dmul_rn(x[(32 * hf + v) * sx], w[(32 * hf + v) * sw]);
+    for (int v = 0; v < 32; ++v) xv[v] = x[(32 * hf + v) * sx], wv[v] = w[(32 * hf + v) * sw];
 #pragma unroll
-    for (int v = 0; v < 32; ++v) acc = __dadd_rn(acc, p[v]);
+    for (int v = 0; v < 32; ++v) acc = __fma_rn(xv[v], wv[v], acc);  // fused, as in chains8
   }
   return acc;
 }
@@ -438,8 +438,8 @@ __device__ __forceinline__ void pacm_h64_body(int S, int B, const int64_t* __res
           double a = 0.0;
 #pragma unroll
           for (int r = 0; r < 8; ++r)
-            if (r < B) a = __dadd_rn(a, __dmul_rn(mh[ii * 8 + r], vr[r]));
-          pool = __dadd_rn(pool, __dmul_rn(a, inv_n));
+            if (r < B) a = __fma_rn(mh[ii * 8 + r], vr[r], a);
+          pool = __fma_rn(a, inv_n, pool);
         }
         mh[64 + H + jh] = pool;
       }
