@@ -835,7 +835,7 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   static bool init = false;
   if (!init) {
     set_smem(k_fsel<NSP, NRED, SEED, true>, smem), set_smem(k_fsel<NSP, NRED, SEED, false>, smem);
-    set_smem(k_fsel<NSP, NRED, SEED, false, true>, smem);
+    set_smem(k_fsel<NSP, NRED, SEED, false, true>, smem), set_smem(k_fsel<NSP, NRED, SEED, true, true>, smem);
     init = true;
   }
   // one CTA per SM (co-resident: a cooperative launch), >= 64 candidates each
@@ -848,10 +848,15 @@ static void run_fast(const DevSketch& S, const DevDevice& D, const Src& src, int
   cfg.attrs = &attr, cfg.numAttrs = 1;
   if (w.k1_ev[0]) cudaEventRecord(w.k1_ev[0], st);
   tt::note_launch();
-  if (out_id)
+  const bool u32 = fits_u32(S, D);
+  if (out_id && u32)
+    cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, true, true>, S, D, src, n, toggles, k, need, w.cost, w.sample,
+                       w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id,
+                       out_count);
+  else if (out_id)
     cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, true>, S, D, src, n, toggles, k, need, w.cost, w.sample, w.state,
                        w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id, out_count);
-  else if (fits_u32(S, D))
+  else if (u32)
     cudaLaunchKernelEx(&cfg, k_fsel<NSP, NRED, SEED, false, true>, S, D, src, n, toggles, k, need, w.cost, w.sample,
                        w.state, w.skey, w.sidx, w.sfp, w.rank, w.dup, w.invalid, out_idx, out_cost, out_id,
                        out_count);
